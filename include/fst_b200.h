@@ -1,0 +1,181 @@
+/*
+ * fst_b200.h — C-ABI of the B200-native thresholded-Ax hot path
+ * (arXiv 2105.05879; reference: /root/reference/proj/include/fst).
+ *
+ * Plain pointers and sizes only; no torch, no Eigen, no C++ types. Every entry
+ * point names the reference interface it replaces (file:line, relative to
+ * /root/reference/proj/include/fst/). The C++ mirror of the reference API
+ * (`fst_b200.hpp`) and the Python mirror (`paper_2105_05879_b200/fst.py`) sit
+ * on top of this header; INTEGRATION.md shows the binding a reference
+ * maintainer would add.
+ *
+ * Residency: every `const void* X` / output pointer may be HOST or DEVICE
+ * memory (detected with cudaPointerGetAttributes). Host buffers are staged
+ * through pinned memory in chunks overlapped with compute (the end-to-end
+ * path); device buffers are used in place.
+ *
+ * Errors: every function returns an fstg_status; the message of the last
+ * failure on the calling thread is returned by fstg_last_error(). There is no
+ * CPU fallback: without a usable sm_100 device the compute entry points fail
+ * with FSTG_ERR_CUDA.
+ */
+#ifndef FST_B200_H_
+#define FST_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FSTG_ABI_VERSION 1
+
+/* Status codes map 1:1 onto the reference's exception classes. */
+typedef enum fstg_status {
+  FSTG_OK = 0,
+  FSTG_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument (stream.hpp:30-38, sketch.hpp:152-153) */
+  FSTG_ERR_OUT_OF_RANGE = 2,     /* std::out_of_range (sketch.hpp:115, kerdock.hpp:122) */
+  FSTG_ERR_OVERFLOW = 3,         /* std::overflow_error (stream.hpp:340-341) */
+  FSTG_ERR_RUNTIME = 4,          /* std::runtime_error: allocation (sketch.hpp:162-165) */
+  FSTG_ERR_CUDA = 5,             /* CUDA runtime failure / no sm_100 device */
+  FSTG_ERR_NOT_SUPPORTED = 6     /* shape outside this build's GPU limits */
+} fstg_status;
+
+typedef enum fstg_dtype { FSTG_F32 = 0, FSTG_F64 = 1 } fstg_dtype;
+
+/* Arithmetic mode of the streaming estimator.
+ *  FAST   : warp-parallel sample coefficients, FMA accumulation (fp32 default).
+ *  STRICT : the reference's exact operation order — Gray-code sequential
+ *           coefficient sums (stream.hpp:89-103), separately rounded
+ *           multiply/add in j order (stream.hpp:232-234); bit-identical
+ *           estimator and candidate set to the reference arithmetic (fp64
+ *           default). */
+typedef enum fstg_mode { FSTG_MODE_DEFAULT = 0, FSTG_MODE_FAST = 1, FSTG_MODE_STRICT = 2 } fstg_mode;
+
+/* Mirrors fst::StreamParams (stream.hpp:22-39); `seed` is the per-call seed. */
+typedef struct fstg_stream_params {
+  double epsilon;
+  double delta;
+  int64_t s;
+  int64_t J;
+  int64_t K;
+  int64_t widen;
+  uint64_t seed;
+  int32_t mode; /* fstg_mode */
+  int32_t reserved;
+} fstg_stream_params;
+
+typedef struct fstg_sketch fstg_sketch; /* opaque; owns device buffers; immutable after create */
+
+typedef struct fstg_sketch_info {
+  int64_t m, n, d, L;         /* sketch.hpp:98-102 */
+  int32_t k;
+  int32_t dtype;              /* fstg_dtype */
+  double row_norm_max;        /* sketch.hpp:105 */
+  int32_t device;
+  int32_t reserved;
+  int64_t column_stride;      /* elements between consecutive columns (>= m, 16-byte multiple) */
+  uint64_t device_bytes;      /* total HBM held by the sketch */
+  double preprocess_ms;       /* device time of the last preprocess, CUDA events */
+} fstg_sketch_info;
+
+/* ---------------------------------------------------------------- misc ---- */
+const char* fstg_last_error(void);
+const char* fstg_version(void);
+/* Number of usable sm_100 devices (0 when none; never falls back to CPU). */
+int fstg_device_count(int* count);
+
+/* ------------------------------------------- host-side design parameters -- */
+/* sketch.hpp:58-63 even_log2_ceil */
+int fstg_even_log2_ceil(int64_t n, int* k);
+/* kerdock.hpp:26-31 DesignParams::make -> d, L */
+int fstg_design_params(int k, int64_t* d, int64_t* L);
+/* kerdock.hpp:55-84 kerdock_matrix: k rows, bit j of row i = entry (i,j) */
+int fstg_kerdock_matrix(int k, uint64_t s, uint64_t* rows);
+/* stream.hpp:58-69 choose_params */
+int fstg_choose_params(double row_norm_max, double gamma, double eta, int64_t m, int64_t* J, int64_t* K);
+/* stream.hpp:30-38 StreamParams::validate */
+int fstg_validate_params(const fstg_stream_params* p);
+/* stream.hpp:245-246 candidate count `want` */
+int64_t fstg_candidate_count(int64_t s, int64_t widen, int64_t m);
+
+/* ------------------------------------------------------- preprocessing ---- */
+/* Replaces fst::preprocess (sketch.hpp:149-211). `a` is m x n row-major of
+ * `dtype` (host or device). The sketch {A s_l}, column-major m x L, is built in
+ * HBM on `device` by the in-shared-memory FWHT kernels; the embedded A is
+ * kept for refinement. `stream` may be NULL (library stream). */
+int fstg_preprocess(const void* a, int dtype, int64_t m, int64_t n, int device, void* stream,
+                    fstg_sketch** out);
+/* Builds only Kerdock bases [basis_begin, basis_end) (and the identity block
+ * when include_identity != 0) into a full-size sketch: the basis-sharded
+ * preprocessing of a multi-GPU replica. */
+int fstg_preprocess_shard(const void* a, int dtype, int64_t m, int64_t n, int device, void* stream,
+                          int64_t basis_begin, int64_t basis_end, int include_identity, fstg_sketch** out);
+int fstg_sketch_info_get(const fstg_sketch* sk, fstg_sketch_info* info);
+/* Sketch::row_norm_max (sketch.hpp:105) */
+int fstg_row_norm_max(const fstg_sketch* sk, double* out);
+/* Sketch::column (sketch.hpp:114-117): copies column ell (m values) to `out`. */
+int fstg_sketch_column(const fstg_sketch* sk, int64_t ell, void* out);
+/* Raw device pointers (column-major, stride column_stride) for zero-copy use
+ * by collectives (all-gather of basis shards) and tests. */
+int fstg_sketch_device_columns(const fstg_sketch* sk, void** columns);
+/* draw_and_gather (stream.hpp:184-191): copies columns indices[0..count) into
+ * out (count x m, row j = column indices[j]); out may be host or device. */
+int fstg_sketch_gather(const fstg_sketch* sk, const int64_t* indices, int64_t count, void* out, void* stream);
+/* Device time of the last preprocess (ms, CUDA events). */
+int fstg_sketch_preprocess_ms(const fstg_sketch* sk, double* ms);
+void fstg_destroy(fstg_sketch* sk);
+
+/* ------------------------------------------------------------ streaming ---- */
+/* draw_samples (stream.hpp:173-182) for B vectors: vector v uses seeds[v] in
+ * place of p->seed. indices: B x (J*K) int64 (host or device). */
+int fstg_draw_samples(const fstg_sketch* sk, const fstg_stream_params* p, const uint64_t* seeds, int64_t B,
+                      int64_t* indices, void* stream);
+
+/* transform (stream.hpp:272-275) over a batch of B vectors X (B x n row-major,
+ * sketch dtype). Vector v draws its indices from seeds[v] (seeds == NULL ->
+ * p->seed for every vector). Outputs (want = fstg_candidate_count):
+ *   counts[B]            support size of each vector
+ *   support[B x want]    sorted ascending support indices (first counts[v] valid)
+ *   values[B x want]     exact (Ax)_i for the support, sketch dtype
+ *   candidates[B x want] optional (NULL): the sorted candidate set
+ *   mu[B x m]            optional (NULL): the median-of-means estimate
+ * Any pointer may be host or device memory. */
+int fstg_transform_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p,
+                         const uint64_t* seeds, int32_t* counts, int32_t* support, void* values,
+                         int32_t* candidates, void* mu, void* stream);
+
+/* transform_with_samples (stream.hpp:197-268): as above with pre-drawn
+ * indices (B x J*K int64, host or device) instead of seeds. */
+int fstg_transform_with_samples_batch(const fstg_sketch* sk, const void* X, int64_t B,
+                                      const fstg_stream_params* p, const int64_t* indices, int32_t* counts,
+                                      int32_t* support, void* values, int32_t* candidates, void* mu,
+                                      void* stream);
+
+/* ------------------------------------------------- synthetic inputs (host) -- */
+/* SeededRng(seed).gaussian() x count (reference rng.hpp:31-43, fill order of
+ * generators.hpp:22-25). */
+int fstg_gen_gaussian(uint64_t seed, int64_t count, double* out);
+/* B target vectors y (B x m): s distinct rows by partial Fisher-Yates
+ * (generators.hpp:44-53) valued +-1/sqrt(s) (value_kind 0) or N(0,1)
+ * (value_kind 1), plus noise_sigma * N(0,1) on every entry. */
+int fstg_gen_sparse_targets(const uint64_t* seeds, int64_t B, int64_t m, int64_t s, int value_kind,
+                            double noise_sigma, double* Y);
+
+/* ------------------------------------------------------------ profiling ---- */
+/* When enabled, the library brackets each launch of its kernels with CUDA
+ * events on the launching stream; fstg_profile_read returns the accumulated
+ * device milliseconds and launch count of kernel `name` ("preprocess_fwht",
+ * "draw", "stream", ...) since the last reset. */
+int fstg_profile_enable(int enable);
+int fstg_profile_reset(void);
+int fstg_profile_read(const char* name, double* ms, int64_t* launches);
+/* Total kernel launches issued by the library since the last reset. */
+int fstg_launch_count(int64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FST_B200_H_ */

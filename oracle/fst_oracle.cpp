@@ -509,6 +509,69 @@ template TransformResult<double> transform_with_samples<double>(const Sketch<dou
 template TransformResult<float> transform_with_samples<float>(const Sketch<float>&, const float*,
                                                               const StreamParams&, const std::vector<std::int64_t>&);
 
+TransformResult<double> transform_gathered(const double* a, std::int64_t m, std::int64_t n, const double* x,
+                                           const StreamParams& p, const std::vector<std::int64_t>& indices,
+                                           const double* gathered) {
+  // Same steps as transform_with_samples; sk.column(ell) replaced by the
+  // gathered copy (stream.hpp:235-236).
+  p.validate();
+  if (static_cast<std::int64_t>(indices.size()) != p.J * p.K)
+    throw std::invalid_argument("transform: drawn sample count does not match J*K");
+  const DesignParams design = DesignParams::make(even_log2_ceil(n));
+  const std::int64_t kb = design.kerdock_bases() * design.d;
+  const double sqrt_d = std::sqrt(static_cast<double>(design.d));
+  std::vector<double> means(static_cast<std::size_t>(m * p.K), 0.0);
+  std::uint64_t rev[16];
+  std::int64_t cached_s = -1;
+  for (std::int64_t b = 0; b < p.K; ++b) {
+    double* col_sum = means.data() + b * m;
+    for (std::int64_t j = 0; j < p.J; ++j) {
+      const std::int64_t jj = b * p.J + j;
+      const std::int64_t ell = indices[static_cast<std::size_t>(jj)];
+      if (ell < 0 || ell >= design.L) throw std::out_of_range("Sketch::column: index out of range");
+      double t;
+      if (ell >= kb) {
+        const std::int64_t pos = ell - kb;
+        t = pos < n ? sqrt_d * x[pos] : 0.0;
+      } else {
+        const std::int64_t s = ell / design.d;
+        if (s != cached_s) {
+          const auto mat = kerdock_matrix(design, static_cast<std::uint64_t>(s));
+          reversed_q_rows(mat.data(), design.k, rev);
+          cached_s = s;
+        }
+        t = kerdock_inner_product(x, n, design.d, rev, static_cast<std::uint64_t>(ell % design.d));
+      }
+      if (t == 0.0) continue;
+      const double* col = gathered + jj * m;
+      for (std::int64_t i = 0; i < m; ++i) col_sum[i] += t * col[i];
+    }
+  }
+  for (auto& v : means) v /= static_cast<double>(p.J);
+  TransformResult<double> res;
+  res.mu = median_of_batch_means(means.data(), m, p.K);
+  res.samples_used = p.J * p.K;
+  const std::int64_t want = candidate_count(p.s, p.widen, m);
+  std::vector<std::int64_t> order(static_cast<std::size_t>(m));
+  std::iota(order.begin(), order.end(), std::int64_t{0});
+  const auto& mu = res.mu;
+  std::nth_element(order.begin(), order.begin() + want, order.end(), [&mu](std::int64_t u, std::int64_t w) {
+    const double mu_u = std::abs(mu[u]), mu_w = std::abs(mu[w]);
+    return mu_u != mu_w ? mu_u > mu_w : u < w;
+  });
+  res.candidate_set.assign(order.begin(), order.begin() + want);
+  std::sort(res.candidate_set.begin(), res.candidate_set.end());
+  for (const std::int64_t i : res.candidate_set) {
+    double v = 0;
+    for (std::int64_t j = 0; j < n; ++j) v += a[i * n + j] * x[j];
+    if (std::abs(v) >= p.epsilon) {
+      res.support.push_back(i);
+      res.values.push_back(v);
+    }
+  }
+  return res;
+}
+
 // ----------------------------------------------------------- generators ----
 
 std::vector<double> gen_orthogonal(std::int64_t n, std::uint64_t seed) {

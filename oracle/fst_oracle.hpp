@@ -168,6 +168,14 @@ template <typename T>
 TransformResult<T> transform_with_samples(const Sketch<T>& sk, const T* x, const StreamParams& p,
                                           const std::vector<std::int64_t>& indices);
 
+/// The draw_and_gather path (stream.hpp:184-191, 197-268 with
+/// drawn.use_gathered): identical arithmetic, columns supplied by the caller
+/// (gathered: N x m, row j = column ell_j). Used to check full-size (n=4096)
+/// GPU runs without materialising the 275 GB fp64 sketch.
+TransformResult<double> transform_gathered(const double* a, std::int64_t m, std::int64_t n, const double* x,
+                                           const StreamParams& p, const std::vector<std::int64_t>& indices,
+                                           const double* gathered);
+
 // --------------------------------------------------------- generators.hpp --
 
 /// generators.hpp:20-33 — Haar orthogonal: Householder QR of a SeededRng

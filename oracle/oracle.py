@@ -348,6 +348,55 @@ def _transform(sk: Sketch, x, p: StreamParams, indices) -> TransformResult:
     return TransformResult(sup[:k].copy(), vals[:k].copy(), cand, mu, p.J * p.K)
 
 
+def transform_gathered(a, x, p: StreamParams, indices, gathered) -> TransformResult:
+    """draw_and_gather path (stream.hpp:184-191): gathered is (J*K, m), row j = column indices[j]."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    m, n = a.shape
+    indices = np.ascontiguousarray(indices, dtype=np.int64)
+    gathered = np.ascontiguousarray(gathered, dtype=np.float64)
+    if gathered.shape != (p.J * p.K, m):
+        raise ValueError("gathered must be (J*K, m)")
+    want = candidate_count(p.s, p.widen, m)
+    mu = np.zeros(m)
+    cand = np.zeros(want, dtype=np.int64)
+    sup = np.zeros(want, dtype=np.int64)
+    vals = np.zeros(want)
+    ns = C.c_int64()
+    _check(lib().orc_transform_gathered(_ptr(a), C.c_int64(m), C.c_int64(n), _ptr(x), C.c_double(p.epsilon),
+                                        C.c_double(p.delta), C.c_int64(p.s), C.c_int64(p.J), C.c_int64(p.K),
+                                        C.c_int64(p.widen), _ptr(indices), _ptr(gathered), _ptr(mu), _ptr(cand),
+                                        _ptr(sup), _ptr(vals), C.byref(ns)))
+    k = ns.value
+    return TransformResult(sup[:k].copy(), vals[:k].copy(), cand, mu, p.J * p.K)
+
+
+def design_columns(k: int, n: int, ells) -> np.ndarray:
+    """(count, n): row j = s_{ells[j]} (kerdock.hpp:156-167)."""
+    ells = np.ascontiguousarray(ells, dtype=np.int64).ravel()
+    out = np.zeros((len(ells), n), dtype=np.float64)
+    _check(lib().orc_design_columns(C.c_int(k), C.c_int64(n), _ptr(ells), C.c_int64(len(ells)), _ptr(out)))
+    return out
+
+
+def bench_gathered(a, X, p: StreamParams, seeds, gathered, L: int, threads: int, total: int):
+    """Times the reference transform() over `total` vectors cycling a pool of P prepared vectors.
+    gathered: (P, J*K, m) fp64 host columns. Returns (pool support counts, wall seconds)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    gathered = np.ascontiguousarray(gathered, dtype=np.float64)
+    m, n = a.shape
+    P = X.shape[0]
+    counts = np.zeros(P, dtype=np.int64)
+    secs = C.c_double()
+    _check(lib().orc_bench_gathered(_ptr(a), C.c_int64(m), C.c_int64(n), _ptr(X), C.c_int64(P),
+                                    C.c_double(p.epsilon), C.c_double(p.delta), C.c_int64(p.s), C.c_int64(p.J),
+                                    C.c_int64(p.K), C.c_int64(p.widen), _ptr(seeds), _ptr(gathered), C.c_int64(L),
+                                    C.c_int(threads), C.c_int64(total), _ptr(counts), C.byref(secs)))
+    return counts, secs.value
+
+
 def transform_stream(sk: Sketch, X: np.ndarray, p: StreamParams, seeds: np.ndarray, threads: int):
     """Runs transform() over B vectors on `threads` host threads; returns (counts, seconds)."""
     X = np.ascontiguousarray(X, dtype=sk.dtype)

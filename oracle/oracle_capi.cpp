@@ -3,7 +3,9 @@
 // Status codes mirror the reference's exception classes:
 //   0 ok, 1 std::invalid_argument, 2 std::out_of_range, 3 std::overflow_error,
 //   4 std::runtime_error, 5 std::logic_error / other.
+#include <atomic>
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -295,6 +297,90 @@ int orc_transform_stream(void* hv, const void* X, std::int64_t B, double eps, do
       pool.emplace_back([&work, f, l] { work(f, l); });
     }
     for (auto& th : pool) th.join();
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+int orc_transform_gathered(const double* a, std::int64_t m, std::int64_t n, const double* x, double eps,
+                           double delta, std::int64_t s, std::int64_t J, std::int64_t K, std::int64_t widen,
+                           const std::int64_t* indices, const double* gathered, double* mu_out,
+                           std::int64_t* cand_out, std::int64_t* support_out, double* values_out,
+                           std::int64_t* nsupport) {
+  return guarded([&] {
+    const StreamParams p = make_params(eps, delta, s, J, K, widen, 0);
+    p.validate();
+    const std::vector<std::int64_t> idx(indices, indices + p.J * p.K);
+    const auto r = transform_gathered(a, m, n, x, p, idx, gathered);
+    std::memcpy(mu_out, r.mu.data(), sizeof(double) * r.mu.size());
+    std::memcpy(cand_out, r.candidate_set.data(), sizeof(std::int64_t) * r.candidate_set.size());
+    std::memcpy(support_out, r.support.data(), sizeof(std::int64_t) * r.support.size());
+    std::memcpy(values_out, r.values.data(), sizeof(double) * r.values.size());
+    *nsupport = static_cast<std::int64_t>(r.support.size());
+  });
+}
+
+// s_ell for each requested index (count x n, row j = s_{ell_j}), kerdock.hpp:156-167.
+int orc_design_columns(int k, std::int64_t n, const std::int64_t* ells, std::int64_t count, double* out) {
+  return guarded([&] {
+    const DesignParams p = DesignParams::make(k);
+    if (n < 1 || n > p.d) throw std::invalid_argument("design_columns: n out of [1,d]");
+    const double sqrt_d = std::sqrt(static_cast<double>(p.d));
+    std::vector<std::uint8_t> qbits;
+    std::int64_t cached = -1;
+    for (std::int64_t j = 0; j < count; ++j) {
+      const DecodedIndex idx = decode_index(p, ells[j]);
+      double* v = out + j * n;
+      if (idx.identity) {
+        std::fill(v, v + n, 0.0);
+        if (static_cast<std::int64_t>(idx.wpos) < n) v[idx.wpos] = sqrt_d;
+        continue;
+      }
+      if (static_cast<std::int64_t>(idx.s) != cached) {
+        const auto m = kerdock_matrix(p, idx.s);
+        qbits.assign(static_cast<std::size_t>(n), 0);
+        for (std::int64_t q = 0; q < n; ++q)
+          qbits[q] = static_cast<std::uint8_t>(
+              quadratic_form(m.data(), p.k, coords_of_position(static_cast<std::uint64_t>(q), p.k)));
+        cached = static_cast<std::int64_t>(idx.s);
+      }
+      for (std::int64_t q = 0; q < n; ++q)
+        v[q] = (qbits[q] ^ (__builtin_popcountll(idx.wpos & static_cast<std::uint64_t>(q)) & 1)) ? -1.0 : 1.0;
+    }
+  });
+}
+
+// CPU baseline over a pool of P prepared vectors (gathered columns in host
+// DRAM, P x N x m): `threads` threads process `total` vectors, vector t taking
+// pool entry t % P; each runs draw_samples + transform_with_samples (the
+// reference's transform(), stream.hpp:272-275) with its columns read from the
+// gathered buffer. Returns wall seconds and the support sizes of the pool.
+int orc_bench_gathered(const double* a, std::int64_t m, std::int64_t n, const double* X, std::int64_t P,
+                       double eps, double delta, std::int64_t s, std::int64_t J, std::int64_t K, std::int64_t widen,
+                       const std::uint64_t* seeds, const double* gathered, std::int64_t L, int threads,
+                       std::int64_t total, std::int64_t* counts_out, double* seconds) {
+  return guarded([&] {
+    const std::int64_t N = J * K;
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    threads = std::max(1, threads);
+    std::atomic<int> failed{0};
+    for (int th = 0; th < threads; ++th) {
+      pool.emplace_back([&, th] {
+        try {
+          for (std::int64_t t = th; t < total; t += threads) {
+            const std::int64_t v = t % P;
+            StreamParams p = make_params(eps, delta, s, J, K, widen, seeds[v]);
+            const auto idx = draw_samples(L, p);
+            const auto r = transform_gathered(a, m, n, X + v * n, p, idx, gathered + v * N * m);
+            if (t < P) counts_out[v] = static_cast<std::int64_t>(r.support.size());
+          }
+        } catch (...) {
+          failed = 1;
+        }
+      });
+    }
+    for (auto& t : pool) t.join();
+    if (failed) throw std::runtime_error("bench_gathered: worker failed");
     *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
 }

@@ -1,0 +1,819 @@
+// C-ABI implementation (include/fst_b200.h): sketch lifetime, batching,
+// host<->device staging and profiling around the sm_100a kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fst_b200.h"
+#include "design.hpp"
+#include "kernels.hpp"
+
+using namespace fstg;
+
+struct fstg_sketch {
+  int device = 0;
+  int dtype = FSTG_F32;
+  Design design;
+  int64_t m = 0, n = 0, ldc = 0, lda = 0;
+  void* cols = nullptr;
+  void* a = nullptr;
+  uint32_t* qplain = nullptr;
+  uint32_t* qtrans = nullptr;
+  uint32_t* revtab = nullptr;
+  double row_norm_max = 0;
+  double preprocess_ms = 0;
+  uint64_t device_bytes = 0;
+};
+
+namespace {
+
+thread_local std::string g_error;
+
+int set_error(int code, const std::string& msg) {
+  g_error = msg;
+  return code;
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return FSTG_OK;
+  } catch (const InvalidArgument& e) {
+    return set_error(FSTG_ERR_INVALID_ARGUMENT, e.what());
+  } catch (const OutOfRange& e) {
+    return set_error(FSTG_ERR_OUT_OF_RANGE, e.what());
+  } catch (const Overflow& e) {
+    return set_error(FSTG_ERR_OVERFLOW, e.what());
+  } catch (const NotSupported& e) {
+    return set_error(FSTG_ERR_NOT_SUPPORTED, e.what());
+  } catch (const CudaError& e) {
+    return set_error(FSTG_ERR_CUDA, e.what());
+  } catch (const std::invalid_argument& e) {
+    return set_error(FSTG_ERR_INVALID_ARGUMENT, e.what());
+  } catch (const std::out_of_range& e) {
+    return set_error(FSTG_ERR_OUT_OF_RANGE, e.what());
+  } catch (const std::overflow_error& e) {
+    return set_error(FSTG_ERR_OVERFLOW, e.what());
+  } catch (const std::bad_alloc& e) {
+    return set_error(FSTG_ERR_RUNTIME, e.what());
+  } catch (const std::runtime_error& e) {
+    return set_error(FSTG_ERR_RUNTIME, e.what());
+  } catch (const std::exception& e) {
+    return set_error(FSTG_ERR_RUNTIME, e.what());
+  }
+}
+
+// ------------------------------------------------------------ profiling ----
+struct ProfEntry {
+  double ms = 0;
+  int64_t launches = 0;
+};
+struct PendingEvent {
+  std::string name;
+  cudaEvent_t start, stop;
+};
+std::mutex g_prof_mu;
+bool g_prof_on = false;
+std::map<std::string, ProfEntry> g_prof;
+std::vector<PendingEvent> g_pending;
+std::atomic<int64_t> g_launches{0};
+
+void resolve_pending_locked() {
+  for (auto& p : g_pending) {
+    float ms = 0;
+    if (cudaEventSynchronize(p.stop) == cudaSuccess && cudaEventElapsedTime(&ms, p.start, p.stop) == cudaSuccess) {
+      auto& e = g_prof[p.name];
+      e.ms += ms;
+      e.launches += 1;
+    }
+    cudaEventDestroy(p.start);
+    cudaEventDestroy(p.stop);
+  }
+  g_pending.clear();
+}
+
+// RAII bracket around one kernel launch.
+class ProfScope {
+ public:
+  ProfScope(const char* name, cudaStream_t st) : name_(name), st_(st) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    on_ = g_prof_on;
+    if (on_) {
+      cudaEventCreate(&start_);
+      cudaEventCreate(&stop_);
+      cudaEventRecord(start_, st_);
+    }
+  }
+  ~ProfScope() {
+    if (!on_) return;
+    cudaEventRecord(stop_, st_);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_pending.push_back({name_, start_, stop_});
+  }
+
+ private:
+  std::string name_;
+  cudaStream_t st_;
+  bool on_ = false;
+  cudaEvent_t start_{}, stop_{};
+};
+
+// ------------------------------------------------------------- helpers ----
+bool is_device_ptr(const void* p) {
+  if (p == nullptr) return false;
+  cudaPointerAttributes attr{};
+  if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+void require_device(int device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    throw CudaError("no CUDA device available (this library has no CPU fallback)");
+  }
+  if (device < 0 || device >= count) throw InvalidArgument("device ordinal out of range");
+  cudaDeviceProp prop{};
+  cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major != 10) throw CudaError("device is not sm_100 (B200); kernels are built for sm_100a only");
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+}
+
+size_t dtype_size(int dtype) {
+  if (dtype == FSTG_F32) return 4;
+  if (dtype == FSTG_F64) return 8;
+  throw InvalidArgument("dtype must be FSTG_F32 or FSTG_F64");
+}
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+void validate(const fstg_stream_params* p) {
+  // stream.hpp:30-38
+  if (p == nullptr) throw InvalidArgument("StreamParams: null");
+  if (!(p->epsilon > p->delta) || p->delta < 0) throw InvalidArgument("StreamParams: need epsilon > delta >= 0");
+  if (p->s < 1) throw InvalidArgument("StreamParams: need s >= 1");
+  if (p->J < 1 || p->K < 1) throw InvalidArgument("StreamParams: need J, K >= 1");
+  if (p->widen < 1) throw InvalidArgument("StreamParams: need widen >= 1");
+  if (p->J > INT64_MAX / p->K) throw Overflow("StreamParams: J*K overflows");
+}
+
+__global__ void finite_check_kernel(const void* a, int dtype, int64_t count, int* bad) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
+    const double v = dtype == FSTG_F64 ? static_cast<const double*>(a)[i] : double(static_cast<const float*>(a)[i]);
+    if (!isfinite(v)) atomicExch(bad, 1);
+  }
+}
+
+template <typename T>
+__global__ void gather_kernel(const T* __restrict__ cols, int64_t ldc, int64_t m, const int64_t* __restrict__ idx,
+                              int64_t count, int64_t L, T* __restrict__ out, int* __restrict__ bad) {
+  for (int64_t j = blockIdx.x; j < count; j += gridDim.x) {
+    const int64_t ell = idx[j];
+    if (ell < 0 || ell >= L) {
+      if (threadIdx.x == 0) atomicExch(bad, 1);
+      continue;
+    }
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) out[j * m + i] = cols[ell * ldc + i];
+  }
+}
+
+// Device scratch released at scope exit (stream-ordered).
+struct DevBuf {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  DevBuf() = default;
+  DevBuf(size_t bytes, cudaStream_t s) : st(s) {
+    if (bytes) cuda_check(cudaMallocAsync(&p, bytes, s), "cudaMallocAsync");
+  }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), st(o.st) { o.p = nullptr; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      if (p) cudaFreeAsync(p, st);
+      p = o.p;
+      st = o.st;
+      o.p = nullptr;
+    }
+    return *this;
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, st);
+  }
+  template <typename U>
+  U* as() const {
+    return static_cast<U*>(p);
+  }
+};
+
+// ---------------------------------------------------------- preprocess ----
+template <typename T>
+void build_sketch(fstg_sketch* sk, const void* a_in, cudaStream_t st, int64_t b0, int64_t b1, bool identity) {
+  const int64_t m = sk->m, n = sk->n;
+  const Design& D = sk->design;
+  const int64_t nk = D.kerdock_bases();
+  constexpr int64_t VEC = 16 / sizeof(T);
+  sk->ldc = round_up(m, VEC);
+  sk->lda = round_up(n, VEC);
+
+  // embedded A (row-major, padded rows zeroed)
+  const size_t a_bytes = size_t(m) * sk->lda * sizeof(T);
+  cuda_check(cudaMalloc(&sk->a, a_bytes), "allocate embedded A");
+  sk->device_bytes += a_bytes;
+  cuda_check(cudaMemsetAsync(sk->a, 0, a_bytes, st), "memset A");
+  cuda_check(cudaMemcpy2DAsync(sk->a, sk->lda * sizeof(T), a_in, n * sizeof(T), n * sizeof(T), m,
+                               cudaMemcpyDefault, st),
+             "copy A to device");
+
+  {  // finite check (sketch.hpp:153)
+    DevBuf bad(sizeof(int), st);
+    cuda_check(cudaMemsetAsync(bad.p, 0, sizeof(int), st), "memset");
+    const int64_t count = m * sk->lda;
+    finite_check_kernel<<<148 * 4, 256, 0, st>>>(sk->a, sk->dtype, count, bad.as<int>());
+    cuda_check(cudaGetLastError(), "finite check");
+    int h = 0;
+    cuda_check(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st), "copy flag");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    if (h) throw InvalidArgument("preprocess: matrix entries must be finite");
+  }
+
+  // sketch columns
+  const uint64_t col_bytes = uint64_t(D.L) * uint64_t(sk->ldc) * sizeof(T);
+  {
+    cudaError_t e = cudaMalloc(&sk->cols, col_bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      sk->cols = nullptr;
+      throw std::runtime_error("preprocess: cannot allocate sketch of " + std::to_string(col_bytes) + " bytes");
+    }
+  }
+  sk->device_bytes += col_bytes;
+  if (sk->ldc != m || b0 != 0 || b1 != nk || !identity)
+    cuda_check(cudaMemsetAsync(sk->cols, 0, col_bytes, st), "memset sketch");
+
+  // Kerdock sign tables
+  const std::vector<uint32_t> rev = reversed_row_table(D);
+  const int64_t wpb = D.d >= 32 ? D.d / 32 : 1;
+  const int64_t twords = (D.d >= 128) ? (D.d >= 1024 ? D.d / 1024 : 1) * 32 : 0;
+  cuda_check(cudaMalloc(&sk->revtab, rev.size() * sizeof(uint32_t)), "allocate tables");
+  cuda_check(cudaMalloc(&sk->qplain, size_t(nk) * wpb * sizeof(uint32_t)), "allocate tables");
+  if (twords) cuda_check(cudaMalloc(&sk->qtrans, size_t(nk) * twords * sizeof(uint32_t)), "allocate tables");
+  sk->device_bytes += rev.size() * 4 + size_t(nk) * (wpb + twords) * 4;
+  cuda_check(cudaMemcpyAsync(sk->revtab, rev.data(), rev.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st),
+             "upload tables");
+  {
+    ProfScope ps("qtables", st);
+    cuda_check(launch_qtables(sk->revtab, D.k, nk, sk->qplain, sk->qtrans, st), "qtable kernel");
+  }
+
+  cudaEvent_t e0, e1;
+  cuda_check(cudaEventCreate(&e0), "event");
+  cuda_check(cudaEventCreate(&e1), "event");
+  cuda_check(cudaEventRecord(e0, st), "event");
+  if (b1 > b0) {
+    ProfScope ps("preprocess_fwht", st);
+    const cudaError_t e = launch_fwht_sketch<T>(D.k, static_cast<const T*>(sk->a), sk->lda, m, n, sk->qplain, b0,
+                                                b1, static_cast<T*>(sk->cols), sk->ldc, st);
+    if (e == cudaErrorNotSupported) {
+      cudaGetLastError();
+      throw NotSupported("preprocess: this (k, dtype) needs more than 227 KiB of shared memory per CTA");
+    }
+    cuda_check(e, "fwht sketch kernel");
+  }
+  if (identity) {
+    ProfScope ps("preprocess_identity", st);
+    cuda_check(launch_identity<T>(static_cast<const T*>(sk->a), sk->lda, m, n, D.d, nk, static_cast<T*>(sk->cols),
+                                  sk->ldc, st),
+               "identity kernel");
+  }
+  cuda_check(cudaEventRecord(e1, st), "event");
+
+  // row_norm_max (sketch.hpp:126-131)
+  DevBuf norms(size_t(m) * sizeof(double), st);
+  {
+    ProfScope ps("row_norms", st);
+    cuda_check(launch_row_norms<T>(static_cast<const T*>(sk->a), sk->lda, m, n, norms.as<double>(), st), "row norms");
+  }
+  std::vector<double> h(static_cast<size_t>(m));
+  cuda_check(cudaMemcpyAsync(h.data(), norms.p, size_t(m) * sizeof(double), cudaMemcpyDeviceToHost, st), "copy norms");
+  cuda_check(cudaStreamSynchronize(st), "preprocess sync");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  sk->preprocess_ms = ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  double rn = 0;
+  for (double v : h) rn = std::max(rn, v);
+  sk->row_norm_max = rn;
+}
+
+void destroy_sketch(fstg_sketch* sk) {
+  if (!sk) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(sk->device);
+  cudaFree(sk->cols);
+  cudaFree(sk->a);
+  cudaFree(sk->qplain);
+  cudaFree(sk->qtrans);
+  cudaFree(sk->revtab);
+  cudaSetDevice(prev);
+  delete sk;
+}
+
+int preprocess_impl(const void* a, int dtype, int64_t m, int64_t n, int device, void* stream, int64_t b0, int64_t b1,
+                    bool full, int include_identity, fstg_sketch** out) {
+  return guarded([&] {
+    if (out == nullptr) throw InvalidArgument("preprocess: out is null");
+    *out = nullptr;
+    dtype_size(dtype);
+    if (m < 1 || n < 1) throw InvalidArgument("preprocess: matrix must be nonempty");
+    if (a == nullptr) throw InvalidArgument("preprocess: matrix pointer is null");
+    const int k = even_log2_ceil(n);
+    const Design D = Design::make(k);
+    if (k > 14) throw NotSupported("preprocess: k > 14 (n > 16384) exceeds this GPU build's FWHT kernels");
+    if (full) {
+      b0 = 0;
+      b1 = D.kerdock_bases();
+    }
+    if (b0 < 0 || b1 > D.kerdock_bases() || b0 > b1) throw OutOfRange("preprocess_shard: basis range out of range");
+    require_device(device);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    auto* sk = new fstg_sketch();
+    sk->device = device;
+    sk->dtype = dtype;
+    sk->design = D;
+    sk->m = m;
+    sk->n = n;
+    try {
+      if (dtype == FSTG_F32)
+        build_sketch<float>(sk, a, st, b0, b1, full || include_identity);
+      else
+        build_sketch<double>(sk, a, st, b0, b1, full || include_identity);
+    } catch (...) {
+      destroy_sketch(sk);
+      throw;
+    }
+    *out = sk;
+  });
+}
+
+// --------------------------------------------------------------- stream ----
+struct Outputs {
+  int32_t* counts;
+  int32_t* support;
+  void* values;
+  int32_t* cands;
+  void* mu;
+};
+
+template <typename T>
+void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p, const uint64_t* seeds,
+               const int64_t* indices, const Outputs& out, cudaStream_t st) {
+  validate(p);
+  if (B < 0) throw InvalidArgument("transform: negative batch size");
+  if (B == 0) return;
+  if (X == nullptr) throw InvalidArgument("transform: X is null");
+  if (out.counts == nullptr || out.support == nullptr || out.values == nullptr)
+    throw InvalidArgument("transform: counts/support/values must be non-null");
+  const Design& D = sk->design;
+  const int64_t N = p->J * p->K;
+  if (N > (int64_t(1) << 40)) throw NotSupported("transform: J*K too large for this build");
+  const int64_t want = candidate_count(p->s, p->widen, sk->m);
+  const bool strict = p->mode == FSTG_MODE_STRICT || (p->mode == FSTG_MODE_DEFAULT && sk->dtype == FSTG_F64);
+  if (p->mode < 0 || p->mode > 2) throw InvalidArgument("StreamParams: unknown mode");
+  cuda_check(cudaSetDevice(sk->device), "cudaSetDevice");
+
+  const int64_t n = sk->n, m = sk->m;
+  const bool x_dev = is_device_ptr(X);
+  const bool seeds_dev = is_device_ptr(seeds);
+  const bool idx_dev = is_device_ptr(indices);
+  const bool o_dev = is_device_ptr(out.counts) && is_device_ptr(out.support) && is_device_ptr(out.values) &&
+                     (out.cands == nullptr || is_device_ptr(out.cands)) && (out.mu == nullptr || is_device_ptr(out.mu));
+  const bool all_dev = x_dev && o_dev && (seeds == nullptr || seeds_dev) && (indices == nullptr || idx_dev);
+
+  // Chunking bounds scratch (indices: chunk x N x 4 bytes) and pipelines host copies.
+  int64_t chunk = all_dev ? B : std::min<int64_t>(B, 4096);
+  chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, (int64_t(1) << 29) / std::max<int64_t>(N, 1)));
+
+  StreamArgs<T> args{};
+  args.cols = static_cast<const T*>(sk->cols);
+  args.ldc = sk->ldc;
+  args.a = static_cast<const T*>(sk->a);
+  args.lda = sk->lda;
+  args.qplain = sk->qplain;
+  args.qtrans = sk->qtrans;
+  args.revtab = sk->revtab;
+  args.k = D.k;
+  args.d = D.d;
+  args.L = D.L;
+  args.m = m;
+  args.n = n;
+  args.kb = D.kerdock_bases() * D.d;
+  args.J = p->J;
+  args.K = p->K;
+  args.N = N;
+  args.want = want;
+  args.epsilon = p->epsilon;
+  args.ldx = n;
+  args.m_pad = sk->ldc;
+  constexpr int64_t SEG = 16384 / sizeof(T);
+  args.nseg = static_cast<int>((sk->ldc + SEG - 1) / SEG);
+  if (args.nseg > 4) throw NotSupported("transform: m too large for this GPU build (m <= 4 * 16 KiB / sizeof(T))");
+  size_t smem = 0;
+  int stages = 0, stage_stride = 0;
+  const int grid_max = stream_grid_size<T>(args, strict, chunk, &smem, &stages, &stage_stride);
+  if (smem > 227 * 1024) throw NotSupported("transform: shared-memory plan exceeds 227 KiB (d or want too large)");
+  args.stages = stages;
+  args.stage_stride = stage_stride;
+
+  const int nbuf = all_dev ? 1 : 2;
+  cudaStream_t copy_st = nullptr;
+  if (!all_dev) cuda_check(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking), "stream");
+  struct Bufs {
+    DevBuf X, idx, counts, support, values, cands, mu, seeds, idx64;
+  };
+  std::vector<Bufs> bufs(nbuf);
+  DevBuf means(size_t(grid_max) * p->K * sk->ldc * sizeof(T), st);
+  DevBuf bad(sizeof(int), st);
+  cuda_check(cudaMemsetAsync(bad.p, 0, sizeof(int), st), "memset");
+  std::vector<cudaEvent_t> ev_in(nbuf), ev_done(nbuf), ev_out(nbuf);
+  for (int b = 0; b < nbuf; ++b) {
+    cuda_check(cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ev_done[b], cudaEventDisableTiming), "event");
+    cuda_check(cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming), "event");
+    Bufs& bf = bufs[b];
+    bf.idx = DevBuf(size_t(chunk) * N * sizeof(uint32_t), st);
+    if (!x_dev) bf.X = DevBuf(size_t(chunk) * n * sizeof(T), st);
+    if (!o_dev) {
+      bf.counts = DevBuf(size_t(chunk) * sizeof(int32_t), st);
+      bf.support = DevBuf(size_t(chunk) * want * sizeof(int32_t), st);
+      bf.values = DevBuf(size_t(chunk) * want * sizeof(T), st);
+      if (out.cands) bf.cands = DevBuf(size_t(chunk) * want * sizeof(int32_t), st);
+      if (out.mu) bf.mu = DevBuf(size_t(chunk) * m * sizeof(T), st);
+    }
+    if (seeds != nullptr && !seeds_dev) bf.seeds = DevBuf(size_t(chunk) * sizeof(uint64_t), st);
+    if (indices != nullptr && !idx_dev) bf.idx64 = DevBuf(size_t(chunk) * N * sizeof(int64_t), st);
+  }
+  if (!all_dev) cuda_check(cudaStreamSynchronize(st), "sync allocations");
+
+  int it = 0;
+  for (int64_t v0 = 0; v0 < B; v0 += chunk, ++it) {
+    const int64_t cb = std::min(chunk, B - v0);
+    const int b = it % nbuf;
+    Bufs& bf = bufs[b];
+    // ---- inputs ----
+    const T* Xd = x_dev ? static_cast<const T*>(X) + v0 * n : bf.X.as<T>();
+    const uint64_t* sd = seeds == nullptr ? nullptr : (seeds_dev ? seeds + v0 : bf.seeds.as<uint64_t>());
+    const int64_t* id64 = indices == nullptr ? nullptr : (idx_dev ? indices + v0 * N : bf.idx64.as<int64_t>());
+    if (!all_dev) {
+      if (it >= nbuf) cuda_check(cudaStreamWaitEvent(copy_st, ev_done[b], 0), "wait");  // buffer free
+      if (!x_dev)
+        cuda_check(cudaMemcpyAsync(bf.X.p, static_cast<const T*>(X) + v0 * n, size_t(cb) * n * sizeof(T),
+                                   cudaMemcpyHostToDevice, copy_st),
+                   "H2D X");
+      if (seeds != nullptr && !seeds_dev)
+        cuda_check(cudaMemcpyAsync(bf.seeds.p, seeds + v0, size_t(cb) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                   copy_st),
+                   "H2D seeds");
+      if (indices != nullptr && !idx_dev)
+        cuda_check(cudaMemcpyAsync(bf.idx64.p, indices + v0 * N, size_t(cb) * N * sizeof(int64_t),
+                                   cudaMemcpyHostToDevice, copy_st),
+                   "H2D indices");
+      cuda_check(cudaEventRecord(ev_in[b], copy_st), "event");
+      cuda_check(cudaStreamWaitEvent(st, ev_in[b], 0), "wait");
+      if (it >= nbuf) cuda_check(cudaStreamWaitEvent(st, ev_out[b], 0), "wait");  // outputs drained
+    }
+    // ---- indices ----
+    if (indices == nullptr) {
+      ProfScope ps("draw", st);
+      cuda_check(launch_draw<uint32_t>(sd, p->seed, cb, N, static_cast<uint64_t>(D.L), bf.idx.as<uint32_t>(), st),
+                 "draw kernel");
+    } else {
+      ProfScope ps("narrow_indices", st);
+      cuda_check(launch_narrow_indices(id64, cb * N, D.L, bf.idx.as<uint32_t>(), bad.as<int>(), st), "indices");
+    }
+    // ---- estimator ----
+    args.X = Xd;
+    args.idx = bf.idx.as<uint32_t>();
+    args.B = cb;
+    args.counts = o_dev ? out.counts + v0 : bf.counts.as<int32_t>();
+    args.support = o_dev ? out.support + v0 * want : bf.support.as<int32_t>();
+    args.values = o_dev ? static_cast<T*>(out.values) + v0 * want : bf.values.as<T>();
+    args.cands = out.cands == nullptr ? nullptr : (o_dev ? out.cands + v0 * want : bf.cands.as<int32_t>());
+    args.mu = out.mu == nullptr ? nullptr : (o_dev ? static_cast<T*>(out.mu) + v0 * m : bf.mu.as<T>());
+    args.means = means.as<T>();
+    const int grid = static_cast<int>(std::min<int64_t>(grid_max, cb));
+    {
+      ProfScope ps("stream", st);
+      cuda_check(launch_stream<T>(args, strict, grid, st), "stream kernel");
+    }
+    // ---- outputs ----
+    if (!all_dev) {
+      cuda_check(cudaEventRecord(ev_done[b], st), "event");
+      if (!o_dev) {
+        cuda_check(cudaStreamWaitEvent(copy_st, ev_done[b], 0), "wait");
+        auto d2h = [&](void* dst, const void* src, size_t bytes) {
+          cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, copy_st), "D2H");
+        };
+        d2h(out.counts + v0, bf.counts.p, size_t(cb) * sizeof(int32_t));
+        d2h(out.support + v0 * want, bf.support.p, size_t(cb) * want * sizeof(int32_t));
+        d2h(static_cast<T*>(out.values) + v0 * want, bf.values.p, size_t(cb) * want * sizeof(T));
+        if (out.cands) d2h(out.cands + v0 * want, bf.cands.p, size_t(cb) * want * sizeof(int32_t));
+        if (out.mu) d2h(static_cast<T*>(out.mu) + v0 * m, bf.mu.p, size_t(cb) * m * sizeof(T));
+        cuda_check(cudaEventRecord(ev_out[b], copy_st), "event");
+      } else {
+        cuda_check(cudaEventRecord(ev_out[b], st), "event");
+      }
+    }
+  }
+  if (indices != nullptr) {
+    int h = 0;
+    cuda_check(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st), "copy flag");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    if (h) throw OutOfRange("Sketch::column: index out of range");
+  }
+  if (!all_dev) {
+    cuda_check(cudaStreamSynchronize(copy_st), "sync copies");
+    cuda_check(cudaStreamSynchronize(st), "sync compute");
+    cudaStreamDestroy(copy_st);
+  }
+  for (int b = 0; b < nbuf; ++b) {
+    cudaEventDestroy(ev_in[b]);
+    cudaEventDestroy(ev_done[b]);
+    cudaEventDestroy(ev_out[b]);
+  }
+}
+
+}  // namespace
+
+// ====================================================================== ABI ==
+extern "C" {
+
+const char* fstg_last_error(void) { return g_error.c_str(); }
+
+const char* fstg_version(void) { return "fst_b200 1 (sm_100a)"; }
+
+int fstg_device_count(int* count) {
+  return guarded([&] {
+    if (!count) throw InvalidArgument("null");
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+      cudaGetLastError();
+      c = 0;
+    }
+    int ok = 0;
+    for (int i = 0; i < c; ++i) {
+      cudaDeviceProp prop{};
+      if (cudaGetDeviceProperties(&prop, i) == cudaSuccess && prop.major == 10) ++ok;
+    }
+    *count = ok;
+  });
+}
+
+int fstg_even_log2_ceil(int64_t n, int* k) {
+  return guarded([&] { *k = even_log2_ceil(n); });
+}
+
+int fstg_design_params(int k, int64_t* d, int64_t* L) {
+  return guarded([&] {
+    const Design D = Design::make(k);
+    *d = D.d;
+    *L = D.L;
+  });
+}
+
+int fstg_kerdock_matrix(int k, uint64_t s, uint64_t* rows) {
+  return guarded([&] {
+    const Design D = Design::make(k);
+    const Field f(k - 1, D.modulus);
+    const auto r = kerdock_matrix(D, f, s);
+    std::memcpy(rows, r.data(), r.size() * sizeof(uint64_t));
+  });
+}
+
+int fstg_choose_params(double r, double gamma, double eta, int64_t m, int64_t* J, int64_t* K) {
+  return guarded([&] { choose_params(r, gamma, eta, m, J, K); });
+}
+
+int fstg_validate_params(const fstg_stream_params* p) {
+  return guarded([&] { validate(p); });
+}
+
+int64_t fstg_candidate_count(int64_t s, int64_t widen, int64_t m) { return candidate_count(s, widen, m); }
+
+int fstg_preprocess(const void* a, int dtype, int64_t m, int64_t n, int device, void* stream, fstg_sketch** out) {
+  return preprocess_impl(a, dtype, m, n, device, stream, 0, 0, true, 1, out);
+}
+
+int fstg_preprocess_shard(const void* a, int dtype, int64_t m, int64_t n, int device, void* stream,
+                          int64_t basis_begin, int64_t basis_end, int include_identity, fstg_sketch** out) {
+  return preprocess_impl(a, dtype, m, n, device, stream, basis_begin, basis_end, false, include_identity, out);
+}
+
+int fstg_sketch_info_get(const fstg_sketch* sk, fstg_sketch_info* info) {
+  return guarded([&] {
+    if (!sk || !info) throw InvalidArgument("null sketch/info");
+    info->m = sk->m;
+    info->n = sk->n;
+    info->d = sk->design.d;
+    info->L = sk->design.L;
+    info->k = sk->design.k;
+    info->dtype = sk->dtype;
+    info->row_norm_max = sk->row_norm_max;
+    info->device = sk->device;
+    info->reserved = 0;
+    info->column_stride = sk->ldc;
+    info->device_bytes = sk->device_bytes;
+    info->preprocess_ms = sk->preprocess_ms;
+  });
+}
+
+int fstg_row_norm_max(const fstg_sketch* sk, double* out) {
+  return guarded([&] {
+    if (!sk || !out) throw InvalidArgument("null");
+    *out = sk->row_norm_max;
+  });
+}
+
+int fstg_sketch_column(const fstg_sketch* sk, int64_t ell, void* out) {
+  return guarded([&] {
+    if (!sk || !out) throw InvalidArgument("null");
+    if (ell < 0 || ell >= sk->design.L) throw OutOfRange("Sketch::column: index out of range");
+    cuda_check(cudaSetDevice(sk->device), "cudaSetDevice");
+    const size_t es = dtype_size(sk->dtype);
+    cuda_check(cudaMemcpy(out, static_cast<const char*>(sk->cols) + size_t(ell) * sk->ldc * es, size_t(sk->m) * es,
+                          cudaMemcpyDefault),
+               "copy column");
+  });
+}
+
+int fstg_sketch_gather(const fstg_sketch* sk, const int64_t* indices, int64_t count, void* out, void* stream) {
+  return guarded([&] {
+    if (!sk || (count > 0 && (!indices || !out))) throw InvalidArgument("sketch_gather: null argument");
+    if (count < 0) throw InvalidArgument("sketch_gather: negative count");
+    if (count == 0) return;
+    cuda_check(cudaSetDevice(sk->device), "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t es = dtype_size(sk->dtype);
+    DevBuf idx_buf, out_buf;
+    const int64_t* idx = indices;
+    if (!is_device_ptr(indices)) {
+      idx_buf = DevBuf(size_t(count) * sizeof(int64_t), st);
+      cuda_check(cudaMemcpyAsync(idx_buf.p, indices, size_t(count) * sizeof(int64_t), cudaMemcpyHostToDevice, st), "H2D");
+      idx = idx_buf.as<int64_t>();
+    }
+    const bool out_dev = is_device_ptr(out);
+    void* dst = out;
+    if (!out_dev) {
+      out_buf = DevBuf(size_t(count) * sk->m * es, st);
+      dst = out_buf.p;
+    }
+    DevBuf bad(sizeof(int), st);
+    cuda_check(cudaMemsetAsync(bad.p, 0, sizeof(int), st), "memset");
+    const unsigned grid = static_cast<unsigned>(std::min<int64_t>(count, 148 * 16));
+    {
+      ProfScope ps("gather", st);
+      if (sk->dtype == FSTG_F32)
+        gather_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float*>(sk->cols), sk->ldc, sk->m, idx, count,
+                                                  sk->design.L, static_cast<float*>(dst), bad.as<int>());
+      else
+        gather_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double*>(sk->cols), sk->ldc, sk->m, idx, count,
+                                                   sk->design.L, static_cast<double*>(dst), bad.as<int>());
+      cuda_check(cudaGetLastError(), "gather kernel");
+    }
+    int h = 0;
+    cuda_check(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st), "copy flag");
+    if (!out_dev) cuda_check(cudaMemcpyAsync(out, dst, size_t(count) * sk->m * es, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    if (h) throw OutOfRange("Sketch::column: index out of range");
+  });
+}
+
+int fstg_sketch_device_columns(const fstg_sketch* sk, void** columns) {
+  return guarded([&] {
+    if (!sk || !columns) throw InvalidArgument("null");
+    *columns = sk->cols;
+  });
+}
+
+int fstg_sketch_preprocess_ms(const fstg_sketch* sk, double* ms) {
+  return guarded([&] {
+    if (!sk || !ms) throw InvalidArgument("null");
+    *ms = sk->preprocess_ms;
+  });
+}
+
+void fstg_destroy(fstg_sketch* sk) { destroy_sketch(sk); }
+
+int fstg_draw_samples(const fstg_sketch* sk, const fstg_stream_params* p, const uint64_t* seeds, int64_t B,
+                      int64_t* indices, void* stream) {
+  return guarded([&] {
+    if (!sk) throw InvalidArgument("null sketch");
+    validate(p);
+    if (B < 0 || (B > 0 && indices == nullptr)) throw InvalidArgument("draw_samples: bad output");
+    if (B == 0) return;
+    cuda_check(cudaSetDevice(sk->device), "cudaSetDevice");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int64_t N = p->J * p->K;
+    const bool out_dev = is_device_ptr(indices);
+    DevBuf sd_buf, out_buf;
+    const uint64_t* sd = seeds;
+    if (seeds != nullptr && !is_device_ptr(seeds)) {
+      sd_buf = DevBuf(size_t(B) * sizeof(uint64_t), st);
+      cuda_check(cudaMemcpyAsync(sd_buf.p, seeds, size_t(B) * sizeof(uint64_t), cudaMemcpyHostToDevice, st), "H2D");
+      sd = sd_buf.as<uint64_t>();
+    }
+    int64_t* dst = indices;
+    if (!out_dev) {
+      out_buf = DevBuf(size_t(B) * N * sizeof(int64_t), st);
+      dst = out_buf.as<int64_t>();
+    }
+    {
+      ProfScope ps("draw", st);
+      cuda_check(launch_draw<int64_t>(sd, p->seed, B, N, static_cast<uint64_t>(sk->design.L), dst, st), "draw");
+    }
+    if (!out_dev) {
+      cuda_check(cudaMemcpyAsync(indices, dst, size_t(B) * N * sizeof(int64_t), cudaMemcpyDeviceToHost, st), "D2H");
+      cuda_check(cudaStreamSynchronize(st), "sync");
+    }
+  });
+}
+
+int fstg_transform_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p,
+                         const uint64_t* seeds, int32_t* counts, int32_t* support, void* values, int32_t* candidates,
+                         void* mu, void* stream) {
+  return guarded([&] {
+    if (!sk) throw InvalidArgument("null sketch");
+    const Outputs o{counts, support, values, candidates, mu};
+    if (sk->dtype == FSTG_F32)
+      run_batch<float>(sk, X, B, p, seeds, nullptr, o, static_cast<cudaStream_t>(stream));
+    else
+      run_batch<double>(sk, X, B, p, seeds, nullptr, o, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fstg_transform_with_samples_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p,
+                                      const int64_t* indices, int32_t* counts, int32_t* support, void* values,
+                                      int32_t* candidates, void* mu, void* stream) {
+  return guarded([&] {
+    if (!sk) throw InvalidArgument("null sketch");
+    if (indices == nullptr && B > 0) throw InvalidArgument("transform_with_samples: indices are null");
+    const Outputs o{counts, support, values, candidates, mu};
+    if (sk->dtype == FSTG_F32)
+      run_batch<float>(sk, X, B, p, nullptr, indices, o, static_cast<cudaStream_t>(stream));
+    else
+      run_batch<double>(sk, X, B, p, nullptr, indices, o, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fstg_profile_enable(int enable) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  g_prof_on = enable != 0;
+  return FSTG_OK;
+}
+
+int fstg_profile_reset(void) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  resolve_pending_locked();
+  g_prof.clear();
+  g_launches.store(0);
+  return FSTG_OK;
+}
+
+int fstg_profile_read(const char* name, double* ms, int64_t* launches) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  resolve_pending_locked();
+  auto it = g_prof.find(name ? name : "");
+  if (ms) *ms = it == g_prof.end() ? 0.0 : it->second.ms;
+  if (launches) *launches = it == g_prof.end() ? 0 : it->second.launches;
+  return FSTG_OK;
+}
+
+int fstg_launch_count(int64_t* launches) {
+  if (launches) *launches = g_launches.load();
+  return FSTG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// Launch wrappers of the sm_100a kernels (preprocess.cu, draw.cu, stream.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace fstg {
+
+// ---- preprocessing (preprocess.cu) ----
+cudaError_t launch_qtables(const uint32_t* revtab, int k, int64_t nbases, uint32_t* qplain, uint32_t* qtrans,
+                           cudaStream_t st);
+template <typename T>
+cudaError_t launch_fwht_sketch(int k, const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
+                               int64_t basis_begin, int64_t basis_end, T* cols, int64_t ldc, cudaStream_t st);
+template <typename T>
+cudaError_t launch_identity(const T* a, int64_t lda, int64_t m, int64_t n, int64_t d, int64_t nk, T* cols,
+                            int64_t ldc, cudaStream_t st);
+template <typename T>
+cudaError_t launch_row_norms(const T* a, int64_t lda, int64_t m, int64_t n, double* out, cudaStream_t st);
+
+// ---- draws (draw.cu) ----
+template <typename IdxT>
+cudaError_t launch_draw(const uint64_t* seeds, uint64_t seed_base, int64_t B, int64_t N, uint64_t L, IdxT* out,
+                        cudaStream_t st);
+cudaError_t launch_narrow_indices(const int64_t* in, int64_t count, int64_t L, uint32_t* out, int* bad,
+                                  cudaStream_t st);
+
+// ---- streaming estimator (stream.cu) ----
+template <typename T>
+struct StreamArgs {
+  // sketch
+  const T* cols;
+  int64_t ldc;  // column stride (elements), multiple of 16 bytes
+  const T* a;
+  int64_t lda;  // row stride of the embedded A (elements), multiple of 16 bytes
+  const uint32_t* qplain;
+  const uint32_t* qtrans;
+  const uint32_t* revtab;
+  int k;
+  int64_t d, L, m, n, kb;  // kb = (d/2)*d, first identity index
+  // params
+  int64_t J, K, N;
+  int64_t want;
+  double epsilon;
+  // batch
+  const T* X;
+  int64_t ldx;
+  const uint32_t* idx;  // B x N
+  int64_t B;
+  // outputs (device)
+  int32_t* counts;
+  int32_t* support;  // B x want
+  T* values;         // B x want
+  int32_t* cands;    // optional B x want
+  T* mu;             // optional B x m
+  // scratch: gridDim.x x K x m_pad batch means
+  T* means;
+  int64_t m_pad;
+  // pipeline
+  int stages;
+  int stage_stride;  // bytes between ring stages (>= one segment, 128-byte multiple)
+  int nseg;
+  int chunk;
+};
+
+template <typename T>
+cudaError_t launch_stream(const StreamArgs<T>& args, bool strict, int grid, cudaStream_t st);
+// Persistent grid size the stream kernel wants for this configuration.
+template <typename T>
+int stream_grid_size(const StreamArgs<T>& args, bool strict, int64_t B, size_t* smem_bytes, int* stages,
+                     int* stage_stride);
+
+}  // namespace fstg

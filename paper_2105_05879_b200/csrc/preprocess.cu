@@ -1,0 +1,373 @@
+// Preprocessing kernels: the Kerdock-sketch {A s_l} (reference sketch.hpp:144-211).
+//
+//  * qtable_kernel   — expands each basis' position-reversed Kerdock rows into
+//                      sign-bit tables Q_s(coords(pos)) (sketch.hpp:176-179,
+//                      kerdock.hpp:38-49), in two layouts: plain (bit pos%32 of
+//                      word pos/32) for the FWHT, and lane-transposed for the
+//                      streaming coefficient kernel.
+//  * fwht_sketch_kernel — per (row tile, basis range): sign-mask R rows of A,
+//                      one unnormalised FWHT per row in registers + one shared
+//                      memory transpose, written transposed into columns
+//                      s*d + w (sketch.hpp:180-196). Butterfly stages run in
+//                      the reference order h = 1, 2, 4, ... with (x+y, x-y)
+//                      (fwht.hpp:20-29), so fp64 output is bit-identical to the
+//                      reference and fp32 output to the same algorithm in fp32.
+//  * identity_kernel — column (d/2)*d + w = sqrt(d) * A[:, w] (sketch.hpp:200-208).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fst_common.cuh"
+#include "kernels.hpp"
+
+namespace fstg {
+
+// ---------------------------------------------------------------------------
+// Sign tables. One thread per (basis, 32-position word).
+// plain:  qplain[s * wpb + w]   bit b = Q_s(pos = 32 w + b)            (wpb = max(1, d/32))
+// trans:  qtrans[(s * tw + t) * 32 + lane] bit f = Q_s(pos = 128*(f/4 + 8 t) + 4*lane + f%4)
+//         (tw = d/1024 words per lane, d >= 128; f in [0,32) covers i = 8t..8t+7, e = 0..3)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int q_of_pos(const uint32_t* rev, int k, uint32_t pos) {
+  // Q_M(coords(pos)) evaluated on the position bits with reversed rows
+  // (stream.hpp:76-84, kerdock.hpp:38-49): sum_{a<b} R_ab pos_a pos_b.
+  int acc = 0;
+  for (uint32_t rest = pos; rest != 0; rest &= rest - 1) {
+    const int a = __ffs(rest) - 1;
+    const uint32_t above = (a + 1 >= 32) ? 0u : (~0u << (a + 1));
+    acc ^= __popc(rev[a] & pos & above) & 1;
+  }
+  (void)k;
+  return acc;
+}
+
+__global__ void qtable_kernel(const uint32_t* __restrict__ revtab, int k, int64_t nbases,
+                              uint32_t* __restrict__ qplain) {
+  const int64_t d = int64_t{1} << k;
+  const int64_t wpb = d >= 32 ? d / 32 : 1;
+  const int64_t total = nbases * wpb;
+  for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t s = g / wpb;
+    const uint32_t w = static_cast<uint32_t>(g % wpb);
+    uint32_t rev[16];
+#pragma unroll
+    for (int a = 0; a < 16; ++a) rev[a] = revtab[s * 16 + a];
+    uint32_t word = 0;
+    const int nbits = d >= 32 ? 32 : static_cast<int>(d);
+    for (int b = 0; b < nbits; ++b) word |= static_cast<uint32_t>(q_of_pos(rev, k, w * 32u + b)) << b;
+    qplain[s * wpb + w] = word;
+  }
+}
+
+// Lane-transposed layout for the streaming coefficient kernel (d >= 128):
+// word (s, t, lane), t < tw = max(1, d/1024): bit f <-> position
+// 128 * (8 t + f / 4) + 4 * lane + f % 4.
+__global__ void qtrans_kernel(const uint32_t* __restrict__ revtab, int k, int64_t nbases,
+                              uint32_t* __restrict__ qtrans) {
+  const int64_t d = int64_t{1} << k;
+  const int64_t tw = d >= 1024 ? d / 1024 : 1;
+  const int64_t total = nbases * tw * 32;
+  for (int64_t g = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; g < total; g += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t s = g / (tw * 32);
+    const uint32_t t = static_cast<uint32_t>((g / 32) % tw), lane = static_cast<uint32_t>(g % 32);
+    uint32_t rev[16];
+#pragma unroll
+    for (int a = 0; a < 16; ++a) rev[a] = revtab[s * 16 + a];
+    uint32_t word = 0;
+    for (int f = 0; f < 32; ++f) {
+      const uint32_t pos = 128u * (8u * t + static_cast<uint32_t>(f / 4)) + 4u * lane + static_cast<uint32_t>(f % 4);
+      if (pos < d) word |= static_cast<uint32_t>(q_of_pos(rev, k, pos)) << f;
+    }
+    qtrans[g] = word;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FWHT sketch kernel.
+// KB = k (even), E = 2^(KB/2) elements per thread per row, P = E threads per
+// row, R = NT / E rows per CTA. Phase 1: thread (r = tid / P, p = tid % P)
+// owns positions p*E + e (bits 0..KB/2-1 in registers). Phase 2: thread
+// (r = tid % R, q = tid / R) owns positions e*E + q (bits KB/2..KB-1).
+// ---------------------------------------------------------------------------
+template <typename T, int KB, int NT>
+struct FwhtCfg {
+  static constexpr int HALF = KB / 2;
+  static constexpr int E = 1 << HALF;
+  static constexpr int D = 1 << KB;
+  static constexpr int R = NT / E;
+  static constexpr int PAD = (R <= 32) ? (32 / R) : 1;
+  static constexpr int RS = D + PAD;  // row stride (elements) of the smem tile
+  static constexpr int SW = (E < 32 ? E : 32) - 1;
+  static constexpr size_t SMEM = size_t(R) * RS * sizeof(T);
+};
+
+template <typename T>
+__device__ __forceinline__ void bfly(T& x, T& y) {
+  const T a = x, b = y;
+  x = a + b;
+  y = a - b;
+}
+
+// Butterflies over register bits [0, HALF) in ascending bit order.
+template <typename T, int HALF>
+__device__ __forceinline__ void reg_fwht(T (&v)[1 << HALF]) {
+  constexpr int E = 1 << HALF;
+#pragma unroll
+  for (int hb = 0; hb < HALF; ++hb) {
+    const int h = 1 << hb;
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+      if ((i & h) == 0) bfly(v[i], v[i + h]);
+  }
+}
+
+// fp32 specialisation with packed FADD2 for stages h >= 2 (pairs (i, i+1)).
+template <>
+__device__ __forceinline__ void reg_fwht<float, 6>(float (&v)[64]) {
+  // stage h = 1 (scalar)
+#pragma unroll
+  for (int i = 0; i < 64; i += 2) bfly(v[i], v[i + 1]);
+#pragma unroll
+  for (int hb = 1; hb < 6; ++hb) {
+    const int h = 1 << hb;
+#pragma unroll
+    for (int i = 0; i < 64; i += 2) {
+      if ((i & h) == 0) {
+        const float2 x = make_float2(v[i], v[i + 1]);
+        const float2 y = make_float2(v[i + h], v[i + h + 1]);
+        const float2 s = __fadd2_rn(x, y);
+        const float2 d = __fadd2_rn(x, make_float2(-y.x, -y.y));
+        v[i] = s.x;
+        v[i + 1] = s.y;
+        v[i + h] = d.x;
+        v[i + h + 1] = d.y;
+      }
+    }
+  }
+}
+
+template <typename T, int KB, int NT>
+__global__ void __launch_bounds__(NT) fwht_sketch_kernel(const T* __restrict__ a, int64_t lda, int64_t m, int64_t n,
+                                                         const uint32_t* __restrict__ qplain, int64_t basis_begin,
+                                                         int64_t basis_end, int bases_per_cta, T* __restrict__ cols,
+                                                         int64_t ldc) {
+  using C = FwhtCfg<T, KB, NT>;
+  constexpr int E = C::E, R = C::R, RS = C::RS, D = C::D, SW = C::SW;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* tile = reinterpret_cast<T*>(smem_raw);
+
+  const int tid = threadIdx.x;
+  const int64_t i0 = int64_t(blockIdx.x) * R;
+  const int64_t s_first = basis_begin + int64_t(blockIdx.y) * bases_per_cta;
+  const int64_t s_last = min(basis_end, s_first + bases_per_cta);
+  const uint64_t pol_keep = policy_evict_last();
+  const uint64_t pol_stream = policy_evict_first();
+
+  // Phase-1 coordinates.
+  const int r1 = tid / E, p1 = tid % E;
+  const int64_t row1 = i0 + r1;
+  // Phase-2 coordinates.
+  const int r2 = tid % R, q2 = tid / R;
+  const int64_t row2 = i0 + r2;
+  constexpr int WPB = D >= 32 ? D / 32 : 1;
+
+  for (int64_t s = s_first; s < s_last; ++s) {
+    T v[E];
+    // ---- load + sign mask + zero padding (sketch.hpp:182-186) ----
+    uint32_t qw[(E + 31) / 32];
+    if constexpr (E >= 32) {
+#pragma unroll
+      for (int w = 0; w < E / 32; ++w) qw[w] = __ldg(qplain + s * WPB + (int64_t(p1) * E) / 32 + w);
+    } else {
+      const int64_t pos0 = int64_t(p1) * E;
+      qw[0] = (__ldg(qplain + s * WPB + pos0 / 32) >> (pos0 % 32));
+    }
+    if (row1 < m) {
+      const T* arow = a + row1 * lda;
+      const int64_t pos0 = int64_t(p1) * E;
+      if (pos0 + E <= n && (reinterpret_cast<uintptr_t>(arow + pos0) % 16) == 0) {
+        if constexpr (sizeof(T) == 4) {
+#pragma unroll
+          for (int e = 0; e < E; e += 4) {
+            const float4 f = ldg_f4_policy(reinterpret_cast<const float4*>(arow + pos0 + e), pol_keep);
+            v[e] = f.x;
+            v[e + 1] = f.y;
+            v[e + 2] = f.z;
+            v[e + 3] = f.w;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; e += 2) {
+            const double2 f = ldg_d2_policy(reinterpret_cast<const double2*>(arow + pos0 + e), pol_keep);
+            v[e] = f.x;
+            v[e + 1] = f.y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = (pos0 + e < n) ? arow[pos0 + e] : T(0);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = T(0);
+    }
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t bit = (qw[e / 32] >> (e % 32)) & 1u;
+      v[e] = bit ? -v[e] : v[e];  // sign[j] * a_ij with sign = +-1 (exact)
+    }
+    // ---- stages h = 1 .. E/2 in registers ----
+    reg_fwht<T, C::HALF>(v);
+    // ---- transpose through shared memory ----
+    __syncthreads();  // previous basis' phase-2 reads are done
+    {
+      T* dst = tile + r1 * RS + p1 * E;
+#pragma unroll
+      for (int e = 0; e < E; ++e) dst[e ^ (p1 & SW)] = v[e];
+    }
+    __syncthreads();
+    {
+      const T* src = tile + r2 * RS;
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = src[e * E + (q2 ^ (e & SW))];
+    }
+    // ---- stages h = E .. D/2 (register index bit j <-> position bit HALF + j) ----
+    reg_fwht<T, C::HALF>(v);
+    // ---- transposed write-back: column s*d + w, row i0 + r2 (sketch.hpp:191-196) ----
+    if (row2 < m) {
+      T* base = cols + (s * D) * ldc + row2;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int64_t w = int64_t(e) * E + q2;
+        if constexpr (sizeof(T) == 4)
+          stg_f32_policy(reinterpret_cast<float*>(base + w * ldc), static_cast<float>(v[e]), pol_stream);
+        else
+          stg_f64_policy(reinterpret_cast<double*>(base + w * ldc), static_cast<double>(v[e]), pol_stream);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Identity block: column nk*d + w = sqrt(d) * A[:, w] for w < n, zero for
+// n <= w < d. 32x32 tiles transposed through shared memory.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void identity_kernel(const T* __restrict__ a, int64_t lda, int64_t m, int64_t n, int64_t d,
+                                int64_t nk, T sqrt_d, T* __restrict__ cols, int64_t ldc) {
+  __shared__ T tile[32][33];
+  const int64_t w0 = int64_t(blockIdx.x) * 32, i0 = int64_t(blockIdx.y) * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t i = i0 + r, w = w0 + tx;
+    tile[r][tx] = (i < m && w < n) ? sqrt_d * a[i * lda + w] : T(0);
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t w = w0 + r, i = i0 + tx;
+    if (w < d && i < m) cols[(nk * d + w) * ldc + i] = tile[tx][r];
+  }
+}
+
+// Per-row 2-norm in double (sketch.hpp:126-131), one warp per row.
+template <typename T>
+__global__ void row_norm_kernel(const T* __restrict__ a, int64_t lda, int64_t m, int64_t n, double* __restrict__ out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
+  if (warp >= m) return;
+  double acc = 0;
+  for (int64_t j = lane; j < n; j += 32) {
+    const double v = static_cast<double>(a[int64_t(warp) * lda + j]);
+    acc += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[warp] = sqrt(acc);
+}
+
+// ----------------------------------------------------------------- launch --
+cudaError_t launch_qtables(const uint32_t* revtab, int k, int64_t nbases, uint32_t* qplain, uint32_t* qtrans,
+                           cudaStream_t st) {
+  const int64_t d = int64_t{1} << k;
+  const int threads = 256;
+  const int64_t cap = 148 * 64;
+  int64_t total = nbases * (d >= 32 ? d / 32 : 1);
+  int64_t blocks = (total + threads - 1) / threads;
+  qtable_kernel<<<static_cast<unsigned>(blocks < cap ? blocks : cap), threads, 0, st>>>(revtab, k, nbases, qplain);
+  if (qtrans != nullptr && d >= 128) {
+    total = nbases * (d >= 1024 ? d / 1024 : 1) * 32;
+    blocks = (total + threads - 1) / threads;
+    qtrans_kernel<<<static_cast<unsigned>(blocks < cap ? blocks : cap), threads, 0, st>>>(revtab, k, nbases, qtrans);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T, int KB>
+static cudaError_t launch_fwht_k(const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
+                                 int64_t b0, int64_t b1, T* cols, int64_t ldc, cudaStream_t st) {
+  constexpr int NT = (sizeof(T) == 8 && KB >= 12) ? 256 : ((KB >= 14) ? 256 : 512);
+  using C = FwhtCfg<T, KB, NT>;
+  static_assert(C::R >= 1, "rows per CTA");
+  auto kern = fwht_sketch_kernel<T, KB, NT>;
+  if (C::SMEM > 227 * 1024) return cudaErrorNotSupported;
+  if (C::SMEM > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    if (e != cudaSuccess) return e;
+  }
+  const int64_t nb = b1 - b0;
+  if (nb <= 0) return cudaSuccess;
+  const int64_t row_tiles = (m + C::R - 1) / C::R;
+  // Bases per CTA: enough CTAs for >= 4 waves, at most 16 bases each.
+  int bpc = 16;
+  while (bpc > 1 && row_tiles * ((nb + bpc - 1) / bpc) < 148 * 8) bpc /= 2;
+  const int64_t gy = (nb + bpc - 1) / bpc;
+  if (row_tiles > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
+  dim3 grid(static_cast<unsigned>(row_tiles), static_cast<unsigned>(gy));
+  kern<<<grid, NT, C::SMEM, st>>>(a, lda, m, n, qplain, b0, b1, bpc, cols, ldc);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_fwht_sketch(int k, const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
+                               int64_t b0, int64_t b1, T* cols, int64_t ldc, cudaStream_t st) {
+  switch (k) {
+    case 2: return launch_fwht_k<T, 2>(a, lda, m, n, qplain, b0, b1, cols, ldc, st);
+    case 4: return launch_fwht_k<T, 4>(a, lda, m, n, qplain, b0, b1, cols, ldc, st);
+    case 6: return launch_fwht_k<T, 6>(a, lda, m, n, qplain, b0, b1, cols, ldc, st);
+    case 8: return launch_fwht_k<T, 8>(a, lda, m, n, qplain, b0, b1, cols, ldc, st);
+    case 10: return launch_fwht_k<T, 10>(a, lda, m, n, qplain, b0, b1, cols, ldc, st);
+    case 12: return launch_fwht_k<T, 12>(a, lda, m, n, qplain, b0, b1, cols, ldc, st);
+    case 14: return launch_fwht_k<T, 14>(a, lda, m, n, qplain, b0, b1, cols, ldc, st);
+    default: return cudaErrorNotSupported;
+  }
+}
+
+template <typename T>
+cudaError_t launch_identity(const T* a, int64_t lda, int64_t m, int64_t n, int64_t d, int64_t nk, T* cols,
+                            int64_t ldc, cudaStream_t st) {
+  const T sqrt_d = static_cast<T>(sqrt(static_cast<double>(d)));
+  dim3 grid(static_cast<unsigned>((d + 31) / 32), static_cast<unsigned>((m + 31) / 32));
+  if (grid.y > 65535) return cudaErrorInvalidConfiguration;
+  identity_kernel<T><<<grid, dim3(32, 8), 0, st>>>(a, lda, m, n, d, nk, sqrt_d, cols, ldc);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_row_norms(const T* a, int64_t lda, int64_t m, int64_t n, double* out, cudaStream_t st) {
+  const int threads = 256;
+  const int64_t blocks = (m * 32 + threads - 1) / threads;
+  row_norm_kernel<T><<<static_cast<unsigned>(blocks), threads, 0, st>>>(a, lda, m, n, out);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_fwht_sketch<float>(int, const float*, int64_t, int64_t, int64_t, const uint32_t*,
+                                               int64_t, int64_t, float*, int64_t, cudaStream_t);
+template cudaError_t launch_fwht_sketch<double>(int, const double*, int64_t, int64_t, int64_t, const uint32_t*,
+                                                int64_t, int64_t, double*, int64_t, cudaStream_t);
+template cudaError_t launch_identity<float>(const float*, int64_t, int64_t, int64_t, int64_t, int64_t, float*,
+                                            int64_t, cudaStream_t);
+template cudaError_t launch_identity<double>(const double*, int64_t, int64_t, int64_t, int64_t, int64_t, double*,
+                                             int64_t, cudaStream_t);
+template cudaError_t launch_row_norms<float>(const float*, int64_t, int64_t, int64_t, double*, cudaStream_t);
+template cudaError_t launch_row_norms<double>(const double*, int64_t, int64_t, int64_t, double*, cudaStream_t);
+
+}  // namespace fstg

@@ -1,0 +1,653 @@
+// Fused streaming estimator + support refinement (reference stream.hpp:197-268).
+//
+// One persistent CTA works through vectors v = blockIdx.x, += gridDim.x.
+// Warp roles:
+//   * producer warp (last warp, one elected lane): streams the sampled sketch
+//     columns C[:, ell_j] (16 KiB segments) HBM -> shared memory with 1-D bulk
+//     copies (cp.async.bulk, SASS UBLKCP) into an S-stage ring guarded by
+//     full/empty mbarriers; it runs ahead across vector boundaries and marks
+//     the stream evict-first in L2.
+//   * consumer warps (NC threads): per chunk of samples compute the sample
+//     coefficients t_j = s_ell^T x (stream.hpp:89-103, 218-229) from the
+//     lane-transposed Kerdock sign tables and x in shared memory; then
+//     accumulate the per-batch running sums acc += t_j * C[:, ell_j]
+//     (stream.hpp:231-234) in registers, divide by J (stream.hpp:237), take
+//     the entrywise median of the K batch means (stream.hpp:126-143), select
+//     the `want` largest |mu| with ties to the smaller index by an MSB radix
+//     select plus an index-ordered ballot scan (stream.hpp:245-257), refine
+//     the candidates with exact fp64-accumulated row dots of A (kept
+//     L2-resident with an evict-last policy; stream.hpp:259-266) and compact
+//     the surviving (|v| >= eps) support in order.
+// STRICT mode reproduces the reference's operation order exactly: Gray-code
+// sequential coefficient sums and separately-rounded multiply/add.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fst_common.cuh"
+#include "kernels.hpp"
+
+namespace fstg {
+
+constexpr int kNC = 256;                    // consumer threads
+constexpr int kNCW = kNC / 32;              // consumer warps
+constexpr int kThreads = kNC + 32;          // + producer warp
+constexpr int kSegBytes = 16384;            // one ring stage at most
+constexpr int kRingBytes = 65536;           // ring budget
+constexpr int kMaxStages = 64;
+constexpr int kChunk = 256;                 // samples per coefficient chunk
+
+template <typename T>
+struct KeyOf;
+template <>
+struct KeyOf<float> {
+  using K = uint32_t;
+  static constexpr int BITS = 32;
+  __device__ static K key(float v) { return __float_as_uint(v) & 0x7fffffffu; }
+};
+template <>
+struct KeyOf<double> {
+  using K = unsigned long long;
+  static constexpr int BITS = 64;
+  __device__ static K key(double v) { return static_cast<K>(__double_as_longlong(v)) & 0x7fffffffffffffffull; }
+};
+
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+  static constexpr int N = 4;
+  using V = float4;
+  __device__ static void get(const V& v, float (&o)[4]) {
+    o[0] = v.x;
+    o[1] = v.y;
+    o[2] = v.z;
+    o[3] = v.w;
+  }
+};
+template <>
+struct Vec<double> {
+  static constexpr int N = 2;
+  using V = double2;
+  __device__ static void get(const V& v, double (&o)[2]) {
+    o[0] = v.x;
+    o[1] = v.y;
+  }
+};
+
+struct SmemLayout {
+  size_t ring, x, tbuf, ibuf, bars, hist, scan, misc, cand, cval, cflag, total;
+};
+
+template <typename T>
+__host__ __device__ inline SmemLayout smem_layout(int64_t d, int stages, int stage_stride, int64_t want) {
+  SmemLayout L{};
+  size_t off = 0;
+  auto take = [&off](size_t bytes, size_t align) {
+    off = (off + align - 1) / align * align;
+    const size_t at = off;
+    off += bytes;
+    return at;
+  };
+  L.ring = take(size_t(stages) * stage_stride, 1024);
+  L.x = take(size_t(d < 4 ? 4 : d) * sizeof(T), 16);
+  L.tbuf = take(kChunk * sizeof(T), 16);
+  L.ibuf = take(kChunk * sizeof(uint32_t), 16);
+  L.bars = take(2 * kMaxStages * sizeof(uint64_t), 8);
+  L.hist = take(256 * sizeof(uint32_t), 16);
+  L.scan = take(2 * 32 * sizeof(uint32_t), 16);
+  L.misc = take(16 * sizeof(unsigned long long), 16);
+  L.cand = take(size_t(want) * sizeof(int32_t), 16);
+  L.cval = take(size_t(want) * sizeof(T), 16);
+  L.cflag = take(size_t(want) * sizeof(uint8_t), 16);
+  L.total = (off + 15) / 16 * 16;
+  return L;
+}
+
+// Block-wide (consumer threads only) exclusive scan of a uint32 value.
+// Returns the exclusive prefix; *total gets the sum over all consumers.
+__device__ __forceinline__ uint32_t consumer_scan(uint32_t v, uint32_t* scan_smem, int parity, uint32_t* total) {
+  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  uint32_t* tot = scan_smem + parity * 32;
+  if (lane == 31) tot[warp] = inc;
+  named_bar_sync(1, kNC);
+  uint32_t wpre = 0, all = 0;
+#pragma unroll
+  for (int w = 0; w < kNCW; ++w) {
+    const uint32_t t = tot[w];
+    wpre += (w < warp) ? t : 0u;
+    all += t;
+  }
+  *total = all;
+  return wpre + inc - v;
+}
+
+// ------------------------------------------------ sample coefficients ----
+// Fast path (d >= 128): lane owns positions 128 i + 4 lane + e; the sign of
+// x[pos] in s_ell is Q_s(pos) ^ parity(w & pos) (kerdock.hpp:132-152).
+template <typename T>
+__device__ __forceinline__ T coeff_fast(const StreamArgs<T>& A, const T* xs, const uint32_t* wbase, uint32_t ell,
+                                        int lane) {
+  if (static_cast<int64_t>(ell) >= A.kb) {
+    const int64_t pos = static_cast<int64_t>(ell) - A.kb;
+    return pos < A.n ? static_cast<T>(sqrt(static_cast<double>(A.d))) * xs[pos] : T(0);
+  }
+  const uint32_t s = ell >> A.k, w = ell & static_cast<uint32_t>(A.d - 1);
+  const uint32_t wlo = w & 3u, wmid = (w >> 2) & 31u, whi = w >> 7;
+  const uint32_t lanebit = __popc(wmid & static_cast<uint32_t>(lane)) & 1u;
+  const uint32_t base = wbase[((whi & 7u) << 2) | wlo];
+  const int64_t rows128 = A.d / 128;  // i in [0, d/128)
+  const int tw = static_cast<int>(A.d >= 1024 ? A.d / 1024 : 1);
+  const uint32_t* q = A.qtrans + (static_cast<int64_t>(s) * tw) * 32 + lane;
+  T acc = T(0);
+  for (int t = 0; t < tw; ++t) {
+    const uint32_t hiflip = __popc(whi & (8u * t)) & 1u;
+    const uint32_t M = __ldg(q + t * 32) ^ base ^ ((hiflip ^ lanebit) ? 0xffffffffu : 0u);
+#pragma unroll
+    for (int ip = 0; ip < 8; ++ip) {
+      const int64_t i = 8 * t + ip;
+      if (i < rows128) {
+        const T* xp = xs + 128 * i + 4 * lane;
+        if constexpr (sizeof(T) == 4) {
+          const float4 xv = *reinterpret_cast<const float4*>(xp);
+          acc += __uint_as_float(__float_as_uint(xv.x) ^ ((M << (31 - (4 * ip + 0))) & 0x80000000u));
+          acc += __uint_as_float(__float_as_uint(xv.y) ^ ((M << (31 - (4 * ip + 1))) & 0x80000000u));
+          acc += __uint_as_float(__float_as_uint(xv.z) ^ ((M << (31 - (4 * ip + 2))) & 0x80000000u));
+          acc += __uint_as_float(__float_as_uint(xv.w) ^ ((M << (31 - (4 * ip + 3))) & 0x80000000u));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const T xvv = xp[e];
+            acc += ((M >> (4 * ip + e)) & 1u) ? -xvv : xvv;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+// Generic warp path (any d): lane owns positions lane + 32 r.
+template <typename T>
+__device__ __forceinline__ T coeff_generic(const StreamArgs<T>& A, const T* xs, uint32_t ell, int lane) {
+  if (static_cast<int64_t>(ell) >= A.kb) {
+    const int64_t pos = static_cast<int64_t>(ell) - A.kb;
+    return pos < A.n ? static_cast<T>(sqrt(static_cast<double>(A.d))) * xs[pos] : T(0);
+  }
+  const uint32_t s = ell >> A.k, w = ell & static_cast<uint32_t>(A.d - 1);
+  const int64_t wpb = A.d >= 32 ? A.d / 32 : 1;
+  T acc = T(0);
+  for (int64_t pos = lane; pos < A.d; pos += 32) {
+    const uint32_t qb = (__ldg(A.qplain + s * wpb + pos / 32) >> (pos % 32)) & 1u;
+    const uint32_t sg = qb ^ (__popc(w & static_cast<uint32_t>(pos)) & 1u);
+    const T xv = xs[pos];
+    acc += sg ? -xv : xv;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+// Strict path: one thread, Gray-code walk in the reference's order
+// (stream.hpp:89-103), separately rounded adds.
+template <typename T>
+__device__ __forceinline__ T coeff_strict(const StreamArgs<T>& A, const T* xs, uint32_t ell) {
+  if (static_cast<int64_t>(ell) >= A.kb) {
+    const int64_t pos = static_cast<int64_t>(ell) - A.kb;
+    const T sqrt_d = static_cast<T>(sqrt(static_cast<double>(A.d)));
+    return pos < A.n ? (sizeof(T) == 8 ? T(__dmul_rn(double(sqrt_d), double(xs[pos])))
+                                       : T(__fmul_rn(float(sqrt_d), float(xs[pos]))))
+                     : T(0);
+  }
+  const uint32_t s = ell >> A.k, wpos = ell & static_cast<uint32_t>(A.d - 1);
+  uint32_t rev[16];
+#pragma unroll
+  for (int a = 0; a < 16; ++a) rev[a] = __ldg(A.revtab + static_cast<int64_t>(s) * 16 + a);
+  T acc = T(0);
+  uint32_t pos = 0;
+  uint32_t sign = 0;
+  const uint32_t d = static_cast<uint32_t>(A.d);
+  for (uint32_t t = 0;; ++t) {
+    if (static_cast<int64_t>(pos) < A.n) {
+      const T xv = xs[pos];
+      if constexpr (sizeof(T) == 8)
+        acc = __dadd_rn(acc, sign ? -xv : xv);
+      else
+        acc = __fadd_rn(acc, sign ? -xv : xv);
+    }
+    if (t + 1 == d) break;
+    const int b = __ffs(t + 1) - 1;
+    sign ^= __popc(rev[b] & pos) & 1u;
+    sign ^= (wpos >> b) & 1u;
+    pos ^= 1u << b;
+  }
+  return acc;
+}
+
+// --------------------------------------------------------------- kernel ----
+template <typename T, bool STRICT, int NSEG>
+__global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T> A) {
+  using KT = typename KeyOf<T>::K;
+  constexpr int VEC = Vec<T>::N;
+  constexpr int SEG = kSegBytes / static_cast<int>(sizeof(T));  // rows per segment
+  constexpr int CPS = SEG / VEC;                                  // 16-byte chunks per segment
+  constexpr int CPT = CPS / kNC;                                  // chunks per consumer thread per segment
+
+  extern __shared__ __align__(1024) unsigned char smem[];
+  const SmemLayout Ls = smem_layout<T>(A.d, A.stages, A.stage_stride, A.want);
+  unsigned char* ring = smem + Ls.ring;
+  T* xs = reinterpret_cast<T*>(smem + Ls.x);
+  T* tbuf = reinterpret_cast<T*>(smem + Ls.tbuf);
+  uint32_t* ibuf = reinterpret_cast<uint32_t*>(smem + Ls.ibuf);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + Ls.bars);
+  uint64_t* empty = full + kMaxStages;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(smem + Ls.hist);
+  uint32_t* scan = reinterpret_cast<uint32_t*>(smem + Ls.scan);
+  unsigned long long* misc = reinterpret_cast<unsigned long long*>(smem + Ls.misc);
+  int32_t* cand = reinterpret_cast<int32_t*>(smem + Ls.cand);
+  T* cval = reinterpret_cast<T*>(smem + Ls.cval);
+  uint8_t* cflag = reinterpret_cast<uint8_t*>(smem + Ls.cflag);
+  __shared__ uint32_t wbase[32];
+
+  const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+  const int S = A.stages;
+  const int64_t seg_last_rows = A.m_pad - int64_t(A.nseg - 1) * SEG;
+  const uint32_t stage_bytes_full = static_cast<uint32_t>((A.nseg > 1 ? SEG : A.m_pad) * sizeof(T));
+  const uint32_t stage_bytes_last = static_cast<uint32_t>(seg_last_rows * sizeof(T));
+
+  if (tid < S) {
+    mbar_init(&full[tid], 1);
+    mbar_init(&empty[tid], kNCW);
+  }
+  if (tid < 32) {
+    // Walsh base masks: bit f (i' = f/4, e = f%4) = parity(hi3 & i') ^ parity(lo2 & e).
+    const uint32_t hi3 = static_cast<uint32_t>(tid) >> 2, lo2 = static_cast<uint32_t>(tid) & 3u;
+    uint32_t m = 0;
+    for (int f = 0; f < 32; ++f)
+      m |= static_cast<uint32_t>((__popc(hi3 & static_cast<uint32_t>(f >> 2)) ^ __popc(lo2 & static_cast<uint32_t>(f & 3))) & 1) << f;
+    wbase[tid] = m;
+  }
+  fence_mbar_init();
+  __syncthreads();
+
+  if (warp == kNCW) {
+    // ======================= producer warp =======================
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      uint64_t g = 0;
+      for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x) {
+        const uint32_t* vidx = A.idx + v * A.N;
+        for (int64_t j = 0; j < A.N; ++j) {
+          const T* col = A.cols + static_cast<int64_t>(__ldg(vidx + j)) * A.ldc;
+          for (int sg = 0; sg < A.nseg; ++sg, ++g) {
+            const int stage = static_cast<int>(g % S);
+            const uint64_t u = g / S;
+            if (u > 0) mbar_wait(&empty[stage], static_cast<uint32_t>((u - 1) & 1));
+            const uint32_t bytes = (sg == A.nseg - 1) ? stage_bytes_last : stage_bytes_full;
+            mbar_arrive_expect_tx(&full[stage], bytes);
+            bulk_g2s(ring + size_t(stage) * A.stage_stride, col + int64_t(sg) * SEG, bytes, &full[stage], pol);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ======================= consumer warps =======================
+  const uint64_t pol_keep = policy_evict_last();
+  const T sqrt_dummy = T(0);
+  (void)sqrt_dummy;
+  uint64_t g = 0;
+  T* means = A.means + int64_t(blockIdx.x) * A.K * A.m_pad;
+
+  for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x) {
+    // ---- x into shared memory, zero padded to d ----
+    const T* xv = A.X + v * A.ldx;
+    for (int64_t p = tid; p < A.d; p += kNC) xs[p] = (p < A.n) ? xv[p] : T(0);
+
+    T acc[NSEG][CPT][VEC];
+#pragma unroll
+    for (int sg = 0; sg < NSEG; ++sg)
+#pragma unroll
+      for (int c = 0; c < CPT; ++c)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[sg][c][e] = T(0);
+
+    const uint32_t* vidx = A.idx + v * A.N;
+    for (int64_t c0 = 0; c0 < A.N; c0 += kChunk) {
+      const int cn = static_cast<int>((A.N - c0) < kChunk ? (A.N - c0) : kChunk);
+      for (int i = tid; i < cn; i += kNC) ibuf[i] = __ldg(vidx + c0 + i);
+      named_bar_sync(1, kNC);  // ibuf + xs ready; previous chunk fully consumed
+      // ---- sample coefficients t_j ----
+      if constexpr (STRICT) {
+        for (int i = tid; i < cn; i += kNC) tbuf[i] = coeff_strict<T>(A, xs, ibuf[i]);
+      } else {
+        if (A.d >= 128) {
+          for (int i = warp; i < cn; i += kNCW) {
+            const T t = coeff_fast<T>(A, xs, wbase, ibuf[i], lane);
+            if (lane == 0) tbuf[i] = t;
+          }
+        } else {
+          for (int i = warp; i < cn; i += kNCW) {
+            const T t = coeff_generic<T>(A, xs, ibuf[i], lane);
+            if (lane == 0) tbuf[i] = t;
+          }
+        }
+      }
+      named_bar_sync(1, kNC);
+      // ---- accumulate t_j * C[:, ell_j] over the ring ----
+      for (int i = 0; i < cn; ++i) {
+        const T t = tbuf[i];
+        const int64_t j = c0 + i;
+#pragma unroll
+        for (int sg = 0; sg < NSEG; ++sg) {
+          if (sg < A.nseg) {
+            const int stage = static_cast<int>(g % S);
+            mbar_wait(&full[stage], static_cast<uint32_t>((g / S) & 1));
+            const typename Vec<T>::V* src = reinterpret_cast<const typename Vec<T>::V*>(ring + size_t(stage) * A.stage_stride);
+            const int64_t rows_here = (sg == A.nseg - 1) ? seg_last_rows : SEG;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+              const int chunk = tid + c * kNC;
+              if (int64_t(chunk) * VEC < rows_here) {
+                T vv[VEC];
+                Vec<T>::get(src[chunk], vv);
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) {
+                  if constexpr (STRICT) {
+                    if constexpr (sizeof(T) == 8)
+                      acc[sg][c][e] = __dadd_rn(acc[sg][c][e], __dmul_rn(t, vv[e]));
+                    else
+                      acc[sg][c][e] = __fadd_rn(acc[sg][c][e], __fmul_rn(t, vv[e]));
+                  } else {
+                    acc[sg][c][e] = fma(t, vv[e], acc[sg][c][e]);
+                  }
+                }
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            ++g;
+          }
+        }
+        if ((j + 1) % A.J == 0) {
+          // batch b complete: mean = sum / J (IEEE division, stream.hpp:237)
+          const int64_t b = j / A.J;
+          T* mb = means + b * A.m_pad;
+          const T Jt = static_cast<T>(A.J);
+#pragma unroll
+          for (int sg = 0; sg < NSEG; ++sg)
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+              const int64_t row0 = int64_t(sg) * SEG + int64_t(tid + c * kNC) * VEC;
+              if (sg < A.nseg && row0 < A.m_pad) {
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) {
+                  mb[row0 + e] = acc[sg][c][e] / Jt;
+                  acc[sg][c][e] = T(0);
+                }
+              }
+            }
+        }
+      }
+    }
+
+    // ---- median of the K batch means (stream.hpp:126-143), keys |mu| ----
+    KT keys[NSEG][CPT][VEC];
+    T muv[NSEG][CPT][VEC];
+#pragma unroll
+    for (int sg = 0; sg < NSEG; ++sg)
+#pragma unroll
+      for (int c = 0; c < CPT; ++c)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const int64_t row = int64_t(sg) * SEG + int64_t(tid + c * kNC) * VEC + e;
+          T mu = T(0);
+          KT key = 0;
+          if (sg < A.nseg && row < A.m) {
+            if (A.K == 1) {
+              mu = means[row];
+            } else if (A.K == 2) {
+              const T x0 = means[row], x1 = means[A.m_pad + row];
+              const T lo = x0 < x1 ? x0 : x1, hi = x0 < x1 ? x1 : x0;
+              mu = T(0.5) * (lo + hi);
+            } else {
+              // rank selection of order statistics K/2 (and K/2-1 for even K)
+              const int64_t hK = A.K / 2;
+              T up = T(0), lo = T(0);
+              for (int64_t i = 0; i < A.K; ++i) {
+                const T xi = means[i * A.m_pad + row];
+                int64_t rank = 0;
+                for (int64_t q = 0; q < A.K; ++q) {
+                  const T xq = means[q * A.m_pad + row];
+                  rank += (xq < xi || (xq == xi && q < i)) ? 1 : 0;
+                }
+                if (rank == hK) up = xi;
+                if (rank == hK - 1) lo = xi;
+              }
+              mu = (A.K % 2 == 1) ? up : T(0.5) * (lo + up);
+            }
+            key = KeyOf<T>::key(mu);
+          }
+          muv[sg][c][e] = mu;
+          keys[sg][c][e] = key;
+          if (A.mu != nullptr && sg < A.nseg && row < A.m) A.mu[v * A.m + row] = mu;
+        }
+
+    // ---- MSB radix select of the want-th largest key ----
+    KT prefix = 0, kmask = 0;
+    int64_t remaining = A.want;
+    for (int shift = KeyOf<T>::BITS - 8; shift >= 0; shift -= 8) {
+      hist[tid] = 0;  // kNC == 256 bins
+      named_bar_sync(1, kNC);
+#pragma unroll
+      for (int sg = 0; sg < NSEG; ++sg)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const int64_t row = int64_t(sg) * SEG + int64_t(tid + c * kNC) * VEC + e;
+            const bool act = (sg < A.nseg) && (row < A.m) && ((keys[sg][c][e] & kmask) == prefix);
+            const uint32_t digit = static_cast<uint32_t>((keys[sg][c][e] >> shift) & 0xffu);
+            const uint32_t am = __ballot_sync(0xffffffffu, act);
+            if (act) {
+              const uint32_t peers = __match_any_sync(am, digit);
+              if (lane == __ffs(peers) - 1) atomicAdd(&hist[digit], static_cast<uint32_t>(__popc(peers)));
+            }
+          }
+      named_bar_sync(1, kNC);
+      if (warp == 0) {
+        // lane l owns bins [255-8l-7, 255-8l], scanned from the top digit down
+        uint32_t h[8], sum = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          h[b] = hist[255 - 8 * lane - b];
+          sum += h[b];
+        }
+        uint32_t inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += y;
+        }
+        const uint32_t exc = inc - sum;
+        const bool here = exc < static_cast<uint32_t>(remaining) && inc >= static_cast<uint32_t>(remaining);
+        if (here) {
+          uint32_t cum = exc;
+          int b = 0;
+          for (; b < 8; ++b) {
+            if (cum + h[b] >= static_cast<uint32_t>(remaining)) break;
+            cum += h[b];
+          }
+          misc[0] = static_cast<unsigned long long>(255 - 8 * lane - b);
+          misc[1] = static_cast<unsigned long long>(remaining - cum);
+        }
+      }
+      named_bar_sync(1, kNC);
+      const KT dg = static_cast<KT>(misc[0]);
+      remaining = static_cast<int64_t>(misc[1]);
+      prefix |= dg << shift;
+      kmask |= static_cast<KT>(0xff) << shift;
+    }
+    // prefix = threshold key T; `remaining` keys equal to T are taken (smallest indices first).
+    const KT thr = prefix;
+    const uint32_t quota = static_cast<uint32_t>(remaining);
+
+    // ---- index-ordered compaction of the candidate set (sorted ascending) ----
+    uint32_t base_gt = 0, base_eq = 0;
+    int parity = 0;
+#pragma unroll
+    for (int sg = 0; sg < NSEG; ++sg)
+#pragma unroll
+      for (int c = 0; c < CPT; ++c) {
+        if (sg < A.nseg) {
+          uint32_t ngt = 0, neq = 0;
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const int64_t row = int64_t(sg) * SEG + int64_t(tid + c * kNC) * VEC + e;
+            if (row < A.m) {
+              ngt += keys[sg][c][e] > thr;
+              neq += keys[sg][c][e] == thr;
+            }
+          }
+          uint32_t total;
+          const uint32_t pre = consumer_scan((neq << 16) | ngt, scan, parity, &total);
+          parity ^= 1;
+          uint32_t gt_before = base_gt + (pre & 0xffffu), eq_before = base_eq + (pre >> 16);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const int64_t row = int64_t(sg) * SEG + int64_t(tid + c * kNC) * VEC + e;
+            if (row < A.m) {
+              const KT kk = keys[sg][c][e];
+              if (kk > thr) {
+                cand[gt_before + (eq_before < quota ? eq_before : quota)] = static_cast<int32_t>(row);
+                ++gt_before;
+              } else if (kk == thr) {
+                if (eq_before < quota) cand[gt_before + eq_before] = static_cast<int32_t>(row);
+                ++eq_before;
+              }
+            }
+          }
+          base_gt += total & 0xffffu;
+          base_eq += total >> 16;
+        }
+      }
+    named_bar_sync(1, kNC);
+
+    // ---- refinement: v_i = a_i . x, fp64 accumulation (stream.hpp:259-266) ----
+    for (int64_t ci = warp; ci < A.want; ci += kNCW) {
+      const int64_t row = cand[ci];
+      const T* arow = A.a + row * A.lda;
+      double dot = 0.0;
+      if constexpr (sizeof(T) == 4) {
+        const int64_t nv = (A.n + 3) / 4;
+        const float4* a4 = reinterpret_cast<const float4*>(arow);
+        const float4* x4 = reinterpret_cast<const float4*>(xs);
+        for (int64_t q = lane; q < nv; q += 32) {
+          const float4 av = ldg_f4_policy(a4 + q, pol_keep);
+          const float4 xv4 = x4[q];
+          dot = fma(static_cast<double>(av.x), static_cast<double>(xv4.x), dot);
+          dot = fma(static_cast<double>(av.y), static_cast<double>(xv4.y), dot);
+          dot = fma(static_cast<double>(av.z), static_cast<double>(xv4.z), dot);
+          dot = fma(static_cast<double>(av.w), static_cast<double>(xv4.w), dot);
+        }
+      } else {
+        const int64_t nv = (A.n + 1) / 2;
+        const double2* a2 = reinterpret_cast<const double2*>(arow);
+        const double2* x2 = reinterpret_cast<const double2*>(xs);
+        for (int64_t q = lane; q < nv; q += 32) {
+          const double2 av = ldg_d2_policy(a2 + q, pol_keep);
+          const double2 xv2 = x2[q];
+          dot = fma(av.x, xv2.x, dot);
+          dot = fma(av.y, xv2.y, dot);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      if (lane == 0) {
+        cval[ci] = static_cast<T>(dot);
+        cflag[ci] = fabs(dot) >= A.epsilon ? 1 : 0;
+      }
+    }
+    named_bar_sync(1, kNC);
+
+    // ---- ordered compaction of the support ----
+    uint32_t out_base = 0;
+    for (int64_t c0 = 0; c0 < A.want; c0 += kNC) {
+      const int64_t ci = c0 + tid;
+      const uint32_t f = (ci < A.want) ? cflag[ci] : 0u;
+      uint32_t total;
+      const uint32_t pre = consumer_scan(f, scan, parity, &total);
+      parity ^= 1;
+      if (f) {
+        const int64_t o = v * A.want + out_base + pre;
+        A.support[o] = cand[ci];
+        A.values[o] = cval[ci];
+      }
+      if (A.cands != nullptr && ci < A.want) A.cands[v * A.want + ci] = cand[ci];
+      out_base += total;
+    }
+    if (tid == 0) A.counts[v] = static_cast<int32_t>(out_base);
+    named_bar_sync(1, kNC);  // cand/cval/xs reuse by the next vector
+  }
+}
+
+// ------------------------------------------------------------- launching --
+template <typename T>
+int stream_grid_size(const StreamArgs<T>& args, bool strict, int64_t B, size_t* smem_bytes, int* stages,
+                     int* stage_stride) {
+  const int64_t stage_bytes = (args.m_pad * int64_t(sizeof(T)) < kSegBytes) ? args.m_pad * int64_t(sizeof(T)) : kSegBytes;
+  const int stride = static_cast<int>((stage_bytes + 127) / 128 * 128);
+  int S = static_cast<int>(kRingBytes / stride);
+  if (S > kMaxStages) S = kMaxStages;
+  if (S < 2) S = 2;
+  const SmemLayout L = smem_layout<T>(args.d, S, stride, args.want);
+  *smem_bytes = L.total;
+  *stages = S;
+  *stage_stride = stride;
+  (void)strict;
+  int per_sm = (L.total <= 100 * 1024) ? 2 : 1;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = int64_t(sms) * per_sm;
+  if (grid > B) grid = B;
+  if (grid < 1) grid = 1;
+  return static_cast<int>(grid);
+}
+
+template <typename T, bool STRICT, int NSEG>
+static cudaError_t launch_one(const StreamArgs<T>& args, int grid, size_t smem, cudaStream_t st) {
+  auto kern = stream_kernel<T, STRICT, NSEG>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  kern<<<grid, kThreads, smem, st>>>(args);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_stream(const StreamArgs<T>& args, bool strict, int grid, cudaStream_t st) {
+  const SmemLayout L = smem_layout<T>(args.d, args.stages, args.stage_stride, args.want);
+  if (L.total > 227 * 1024) return cudaErrorInvalidConfiguration;
+  if (args.nseg <= 1) {
+    return strict ? launch_one<T, true, 1>(args, grid, L.total, st) : launch_one<T, false, 1>(args, grid, L.total, st);
+  }
+  if (args.nseg <= 4) {
+    return strict ? launch_one<T, true, 4>(args, grid, L.total, st) : launch_one<T, false, 4>(args, grid, L.total, st);
+  }
+  return cudaErrorNotSupported;
+}
+
+template cudaError_t launch_stream<float>(const StreamArgs<float>&, bool, int, cudaStream_t);
+template cudaError_t launch_stream<double>(const StreamArgs<double>&, bool, int, cudaStream_t);
+template int stream_grid_size<float>(const StreamArgs<float>&, bool, int64_t, size_t*, int*, int*);
+template int stream_grid_size<double>(const StreamArgs<double>&, bool, int64_t, size_t*, int*, int*);
+
+}  // namespace fstg

@@ -1,0 +1,437 @@
+"""Python mirror of the reference ``fst`` API for the thresholded-Ax hot path.
+
+Same names, argument meaning and error behaviour as
+/root/reference/proj/include/fst/{sketch,stream}.hpp — ``preprocess``,
+``Sketch``, ``StreamParams``, ``choose_params``, ``draw_samples``,
+``transform``, ``transform_with_samples``, ``TransformResult`` — plus the
+batched stream entry point ``transform_batch`` the GPU is built around. Every
+call goes through the C-ABI in ``include/fst_b200.h`` (libfst_b200.so, sm_100a
+kernels). There is no CPU fallback: without the built library or a B200 the
+calls raise.
+
+Exception mapping (reference -> Python): std::invalid_argument -> ValueError,
+std::out_of_range -> IndexError, std::overflow_error -> OverflowError,
+std::runtime_error (allocation) -> MemoryError, CUDA failure -> CudaError,
+unsupported shape -> NotSupportedError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfst_b200.so")
+
+F32, F64 = 0, 1
+MODE_DEFAULT, MODE_FAST, MODE_STRICT = 0, 1, 2
+
+
+class CudaError(RuntimeError):
+    """CUDA runtime failure or no sm_100 device (no CPU fallback exists)."""
+
+
+class NotSupportedError(RuntimeError):
+    """Shape outside this build's GPU limits."""
+
+
+_ERRORS = {1: ValueError, 2: IndexError, 3: OverflowError, 4: MemoryError, 5: CudaError, 6: NotSupportedError}
+
+
+class _Params(C.Structure):
+    _fields_ = [("epsilon", C.c_double), ("delta", C.c_double), ("s", C.c_int64), ("J", C.c_int64),
+                ("K", C.c_int64), ("widen", C.c_int64), ("seed", C.c_uint64), ("mode", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+class _Info(C.Structure):
+    _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("d", C.c_int64), ("L", C.c_int64), ("k", C.c_int32),
+                ("dtype", C.c_int32), ("row_norm_max", C.c_double), ("device", C.c_int32),
+                ("reserved", C.c_int32), ("column_stride", C.c_int64), ("device_bytes", C.c_uint64),
+                ("preprocess_ms", C.c_double)]
+
+
+_lib = None
+
+# Every symbol the C-ABI header declares (checked by tests/test_abi.py).
+EXPORTED = [
+    "fstg_last_error", "fstg_version", "fstg_device_count", "fstg_even_log2_ceil", "fstg_design_params",
+    "fstg_kerdock_matrix", "fstg_choose_params", "fstg_validate_params", "fstg_candidate_count",
+    "fstg_preprocess", "fstg_preprocess_shard", "fstg_sketch_info_get", "fstg_row_norm_max",
+    "fstg_sketch_column", "fstg_sketch_gather", "fstg_sketch_device_columns", "fstg_sketch_preprocess_ms", "fstg_destroy",
+    "fstg_draw_samples", "fstg_transform_batch", "fstg_transform_with_samples_batch", "fstg_profile_enable",
+    "fstg_profile_reset", "fstg_profile_read", "fstg_launch_count", "fstg_gen_gaussian",
+    "fstg_gen_sparse_targets",
+]
+
+
+def lib():
+    """Loads libfst_b200.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (make -C "
+                              f"paper_2105_05879_b200/csrc)")
+        L = C.CDLL(LIB_PATH)
+        L.fstg_last_error.restype = C.c_char_p
+        L.fstg_version.restype = C.c_char_p
+        L.fstg_candidate_count.restype = C.c_int64
+        L.fstg_candidate_count.argtypes = [C.c_int64, C.c_int64, C.c_int64]
+        L.fstg_destroy.argtypes = [C.c_void_p]
+        L.fstg_destroy.restype = None
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        raise _ERRORS.get(rc, RuntimeError)(lib().fstg_last_error().decode())
+
+
+def device_count() -> int:
+    c = C.c_int()
+    _check(lib().fstg_device_count(C.byref(c)))
+    return c.value
+
+
+# -------------------------------------------------------------- pointers ----
+def _is_torch(t) -> bool:
+    return type(t).__module__.startswith("torch")
+
+
+def _ptr(a) -> C.c_void_p:
+    if a is None:
+        return C.c_void_p(None)
+    if _is_torch(a):
+        if not a.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return C.c_void_p(a.data_ptr())
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("array must be C-contiguous")
+        return C.c_void_p(a.ctypes.data)
+    raise TypeError(f"unsupported buffer type {type(a)}")
+
+
+def _dtype_code(dt) -> int:
+    s = str(dt)
+    if "float64" in s or s == "double":
+        return F64
+    if "float32" in s or s == "float":
+        return F32
+    raise ValueError(f"dtype must be float32 or float64, got {dt}")
+
+
+# ----------------------------------------------------------- host helpers ----
+def even_log2_ceil(n: int) -> int:
+    """sketch.hpp:58-63"""
+    k = C.c_int()
+    _check(lib().fstg_even_log2_ceil(C.c_int64(n), C.byref(k)))
+    return k.value
+
+
+def design_params(k: int):
+    """kerdock.hpp:26-31 -> (d, L)"""
+    d, L = C.c_int64(), C.c_int64()
+    _check(lib().fstg_design_params(C.c_int(k), C.byref(d), C.byref(L)))
+    return d.value, L.value
+
+
+def kerdock_matrix(k: int, s: int) -> np.ndarray:
+    """kerdock.hpp:55-84 (bit j of row i = entry (i, j))"""
+    out = np.zeros(k, dtype=np.uint64)
+    _check(lib().fstg_kerdock_matrix(C.c_int(k), C.c_uint64(s), out.ctypes.data_as(C.c_void_p)))
+    return out
+
+
+def choose_params(row_norm_max: float, gamma: float, eta: float, m: int):
+    """stream.hpp:58-69 -> (J, K)"""
+    J, K = C.c_int64(), C.c_int64()
+    _check(lib().fstg_choose_params(C.c_double(row_norm_max), C.c_double(gamma), C.c_double(eta), C.c_int64(m),
+                                    C.byref(J), C.byref(K)))
+    return J.value, K.value
+
+
+def candidate_count(s: int, widen: int, m: int) -> int:
+    """stream.hpp:245-246 (`want`)"""
+    return int(lib().fstg_candidate_count(s, widen, m))
+
+
+@dataclass
+class StreamParams:
+    """stream.hpp:22-39; ``mode`` selects FAST (fp32 default) or STRICT (fp64 default) arithmetic."""
+    epsilon: float = 0.0
+    delta: float = 0.0
+    s: int = 1
+    J: int = 1
+    K: int = 1
+    widen: int = 10
+    seed: int = 0
+    mode: int = MODE_DEFAULT
+
+    def _c(self) -> _Params:
+        return _Params(self.epsilon, self.delta, self.s, self.J, self.K, self.widen, self.seed & (2**64 - 1),
+                       self.mode, 0)
+
+    def validate(self) -> None:
+        p = self._c()
+        _check(lib().fstg_validate_params(C.byref(p)))
+
+
+@dataclass
+class TransformResult:
+    """stream.hpp:41-54: sorted support with exact values, the candidate set and mu."""
+    support: np.ndarray
+    values: np.ndarray
+    candidate_set: np.ndarray
+    mu: np.ndarray
+    samples_used: int
+
+
+@dataclass
+class BatchResult:
+    """Batched outputs (row v belongs to vector v; first counts[v] support entries valid)."""
+    counts: object
+    support: object
+    values: object
+    candidates: object = None
+    mu: object = None
+
+    def result(self, v: int, samples_used: int = 0) -> TransformResult:
+        c = int(_to_numpy(self.counts)[v])
+        sup = _to_numpy(self.support)[v, :c].astype(np.int64)
+        val = _to_numpy(self.values)[v, :c].copy()
+        cand = _to_numpy(self.candidates)[v].astype(np.int64) if self.candidates is not None else None
+        mu = _to_numpy(self.mu)[v].copy() if self.mu is not None else None
+        return TransformResult(sup, val, cand, mu, samples_used)
+
+
+def _to_numpy(a):
+    if a is None:
+        return None
+    if _is_torch(a):
+        return a.detach().cpu().numpy()
+    return a
+
+
+# ----------------------------------------------------------------- sketch ----
+class Sketch:
+    """sketch.hpp:70-142 — device-resident {A s_l} (column-major m x L) + embedded A."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        info = _Info()
+        _check(lib().fstg_sketch_info_get(self._h, C.byref(info)))
+        self.m, self.n, self.d, self.L, self.k = info.m, info.n, info.d, info.L, info.k
+        self.dtype = np.float64 if info.dtype == F64 else np.float32
+        self.device = info.device
+        self.column_stride = info.column_stride
+        self.device_bytes = info.device_bytes
+        self.preprocess_ms = info.preprocess_ms
+        self._row_norm_max = info.row_norm_max
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib().fstg_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    def row_norm_max(self) -> float:
+        return self._row_norm_max
+
+    def kerdock_bases(self) -> int:
+        return self.d // 2
+
+    def column(self, ell: int) -> np.ndarray:
+        """Sketch::column (sketch.hpp:114-117), copied to host."""
+        out = np.zeros(self.m, dtype=self.dtype)
+        _check(lib().fstg_sketch_column(self._h, C.c_int64(ell), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def gather(self, indices) -> np.ndarray:
+        """draw_and_gather (stream.hpp:184-191): (count, m) host array of columns indices[j]."""
+        idx = np.ascontiguousarray(indices, dtype=np.int64).ravel()
+        out = np.zeros((len(idx), self.m), dtype=self.dtype)
+        _check(lib().fstg_sketch_gather(self._h, _ptr(idx), C.c_int64(len(idx)), _ptr(out), C.c_void_p(None)))
+        return out
+
+    def device_columns_ptr(self) -> int:
+        p = C.c_void_p()
+        _check(lib().fstg_sketch_device_columns(self._h, C.byref(p)))
+        return p.value
+
+
+def preprocess(a, device: int = 0, stream: Optional[int] = None) -> Sketch:
+    """sketch.hpp:149-211. ``a``: m x n float32/float64, numpy (host) or torch (host/cuda)."""
+    if _is_torch(a):
+        a = a.contiguous()
+        dt, shape = a.dtype, tuple(a.shape)
+    else:
+        a = np.ascontiguousarray(a)
+        if a.dtype not in (np.float32, np.float64):
+            a = a.astype(np.float64)
+        dt, shape = a.dtype, a.shape
+    if len(shape) != 2:
+        raise ValueError("preprocess: matrix must be 2-D")
+    m, n = shape
+    if m < 1 or n < 1:
+        raise ValueError("preprocess: matrix must be nonempty")
+    h = C.c_void_p()
+    _check(lib().fstg_preprocess(_ptr(a), C.c_int(_dtype_code(dt)), C.c_int64(m), C.c_int64(n), C.c_int(device),
+                                 C.c_void_p(stream), C.byref(h)))
+    return Sketch(h.value)
+
+
+def preprocess_shard(a, basis_begin: int, basis_end: int, include_identity: bool, device: int = 0,
+                     stream: Optional[int] = None) -> Sketch:
+    """Basis-sharded build of a full-size sketch (only bases [begin, end) computed)."""
+    a = a.contiguous() if _is_torch(a) else np.ascontiguousarray(a)
+    m, n = tuple(a.shape)
+    h = C.c_void_p()
+    _check(lib().fstg_preprocess_shard(_ptr(a), C.c_int(_dtype_code(a.dtype)), C.c_int64(m), C.c_int64(n),
+                                       C.c_int(device), C.c_void_p(stream), C.c_int64(basis_begin),
+                                       C.c_int64(basis_end), C.c_int(1 if include_identity else 0), C.byref(h)))
+    return Sketch(h.value)
+
+
+# ----------------------------------------------------------------- stream ----
+def draw_samples(sk: Sketch, p: StreamParams, seeds=None, B: Optional[int] = None) -> np.ndarray:
+    """stream.hpp:173-182 on the GPU. Returns (J*K,) or, with per-vector seeds, (B, J*K) int64."""
+    p.validate()
+    N = p.J * p.K
+    if seeds is None:
+        out = np.zeros((1 if B is None else B, N), dtype=np.int64)
+        sp = None
+    else:
+        seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+        out = np.zeros((len(seeds), N), dtype=np.int64)
+        sp = seeds
+    pc = p._c()
+    _check(lib().fstg_draw_samples(sk.handle, C.byref(pc), _ptr(sp), C.c_int64(out.shape[0]), _ptr(out),
+                                   C.c_void_p(None)))
+    return out[0] if (seeds is None and B is None) else out
+
+
+def _alloc_outputs(like_torch, B, want, m, dtype, want_cands, want_mu, device):
+    if like_torch:
+        import torch
+        tdt = torch.float64 if dtype == np.float64 else torch.float32
+        dev = f"cuda:{device}"
+        return BatchResult(torch.zeros(B, dtype=torch.int32, device=dev),
+                           torch.zeros((B, want), dtype=torch.int32, device=dev),
+                           torch.zeros((B, want), dtype=tdt, device=dev),
+                           torch.zeros((B, want), dtype=torch.int32, device=dev) if want_cands else None,
+                           torch.zeros((B, m), dtype=tdt, device=dev) if want_mu else None)
+    return BatchResult(np.zeros(B, dtype=np.int32), np.zeros((B, want), dtype=np.int32),
+                       np.zeros((B, want), dtype=dtype),
+                       np.zeros((B, want), dtype=np.int32) if want_cands else None,
+                       np.zeros((B, m), dtype=dtype) if want_mu else None)
+
+
+def _prep_x(sk: Sketch, X):
+    if _is_torch(X):
+        X = X.contiguous()
+    else:
+        X = np.ascontiguousarray(X, dtype=sk.dtype)
+    if str(X.dtype).split(".")[-1] != np.dtype(sk.dtype).name:
+        raise ValueError("transform: vector dtype does not match sketch")
+    if X.ndim == 1:
+        X = X.reshape(1, -1)
+    if X.shape[1] != sk.n:
+        raise ValueError("transform: vector length does not match sketch")
+    return X
+
+
+def transform_batch(sk: Sketch, X, p: StreamParams, seeds=None, *, candidates: bool = False, mu: bool = False,
+                    out: Optional[BatchResult] = None, stream: Optional[int] = None) -> BatchResult:
+    """transform (stream.hpp:272-275) over a batch X (B x n). seeds: per-vector seeds (None -> p.seed)."""
+    X = _prep_x(sk, X)
+    B = X.shape[0]
+    want = candidate_count(p.s, p.widen, sk.m)
+    p.validate()
+    if out is None:
+        out = _alloc_outputs(_is_torch(X) and X.is_cuda, B, want, sk.m, sk.dtype, candidates, mu, sk.device)
+    if seeds is not None and not _is_torch(seeds):
+        seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    pc = p._c()
+    _check(lib().fstg_transform_batch(sk.handle, _ptr(X), C.c_int64(B), C.byref(pc), _ptr(seeds),
+                                      _ptr(out.counts), _ptr(out.support), _ptr(out.values),
+                                      _ptr(out.candidates), _ptr(out.mu), C.c_void_p(stream)))
+    return out
+
+
+def transform_with_samples_batch(sk: Sketch, X, p: StreamParams, indices, *, candidates: bool = False,
+                                 mu: bool = False, out: Optional[BatchResult] = None,
+                                 stream: Optional[int] = None) -> BatchResult:
+    """transform_with_samples (stream.hpp:197-268) with pre-drawn indices (B x J*K int64)."""
+    X = _prep_x(sk, X)
+    B = X.shape[0]
+    p.validate()
+    if not _is_torch(indices):
+        indices = np.ascontiguousarray(indices, dtype=np.int64).reshape(B, -1)
+    if tuple(indices.shape) != (B, p.J * p.K):
+        raise ValueError("transform: drawn sample count does not match J*K")
+    want = candidate_count(p.s, p.widen, sk.m)
+    if out is None:
+        out = _alloc_outputs(_is_torch(X) and X.is_cuda, B, want, sk.m, sk.dtype, candidates, mu, sk.device)
+    pc = p._c()
+    _check(lib().fstg_transform_with_samples_batch(sk.handle, _ptr(X), C.c_int64(B), C.byref(pc), _ptr(indices),
+                                                   _ptr(out.counts), _ptr(out.support), _ptr(out.values),
+                                                   _ptr(out.candidates), _ptr(out.mu), C.c_void_p(stream)))
+    return out
+
+
+def transform(sk: Sketch, x, p: StreamParams) -> TransformResult:
+    """stream.hpp:272-275 for one vector (seed = p.seed)."""
+    x = np.asarray(x)
+    if x.ndim != 1:
+        raise ValueError("transform: x must be a vector")
+    r = transform_batch(sk, x.reshape(1, -1), p, candidates=True, mu=True)
+    return r.result(0, p.J * p.K)
+
+
+def transform_with_samples(sk: Sketch, x, p: StreamParams, indices) -> TransformResult:
+    """stream.hpp:197-268 for one vector with pre-drawn indices."""
+    x = np.asarray(x)
+    r = transform_with_samples_batch(sk, x.reshape(1, -1), p, np.asarray(indices, dtype=np.int64).reshape(1, -1),
+                                     candidates=True, mu=True)
+    return r.result(0, p.J * p.K)
+
+
+# -------------------------------------------------------------- profiling ----
+def profile_enable(on: bool = True) -> None:
+    _check(lib().fstg_profile_enable(C.c_int(1 if on else 0)))
+
+
+def profile_reset() -> None:
+    _check(lib().fstg_profile_reset())
+
+
+def profile_read(name: str):
+    ms, n = C.c_double(), C.c_int64()
+    _check(lib().fstg_profile_read(name.encode(), C.byref(ms), C.byref(n)))
+    return ms.value, n.value
+
+
+def launch_count() -> int:
+    n = C.c_int64()
+    _check(lib().fstg_launch_count(C.byref(n)))
+    return n.value

@@ -1,0 +1,110 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol include/fst_b200.h
+declares, its host-side design logic matches the oracle bit-exactly, and the
+compute entry points fail loudly (no CPU fallback) when no B200 is present."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "fst_b200.h")
+
+
+@pytest.fixture(scope="module")
+def fst():
+    from paper_2105_05879_b200 import fst
+    if not os.path.exists(fst.LIB_PATH):
+        import __graft_entry__
+        __graft_entry__.build()
+    return fst
+
+
+def _declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(fstg_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol(fst):
+    lib = C.CDLL(fst.LIB_PATH)
+    declared = _declared_functions()
+    assert len(declared) >= 20
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert sorted(fst.EXPORTED) == declared
+
+
+def test_sm100a_cubin_only(fst):
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", fst.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out.replace("sm_100a", ""))
+
+
+def test_design_params_and_log2(fst, orc):
+    for n in [1, 3, 4, 5, 16, 17, 64, 65, 256, 1024, 4096, 16384]:
+        assert fst.even_log2_ceil(n) == orc.even_log2_ceil(n)
+    for k in (2, 4, 6, 8, 10, 12, 14, 16):
+        assert fst.design_params(k) == orc.design_params(k)
+    for bad in (0, 3, 18):
+        with pytest.raises(ValueError):
+            fst.design_params(bad)
+    with pytest.raises(ValueError):
+        fst.even_log2_ceil(0)
+
+
+@pytest.mark.parametrize("k", [2, 4, 6, 8, 10, 12])
+def test_kerdock_matrices_match_oracle(fst, orc, k):
+    d, _ = orc.design_params(k)
+    bases = range(d // 2) if k <= 10 else list(range(64)) + list(range(d // 2 - 64, d // 2))
+    for s in bases:
+        assert fst.kerdock_matrix(k, s).tolist() == orc.kerdock_matrix(k, s).tolist(), (k, s)
+
+
+def test_kerdock_k14_sampled(fst, orc):
+    rng = np.random.default_rng(14)
+    for s in rng.integers(0, 8192, size=40):
+        assert fst.kerdock_matrix(14, int(s)).tolist() == orc.kerdock_matrix(14, int(s)).tolist()
+    with pytest.raises(ValueError):
+        fst.kerdock_matrix(4, 8)
+
+
+def test_choose_params_matches_reference(fst, orc):
+    assert fst.choose_params(1.0, 1.0, 1.0, 1) == (30, 1)
+    assert fst.choose_params(1.0, 0.5, 0.01, 4096) == (119, 26)
+    rng = np.random.default_rng(5)
+    for _ in range(200):
+        r, g, eta, m = rng.uniform(0.1, 3), rng.uniform(0.01, 2), rng.uniform(0.01, 1), int(rng.integers(1, 10**5))
+        assert fst.choose_params(r, g, eta, m) == orc.choose_params(r, g, eta, m)
+    for bad in [(1.0, 0.0, 0.5, 16), (1.0, 0.5, 0.0, 16), (1.0, 0.5, 1.5, 16), (1.0, 0.5, 0.5, 0)]:
+        with pytest.raises(ValueError):
+            fst.choose_params(*bad)
+
+
+def test_candidate_count(fst, orc):
+    for s, w, m in [(32, 10, 4096), (8, 10, 256), (2, 8, 16), (4, 10, 32), (10**15, 10, 64), (3, 1, 5)]:
+        assert fst.candidate_count(s, w, m) == orc.candidate_count(s, w, m)
+
+
+def test_param_validation(fst):
+    P = fst.StreamParams
+    P(epsilon=0.1, s=1, J=2, K=2).validate()
+    for kw in [dict(epsilon=0.0), dict(epsilon=0.1, delta=0.2), dict(epsilon=0.1, s=0), dict(epsilon=0.1, J=0),
+               dict(epsilon=0.1, K=0), dict(epsilon=0.1, widen=0), dict(epsilon=0.1, delta=-1.0)]:
+        with pytest.raises(ValueError):
+            P(**{**dict(s=1, J=2, K=2), **kw}).validate()
+    with pytest.raises(OverflowError):
+        P(epsilon=0.1, s=1, J=(2**63 - 1) // 2, K=3).validate()
+
+
+def test_no_cpu_fallback_without_gpu(fst):
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("a GPU is present")
+    except ImportError:
+        pass
+    assert fst.device_count() == 0
+    with pytest.raises(fst.CudaError):
+        fst.preprocess(np.eye(4))

@@ -1,0 +1,324 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): index draws, sketch bits in fp64, candidate
+sets and supports bit-exact; values within 1e-12 (fp64) / 1e-5 relative (fp32).
+fp32 runs are compared with the fp64 oracle on the same (fp32-rounded) inputs;
+a support difference is only accepted where the reference rule allows it
+(|Ax_i| within 1e-6 of eps) or where it is forced by an estimator tie at the
+candidate cut-off (documented in DESIGN.md §Parity).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fst():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2105_05879_b200 import fst
+    return fst
+
+
+def _orth(orc, n, seed):
+    return orc.gen_orthogonal(n, seed)
+
+
+def _rand(m, n, seed, dtype=np.float64):
+    return np.random.default_rng(seed).standard_normal((m, n)).astype(dtype)
+
+
+# ------------------------------------------------------------------ draws ----
+@pytest.mark.parametrize("L", [12, 144, 33024, 525312, 8392704, 134234112])
+def test_draws_bit_exact(fst, orc, L):
+    k = {12: 2, 144: 4, 33024: 8, 525312: 10, 8392704: 12, 134234112: 14}[L]
+    d, LL = orc.design_params(k)
+    assert LL == L
+    # a sketch of the right design is needed by the API: draw against a tiny one
+    sk = fst.preprocess(np.ones((1, d // 2 + 1), dtype=np.float32) if d > 4 else np.ones((1, 3), dtype=np.float32))
+    assert sk.L == L
+    seeds = np.array([0, 1, 42, 9000, 2**63 + 5, orc.stream_seed(7)], dtype=np.uint64)
+    for J, K in [(375, 2), (1, 1), (313, 1), (100, 7)]:
+        p = fst.StreamParams(epsilon=0.1, s=1, J=J, K=K)
+        got = fst.draw_samples(sk, p, seeds=seeds)
+        for v, seed in enumerate(seeds):
+            ref = orc.draw_samples(L, orc.StreamParams(epsilon=0.1, s=1, J=J, K=K, seed=int(seed)))
+            assert got[v].tolist() == ref.tolist()
+
+
+# ------------------------------------------------------------- preprocess ----
+@pytest.mark.parametrize("m,n,seed", [(8, 16, 99), (5, 13, 1), (3, 50, 2), (7, 4, 3), (1, 4, 0), (33, 64, 4),
+                                      (40, 50, 5), (256, 256, 6), (17, 200, 7), (64, 1024, 8)])
+def test_preprocess_fp64_bit_exact(fst, orc, m, n, seed):
+    a = _rand(m, n, seed)
+    sk = fst.preprocess(a)
+    ref = orc.preprocess(a)
+    assert (sk.m, sk.n, sk.k, sk.L) == (ref.m, ref.n, ref.k, ref.L)
+    cols = ref.columns()
+    rng = np.random.default_rng(seed)
+    ells = range(sk.L) if sk.L <= 40000 else rng.integers(0, sk.L, size=3000)
+    for ell in ells:
+        got = sk.column(int(ell))
+        assert got.tobytes() == cols[int(ell)].tobytes(), ell
+    assert sk.row_norm_max() == pytest.approx(ref.row_norm_max, rel=1e-14)
+
+
+def test_preprocess_config1_fp64_bit_exact(fst, orc):
+    a = orc.gen_orthogonal(256, 777)
+    sk = fst.preprocess(a)
+    ref = orc.preprocess(a)
+    cols = ref.columns()
+    got = np.stack([sk.column(ell) for ell in range(sk.L)])
+    assert got.tobytes() == cols.tobytes()
+
+
+@pytest.mark.parametrize("m,n", [(16, 256), (8, 1024), (8, 4096), (5, 4000)])
+def test_preprocess_fp32_bit_exact_vs_float_restatement(fst, orc, m, n):
+    a = _rand(m, n, n, np.float32)
+    sk = fst.preprocess(a)
+    ref = orc.preprocess(a, dtype=np.float32, threads=8)
+    cols = ref.columns()
+    rng = np.random.default_rng(m)
+    for ell in rng.integers(0, sk.L, size=2000):
+        assert sk.column(int(ell)).tobytes() == cols[int(ell)].tobytes(), ell
+    for ell in list(range(sk.L - sk.d, sk.L)):  # identity block
+        assert sk.column(ell).tobytes() == cols[ell].tobytes()
+
+
+def test_preprocess_errors(fst):
+    with pytest.raises(ValueError):
+        fst.preprocess(np.zeros((0, 4)))
+    bad = np.ones((2, 2))
+    bad[0, 1] = np.nan
+    with pytest.raises(ValueError):
+        fst.preprocess(bad)
+    bad[0, 1] = np.inf
+    with pytest.raises(ValueError):
+        fst.preprocess(bad)
+    sk = fst.preprocess(np.ones((2, 5)))
+    with pytest.raises(IndexError):
+        sk.column(sk.L)
+    with pytest.raises(IndexError):
+        sk.column(-1)
+    assert not sk.column(sk.L - 1).any()  # identity column past n
+
+
+# ------------------------------------------------------- transform, fp64 ----
+def _check_exact(g, r, rtol=1e-12):
+    assert np.array_equal(g.mu, r.mu)
+    assert g.candidate_set.tolist() == r.candidate_set.tolist()
+    assert g.support.tolist() == r.support.tolist()
+    np.testing.assert_allclose(g.values, r.values, rtol=rtol, atol=1e-15)
+
+
+@pytest.mark.parametrize("J,K", [(375, 2), (60, 3), (11, 1), (7, 4), (1, 5)])
+def test_transform_fp64_strict_bit_exact(fst, orc, J, K):
+    a = orc.gen_orthogonal(256, 424242)
+    sk, ref = fst.preprocess(a), orc.preprocess(a)
+    B = 16
+    xs, seeds = [], []
+    for v in range(B):
+        x, _ = orc.gen_exact_sparse(a, 8, orc.gen_seed(1000 + v))
+        xs.append(x)
+        seeds.append(orc.stream_seed(1000 + v))
+    X = np.stack(xs)
+    p = fst.StreamParams(epsilon=0.1, s=8, J=J, K=K)
+    out = fst.transform_batch(sk, X, p, seeds=np.array(seeds, dtype=np.uint64), candidates=True, mu=True)
+    for v in range(B):
+        r = orc.transform(ref, X[v], orc.StreamParams(epsilon=0.1, s=8, J=J, K=K, seed=seeds[v]))
+        _check_exact(out.result(v), r)
+
+
+def test_transform_config1_choose_params(fst, orc):
+    """Config 1 with the reference's default parameters (choose_params)."""
+    a = orc.gen_orthogonal(256, 777)
+    sk, ref = fst.preprocess(a), orc.preprocess(a)
+    J, K = fst.choose_params(sk.row_norm_max(), 0.05, 0.1, 256)
+    assert (J, K) == orc.choose_params(ref.row_norm_max, 0.05, 0.1, 256)
+    X, seeds = [], []
+    for v in range(4):
+        x, _ = orc.gen_exact_sparse(a, 8, orc.gen_seed(v))
+        X.append(x)
+        seeds.append(orc.stream_seed(v))
+    X = np.stack(X)
+    out = fst.transform_batch(sk, X, fst.StreamParams(epsilon=0.1, s=8, J=J, K=K),
+                              seeds=np.array(seeds, dtype=np.uint64), candidates=True, mu=True)
+    for v in range(4):
+        r = orc.transform(ref, X[v], orc.StreamParams(epsilon=0.1, s=8, J=J, K=K, seed=seeds[v]))
+        _check_exact(out.result(v), r)
+        assert len(r.support) == 8
+
+
+@pytest.mark.parametrize("m,n", [(16, 16), (5, 13), (40, 50), (300, 64), (64, 200), (1, 4)])
+def test_transform_fp64_shapes(fst, orc, m, n):
+    a = _rand(m, n, m * 1000 + n)
+    sk, ref = fst.preprocess(a), orc.preprocess(a)
+    rng = np.random.default_rng(m + n)
+    for s, widen, J, K in [(2, 10, 30, 3), (1, 1, 5, 2), (3, 100, 4, 1)]:
+        for t in range(3):
+            x = rng.standard_normal(n)
+            x /= np.linalg.norm(x)
+            p = fst.StreamParams(epsilon=0.05, s=s, widen=widen, J=J, K=K, seed=77 + t)
+            g = fst.transform(sk, x, p)
+            r = orc.transform(ref, x, orc.StreamParams(epsilon=0.05, s=s, widen=widen, J=J, K=K, seed=77 + t))
+            _check_exact(g, r)
+
+
+def test_transform_edge_cases(fst, orc):
+    a = orc.gen_orthogonal(16, 3)
+    sk, ref = fst.preprocess(a), orc.preprocess(a)
+    # x = 0: empty support, mu exactly zero (test_stream.cpp:191-202)
+    g = fst.transform(sk, np.zeros(16), fst.StreamParams(epsilon=0.1, s=2, J=5, K=2))
+    assert len(g.support) == 0 and not g.mu.any()
+    # widen*s >= m: exact hard threshold (test_stream.cpp:162-189)
+    x = np.random.default_rng(2).standard_normal(16)
+    x /= np.linalg.norm(x)
+    g = fst.transform(sk, x, fst.StreamParams(epsilon=0.2, s=2, widen=8, J=3, K=2, seed=42))
+    ax = a @ x
+    assert g.support.tolist() == np.nonzero(np.abs(ax) >= 0.2)[0].tolist()
+    np.testing.assert_allclose(g.values, ax[g.support], rtol=1e-12)
+    assert len(g.candidate_set) == 16
+    # one spike, 100 seeds (test_stream.cpp:204-225)
+    a4 = orc.gen_orthogonal(16, 4)
+    sk4 = fst.preprocess(a4)
+    X = np.tile(a4[0], (100, 1))
+    out = fst.transform_batch(sk4, X, fst.StreamParams(epsilon=0.5, s=1, J=500, K=3),
+                              seeds=np.arange(100, dtype=np.uint64))
+    for v in range(100):
+        r = out.result(v)
+        assert r.support.tolist() == [0] and abs(r.values[0] - 1.0) <= 1e-10
+    # B = 0 is a no-op; errors
+    fst.transform_batch(sk, np.zeros((0, 16)), fst.StreamParams(epsilon=0.1, s=1, J=2, K=2))
+    with pytest.raises(ValueError):
+        fst.transform(sk, np.zeros(15), fst.StreamParams(epsilon=0.1, s=1, J=2, K=2))
+    with pytest.raises(ValueError):
+        fst.transform(sk, np.zeros(16), fst.StreamParams(epsilon=0.0, s=1, J=2, K=2))
+    with pytest.raises(OverflowError):
+        fst.transform(sk, np.zeros(16), fst.StreamParams(epsilon=0.1, s=1, J=(2**63 - 1) // 2, K=3))
+    with pytest.raises(IndexError):
+        fst.transform_with_samples(sk, x, fst.StreamParams(epsilon=0.1, s=1, J=2, K=1), [0, sk.L])
+
+
+def test_transform_with_samples_matches_transform(fst, orc):
+    a = orc.gen_orthogonal(32, 10)
+    sk = fst.preprocess(a)
+    x = np.random.default_rng(11).standard_normal(32)
+    x /= np.linalg.norm(x)
+    p = fst.StreamParams(epsilon=0.05, s=3, J=25, K=4, seed=1234)
+    r1, r2 = fst.transform(sk, x, p), fst.transform(sk, x, p)
+    r3 = fst.transform_with_samples(sk, x, p, fst.draw_samples(sk, p))
+    for r in (r2, r3):
+        assert r.support.tolist() == r1.support.tolist()
+        assert r.values.tobytes() == r1.values.tobytes()
+        assert r.mu.tobytes() == r1.mu.tobytes()
+
+
+# ------------------------------------------------------- transform, fp32 ----
+def _support_diff_allowed(g, r, mu_ref, ax, eps, want):
+    """A support difference is allowed only at |Ax_i| within 1e-6 of eps, or when
+    the differing candidate sits at the rank-`want` estimator cut-off (|mu| ties
+    within fp32 rounding of the boundary value)."""
+    diff = set(g.support.tolist()) ^ set(r.support.tolist())
+    if not diff:
+        return True
+    order = np.sort(np.abs(mu_ref))[::-1]
+    cut = order[want - 1] if want <= len(order) else 0.0
+    for i in diff:
+        near_eps = abs(abs(ax[i]) - eps) <= 1e-6
+        near_cut = abs(abs(mu_ref[i]) - cut) <= 1e-5 * max(1.0, cut)
+        if not (near_eps or near_cut):
+            return False
+    return True
+
+
+@pytest.mark.parametrize("n,s,eps", [(256, 8, 0.1), (1024, 16, 0.1), (64, 4, 0.2)])
+def test_transform_fp32_fast_vs_fp64_oracle(fst, orc, n, s, eps):
+    a64 = orc.gen_orthogonal(n, 5150 + n)
+    a32 = a64.astype(np.float32)
+    a = a32.astype(np.float64)  # the oracle sees exactly the GPU's inputs
+    sk, ref = fst.preprocess(a32), orc.preprocess(a)
+    B = 24
+    X32 = np.zeros((B, n), dtype=np.float32)
+    seeds = np.array([orc.stream_seed(v) for v in range(B)], dtype=np.uint64)
+    for v in range(B):
+        x, _ = orc.gen_exact_sparse(a64, s, orc.gen_seed(v))
+        X32[v] = x.astype(np.float32)
+    p = fst.StreamParams(epsilon=eps, s=s, J=375, K=2)
+    out = fst.transform_batch(sk, X32, p, seeds=seeds, candidates=True, mu=True)
+    want = fst.candidate_count(s, 10, n)
+    exact_supports = 0
+    for v in range(B):
+        x = X32[v].astype(np.float64)
+        r = orc.transform(ref, x, orc.StreamParams(epsilon=eps, s=s, J=375, K=2, seed=int(seeds[v])))
+        g = out.result(v)
+        np.testing.assert_allclose(g.mu, r.mu, rtol=1e-4, atol=2e-6)
+        ax = a @ x
+        assert _support_diff_allowed(g, r, r.mu, ax, eps, want), (v, g.support, r.support)
+        exact_supports += int(g.support.tolist() == r.support.tolist())
+        common = np.intersect1d(g.support, r.support)
+        gi = {i: val for i, val in zip(g.support, g.values)}
+        ri = {i: val for i, val in zip(r.support, r.values)}
+        for i in common:
+            assert abs(gi[i] - ri[i]) <= 1e-5 * abs(ri[i])
+        assert np.all(np.abs(g.values) >= eps * (1 - 1e-7))
+    assert exact_supports >= B - 1
+
+
+def test_transform_fp32_strict_bit_exact_vs_float_restatement(fst, orc):
+    """STRICT mode in fp32 reproduces the reference arithmetic run in float."""
+    n = 256
+    a32 = orc.gen_orthogonal(n, 99).astype(np.float32)
+    sk, ref = fst.preprocess(a32), orc.preprocess(a32, dtype=np.float32)
+    rng = np.random.default_rng(3)
+    for t in range(6):
+        x = rng.standard_normal(n).astype(np.float32)
+        p = fst.StreamParams(epsilon=0.05, s=4, J=50, K=3, seed=t, mode=fst.MODE_STRICT)
+        g = fst.transform(sk, x, p)
+        oi = orc.StreamParams(epsilon=0.05, s=4, J=50, K=3, seed=t)
+        r = orc.transform(ref, x, oi)
+        assert g.mu.tobytes() == r.mu.tobytes()
+        assert g.candidate_set.tolist() == r.candidate_set.tolist()
+
+
+# ------------------------------------------------- full size (config 3) ----
+def test_config3_full_size_vs_gathered_oracle(fst, orc):
+    """n = 4096 fp32 through the real 137 GB sketch: columns spot-checked against
+    the fp64 oracle's FWHT, then the estimator/support of 3 vectors checked
+    against the oracle's draw_and_gather path on the GPU's own gathered columns."""
+    import torch
+    from paper_2105_05879_b200 import generators
+    prob = generators.config3_problem(B=3, seed=20251019, device="cuda:0")
+    a32 = prob.A.cpu().numpy()
+    sk = fst.preprocess(prob.A)
+    assert sk.L == 8392704
+    # sketch spot-check: 2 random bases, every row, vs FWHT in fp64 of the fp32 rows
+    rng = np.random.default_rng(0)
+    a64 = a32.astype(np.float64)
+    for s in rng.integers(0, 2048, size=2):
+        mat = orc.kerdock_matrix(12, int(s))
+        signs = np.array([1.0 - 2.0 * orc.quadratic_form(mat, orc.coords_of_position(j, 12)) for j in range(4096)])
+        for w in rng.integers(0, 4096, size=3):
+            ell = int(s) * 4096 + int(w)
+            walsh = np.array([1.0 - 2.0 * (bin(int(w) & j).count("1") & 1) for j in range(4096)])
+            expect = a64 @ (signs * walsh)
+            got = sk.column(ell).astype(np.float64)
+            assert np.max(np.abs(got - expect)) <= 1e-4 * np.max(np.abs(expect))
+    X = prob.X.cpu().numpy()
+    p = fst.StreamParams(epsilon=0.1, s=32, J=375, K=2)
+    out = fst.transform_batch(sk, prob.X, p, seeds=torch.as_tensor(prob.seeds.astype(np.int64)).cuda(),
+                              candidates=True, mu=True)
+    idx = fst.draw_samples(sk, p, seeds=prob.seeds)
+    for v in range(3):
+        ref_idx = orc.draw_samples(sk.L, orc.StreamParams(epsilon=0.1, s=32, J=375, K=2, seed=int(prob.seeds[v])))
+        assert idx[v].tolist() == ref_idx.tolist()
+        gathered = np.stack([sk.column(int(ell)) for ell in idx[v]]).astype(np.float64)
+        x = X[v].astype(np.float64)
+        r = orc.transform_gathered(a64, x, orc.StreamParams(epsilon=0.1, s=32, J=375, K=2), idx[v], gathered)
+        g = out.result(v)
+        np.testing.assert_allclose(g.mu, r.mu, rtol=1e-4, atol=5e-6)
+        assert _support_diff_allowed(g, r, r.mu, a64 @ x, 0.1, 320)
+        assert g.support.tolist() == r.support.tolist()
+        np.testing.assert_allclose(g.values, r.values, rtol=1e-5)
+    sk.close()
