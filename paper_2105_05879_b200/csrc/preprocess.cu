@@ -136,7 +136,7 @@ __device__ __forceinline__ void reg_fwht<float, 6>(float (&v)[64]) {
         const float2 x = make_float2(v[i], v[i + 1]);
         const float2 y = make_float2(v[i + h], v[i + h + 1]);
         const float2 s = __fadd2_rn(x, y);
-        const float2 d = __fadd2_rn(x, make_float2(-y.x, -y.y));
+        const float2 d = __ffma2_rn(y, make_float2(-1.f, -1.f), x);
         v[i] = s.x;
         v[i + 1] = s.y;
         v[i + h] = d.x;
@@ -235,17 +235,189 @@ __global__ void __launch_bounds__(NT) fwht_sketch_kernel(const T* __restrict__ a
     reg_fwht<T, C::HALF>(v);
     // ---- transposed write-back: column s*d + w, row i0 + r2 (sketch.hpp:191-196) ----
     if (row2 < m) {
-      T* base = cols + (s * D) * ldc + row2;
+      T* ptr = cols + (s * D + q2) * ldc + row2;
+      const int64_t step = int64_t(E) * ldc;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const int64_t w = int64_t(e) * E + q2;
         if constexpr (sizeof(T) == 4)
-          stg_f32_policy(reinterpret_cast<float*>(base + w * ldc), static_cast<float>(v[e]), pol_stream);
+          stg_f32_policy(reinterpret_cast<float*>(ptr), static_cast<float>(v[e]), pol_stream);
         else
-          stg_f64_policy(reinterpret_cast<double*>(base + w * ldc), static_cast<double>(v[e]), pol_stream);
+          stg_f64_policy(reinterpret_cast<double*>(ptr), static_cast<double>(v[e]), pol_stream);
+        ptr += step;
+        asm volatile("" : "+l"(ptr));
       }
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// k = 12 fp32 specialisation (the n = 4096 headline): the CTA's 8 rows of A
+// are parked in tensor memory (TMEM, 128 KiB of the SM's 256 KiB) once and
+// re-read with tcgen05.ld for every basis, so the per-basis loop has no
+// global loads; butterflies on register bits >= 1 use packed FADD2 / FFMA2
+// (x - y as fma(y, -1, x), exactly rounded like the reference's x - y); the
+// smem transpose uses 16-byte chunk-swizzled stores.
+// Thread layout as in the generic kernel: E = 64, R = 8 rows, 512 threads.
+// TMEM: warp w owns lanes 32*(w%4) .. +31 and columns 64*(w/4) .. +63.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+      "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+      "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+      "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, float* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]), "=f"(v[8]),
+        "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15]), "=f"(v[16]),
+        "=f"(v[17]), "=f"(v[18]), "=f"(v[19]), "=f"(v[20]), "=f"(v[21]), "=f"(v[22]), "=f"(v[23]), "=f"(v[24]),
+        "=f"(v[25]), "=f"(v[26]), "=f"(v[27]), "=f"(v[28]), "=f"(v[29]), "=f"(v[30]), "=f"(v[31])
+      : "r"(taddr)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Butterflies over register-index bits [0, 6) of v[64], ascending; bit 0
+// scalar, bits >= 1 as packed pairs (i, i+1) with FADD2 / FFMA2(-1).
+__device__ __forceinline__ void reg_fwht64_packed(float (&v)[64]) {
+#pragma unroll
+  for (int i = 0; i < 64; i += 2) {
+    const float a = v[i], b = v[i + 1];
+    v[i] = a + b;
+    v[i + 1] = a - b;
+  }
+#pragma unroll
+  for (int hb = 1; hb < 6; ++hb) {
+    const int h = 1 << hb;
+#pragma unroll
+    for (int i = 0; i < 64; i += 2) {
+      if ((i & h) == 0) {
+        const float2 x = make_float2(v[i], v[i + 1]);
+        const float2 y = make_float2(v[i + h], v[i + h + 1]);
+        const float2 s = __fadd2_rn(x, y);
+        const float2 d = __ffma2_rn(y, make_float2(-1.f, -1.f), x);
+        v[i] = s.x;
+        v[i + 1] = s.y;
+        v[i + h] = d.x;
+        v[i + h + 1] = d.y;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512, 1) fwht12_tmem_kernel(const float* __restrict__ a, int64_t lda, int64_t m,
+                                                             int64_t n, const uint32_t* __restrict__ qplain,
+                                                             int64_t basis_begin, int64_t basis_end,
+                                                             int bases_per_cta, float* __restrict__ cols,
+                                                             int64_t ldc) {
+  constexpr int E = 64, R = 8, RS = 4096 + 4, D = 4096, WPB = 128;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* tile = reinterpret_cast<float*>(smem_raw);
+  __shared__ uint32_t tmem_base_slot;
+
+  const int tid = threadIdx.x, warp = tid / 32;
+  const int64_t i0 = int64_t(blockIdx.x) * R;
+  const int64_t s_first = basis_begin + int64_t(blockIdx.y) * bases_per_cta;
+  const int64_t s_last = min(basis_end, s_first + bases_per_cta);
+  const uint64_t pol_stream = policy_evict_first();
+
+  const int r1 = tid / E, p1 = tid % E;
+  const int64_t row1 = i0 + r1;
+  const int r2 = tid % R, q2 = tid / R;
+  const int64_t row2 = i0 + r2;
+
+  // ---- TMEM: allocate 256 columns, park the A tile ----
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t taddr = tmem_base_slot + (static_cast<uint32_t>(32 * (warp % 4)) << 16) +
+                         static_cast<uint32_t>(64 * (warp / 4));
+  {
+    float v[E];
+    const int64_t pos0 = int64_t(p1) * E;
+    if (row1 < m) {
+      const float* arow = a + row1 * lda;
+      if (pos0 + E <= n) {
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(arow + pos0 + e));
+          v[e] = f.x;
+          v[e + 1] = f.y;
+          v[e + 2] = f.z;
+          v[e + 3] = f.w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = (pos0 + e < n) ? arow[pos0 + e] : 0.f;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = 0.f;
+    }
+    tmem_st_x32(taddr, v);
+    tmem_st_x32(taddr + 32, v + 32);
+    tmem_wait_st();
+  }
+
+  for (int64_t s = s_first; s < s_last; ++s) {
+    float v[E];
+    tmem_ld_x32(taddr, v);
+    tmem_ld_x32(taddr + 32, v + 32);
+    const uint32_t q0 = __ldg(qplain + s * WPB + 2 * p1), q1 = __ldg(qplain + s * WPB + 2 * p1 + 1);
+    tmem_wait_ld();
+    // sign mask (sketch.hpp:185): flip the sign bit where Q_s(pos) = 1 (exact)
+#pragma unroll
+    for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(__float_as_uint(v[e]) ^ ((q0 << (31 - e)) & 0x80000000u));
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      v[32 + e] = __uint_as_float(__float_as_uint(v[32 + e]) ^ ((q1 << (31 - e)) & 0x80000000u));
+    reg_fwht64_packed(v);  // position bits 0..5
+    __syncthreads();       // previous basis' phase-2 reads done
+    {
+      float* dst = tile + r1 * RS + p1 * E;
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        *reinterpret_cast<float4*>(dst + 4 * (c ^ (p1 & 15))) =
+            make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+    }
+    __syncthreads();
+    {
+      const float* src = tile + r2 * RS + (q2 & 3);
+      const int cq = q2 >> 2;
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = src[e * E + 4 * (cq ^ (e & 15))];
+    }
+    reg_fwht64_packed(v);  // position bits 6..11
+    if (row2 < m) {
+      // incremental addressing keeps 64 hoisted 64-bit offsets out of registers
+      float* ptr = cols + (s * D + q2) * ldc + row2;
+      const int64_t step = int64_t(E) * ldc;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        stg_f32_policy(ptr, v[e], pol_stream);
+        ptr += step;
+        asm volatile("" : "+l"(ptr));
+      }
+    }
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_base_slot) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -326,9 +498,29 @@ static cudaError_t launch_fwht_k(const T* a, int64_t lda, int64_t m, int64_t n, 
   return cudaGetLastError();
 }
 
+static cudaError_t launch_fwht12_tmem(const float* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
+                                      int64_t b0, int64_t b1, float* cols, int64_t ldc, cudaStream_t st) {
+  constexpr size_t smem = size_t(8) * (4096 + 4) * sizeof(float);
+  cudaError_t e = cudaFuncSetAttribute(fwht12_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  const int64_t nb = b1 - b0;
+  if (nb <= 0) return cudaSuccess;
+  const int64_t row_tiles = (m + 7) / 8;
+  int bpc = 32;
+  while (bpc > 1 && row_tiles * ((nb + bpc - 1) / bpc) < 148 * 8) bpc /= 2;
+  const int64_t gy = (nb + bpc - 1) / bpc;
+  if (row_tiles > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
+  fwht12_tmem_kernel<<<dim3(static_cast<unsigned>(row_tiles), static_cast<unsigned>(gy)), 512, smem, st>>>(
+      a, lda, m, n, qplain, b0, b1, bpc, cols, ldc);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_fwht_sketch(int k, const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
                                int64_t b0, int64_t b1, T* cols, int64_t ldc, cudaStream_t st) {
+  if constexpr (sizeof(T) == 4) {
+    if (k == 12 && (lda % 4) == 0) return launch_fwht12_tmem(a, lda, m, n, qplain, b0, b1, cols, ldc, st);
+  }
   switch (k) {
     case 2: return launch_fwht_k<T, 2>(a, lda, m, n, qplain, b0, b1, cols, ldc, st);
     case 4: return launch_fwht_k<T, 4>(a, lda, m, n, qplain, b0, b1, cols, ldc, st);

@@ -31,11 +31,13 @@ namespace fstg {
 
 constexpr int kNC = 256;                    // consumer threads
 constexpr int kNCW = kNC / 32;              // consumer warps
-constexpr int kThreads = kNC + 32;          // + producer warp
+constexpr int kCW = 4;                      // coefficient warps
+constexpr int kThreads = kNC + kCW * 32 + 32;  // + coefficient warps + producer warp
+constexpr int kTRing = 64;                  // slots of the coefficient ring
+constexpr int kNS = 4;                      // samples per coefficient-warp group
 constexpr int kSegBytes = 16384;            // one ring stage at most
 constexpr int kRingBytes = 65536;           // ring budget
 constexpr int kMaxStages = 64;
-constexpr int kChunk = 256;                 // samples per coefficient chunk
 
 template <typename T>
 struct KeyOf;
@@ -90,10 +92,10 @@ __host__ __device__ inline SmemLayout smem_layout(int64_t d, int stages, int sta
     return at;
   };
   L.ring = take(size_t(stages) * stage_stride, 1024);
-  L.x = take(size_t(d < 4 ? 4 : d) * sizeof(T), 16);
-  L.tbuf = take(kChunk * sizeof(T), 16);
-  L.ibuf = take(kChunk * sizeof(uint32_t), 16);
-  L.bars = take(2 * kMaxStages * sizeof(uint64_t), 8);
+  L.x = take(2 * size_t(d < 4 ? 4 : d) * sizeof(T), 16);
+  L.tbuf = take(kTRing * sizeof(T), 16);
+  L.ibuf = take(16, 16);
+  L.bars = take((2 * kMaxStages + 2 * kTRing + 4) * sizeof(uint64_t), 8);
   L.hist = take(256 * sizeof(uint32_t), 16);
   L.scan = take(2 * 32 * sizeof(uint32_t), 16);
   L.misc = take(16 * sizeof(unsigned long long), 16);
@@ -175,6 +177,85 @@ __device__ __forceinline__ T coeff_fast(const StreamArgs<T>& A, const T* xs, con
   return acc;
 }
 
+// Fast path for NS samples at once (d >= 128): the x loads are shared by the
+// NS samples and the NS accumulation chains are independent, so one warp keeps
+// NS sign-table loads and NS FADD chains in flight. ells[k] >= kb (identity
+// block) are handled by the caller.
+template <typename T, int NS>
+__device__ __forceinline__ void coeff_fast_multi(const StreamArgs<T>& A, const T* xs, const uint32_t* wbase,
+                                                 const uint32_t (&ells)[NS], int lane, T (&out)[NS]) {
+  constexpr int TWC = 4;  // sign-table words per sample loaded up front (d = 4096 -> all of them)
+  const int64_t rows128 = A.d / 128;
+  const int tw = static_cast<int>(A.d >= 1024 ? A.d / 1024 : 1);
+  uint32_t whi[NS], fix[NS], base[NS];
+  const uint32_t* q[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    const uint32_t ell = static_cast<int64_t>(ells[k]) >= A.kb ? 0u : ells[k];
+    const uint32_t s = ell >> A.k, w = ell & static_cast<uint32_t>(A.d - 1);
+    whi[k] = w >> 7;
+    fix[k] = __popc(((w >> 2) & 31u) & static_cast<uint32_t>(lane)) & 1u;
+    base[k] = wbase[((whi[k] & 7u) << 2) | (w & 3u)];
+    q[k] = A.qtrans + (static_cast<int64_t>(s) * tw) * 32 + lane;
+  }
+  T acc[NS];
+#pragma unroll
+  for (int k = 0; k < NS; ++k) acc[k] = T(0);
+  for (int t0 = 0; t0 < tw; t0 += TWC) {
+    uint32_t raw[TWC][NS];
+#pragma unroll
+    for (int tt = 0; tt < TWC; ++tt)
+#pragma unroll
+      for (int k = 0; k < NS; ++k) raw[tt][k] = (t0 + tt < tw) ? __ldg(q[k] + (t0 + tt) * 32) : 0u;
+#pragma unroll
+    for (int tt = 0; tt < TWC; ++tt) {
+      const int t = t0 + tt;
+      if (t < tw) {
+        uint32_t M[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+          const uint32_t hiflip = __popc(whi[k] & (8u * t)) & 1u;
+          M[k] = raw[tt][k] ^ base[k] ^ ((hiflip ^ fix[k]) ? 0xffffffffu : 0u);
+        }
+#pragma unroll
+        for (int ip = 0; ip < 8; ++ip) {
+          const int64_t i = 8 * t + ip;
+          if (i < rows128) {
+            const T* xp = xs + 128 * i + 4 * lane;
+            if constexpr (sizeof(T) == 4) {
+              const float4 xv = *reinterpret_cast<const float4*>(xp);
+              const uint32_t xb[4] = {__float_as_uint(xv.x), __float_as_uint(xv.y), __float_as_uint(xv.z),
+                                      __float_as_uint(xv.w)};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+#pragma unroll
+                for (int k = 0; k < NS; ++k)
+                  acc[k] += __uint_as_float(xb[e] ^ ((M[k] << (31 - (4 * ip + e))) & 0x80000000u));
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const T xvv = xp[e];
+#pragma unroll
+                for (int k = 0; k < NS; ++k) acc[k] += ((M[k] >> (4 * ip + e)) & 1u) ? -xvv : xvv;
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+    if (static_cast<int64_t>(ells[k]) >= A.kb) {
+      const int64_t pos = static_cast<int64_t>(ells[k]) - A.kb;
+      acc[k] = pos < A.n ? static_cast<T>(sqrt(static_cast<double>(A.d))) * xs[pos] : T(0);
+    }
+    out[k] = acc[k];
+  }
+}
+
 // Generic warp path (any d): lane owns positions lane + 32 r.
 template <typename T>
 __device__ __forceinline__ T coeff_generic(const StreamArgs<T>& A, const T* xs, uint32_t ell, int lane) {
@@ -233,6 +314,7 @@ __device__ __forceinline__ T coeff_strict(const StreamArgs<T>& A, const T* xs, u
 }
 
 // --------------------------------------------------------------- kernel ----
+// Warp roles: [0, kNCW) consumers, [kNCW, kNCW + kCW) coefficient warps, last = producer.
 template <typename T, bool STRICT, int NSEG>
 __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T> A) {
   using KT = typename KeyOf<T>::K;
@@ -244,11 +326,14 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
   extern __shared__ __align__(1024) unsigned char smem[];
   const SmemLayout Ls = smem_layout<T>(A.d, A.stages, A.stage_stride, A.want);
   unsigned char* ring = smem + Ls.ring;
-  T* xs = reinterpret_cast<T*>(smem + Ls.x);
-  T* tbuf = reinterpret_cast<T*>(smem + Ls.tbuf);
-  uint32_t* ibuf = reinterpret_cast<uint32_t*>(smem + Ls.ibuf);
+  T* xbuf = reinterpret_cast<T*>(smem + Ls.x);  // two x buffers of d values (double-buffered over vectors)
+  T* tring = reinterpret_cast<T*>(smem + Ls.tbuf);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Ls.bars);
   uint64_t* empty = full + kMaxStages;
+  uint64_t* t_full = empty + kMaxStages;
+  uint64_t* t_empty = t_full + kTRing;
+  uint64_t* x_full = t_empty + kTRing;
+  uint64_t* x_empty = x_full + 2;
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + Ls.hist);
   uint32_t* scan = reinterpret_cast<uint32_t*>(smem + Ls.scan);
   unsigned long long* misc = reinterpret_cast<unsigned long long*>(smem + Ls.misc);
@@ -259,6 +344,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
 
   const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
   const int S = A.stages;
+  const int64_t dx = A.d < 4 ? 4 : A.d;
   const int64_t seg_last_rows = A.m_pad - int64_t(A.nseg - 1) * SEG;
   const uint32_t stage_bytes_full = static_cast<uint32_t>((A.nseg > 1 ? SEG : A.m_pad) * sizeof(T));
   const uint32_t stage_bytes_last = static_cast<uint32_t>(seg_last_rows * sizeof(T));
@@ -266,6 +352,14 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
   if (tid < S) {
     mbar_init(&full[tid], 1);
     mbar_init(&empty[tid], kNCW);
+  }
+  if (tid < kTRing) {
+    mbar_init(&t_full[tid], 1);
+    mbar_init(&t_empty[tid], kNCW);
+  }
+  if (tid < 2) {
+    mbar_init(&x_full[tid], 1);
+    mbar_init(&x_empty[tid], kNCW);
   }
   if (tid < 32) {
     // Walsh base masks: bit f (i' = f/4, e = f%4) = parity(hi3 & i') ^ parity(lo2 & e).
@@ -278,22 +372,26 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
   fence_mbar_init();
   __syncthreads();
 
-  if (warp == kNCW) {
+  if (warp == kNCW + kCW) {
     // ======================= producer warp =======================
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      uint64_t g = 0;
+      int stage = 0;
+      uint32_t phase = 0, used = 0;
       for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x) {
         const uint32_t* vidx = A.idx + v * A.N;
         for (int64_t j = 0; j < A.N; ++j) {
           const T* col = A.cols + static_cast<int64_t>(__ldg(vidx + j)) * A.ldc;
-          for (int sg = 0; sg < A.nseg; ++sg, ++g) {
-            const int stage = static_cast<int>(g % S);
-            const uint64_t u = g / S;
-            if (u > 0) mbar_wait(&empty[stage], static_cast<uint32_t>((u - 1) & 1));
+          for (int sg = 0; sg < A.nseg; ++sg) {
+            if (used) mbar_wait(&empty[stage], phase ^ 1u);
             const uint32_t bytes = (sg == A.nseg - 1) ? stage_bytes_last : stage_bytes_full;
             mbar_arrive_expect_tx(&full[stage], bytes);
             bulk_g2s(ring + size_t(stage) * A.stage_stride, col + int64_t(sg) * SEG, bytes, &full[stage], pol);
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1u;
+              used = 1;
+            }
           }
         }
       }
@@ -301,17 +399,99 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
     return;
   }
 
+  if (warp >= kNCW) {
+    // ======================= coefficient warps =======================
+    // Load x of each vector into its x buffer, then produce t_j for samples
+    // j = cw, cw + kCW, ... into the t ring (one writer per slot).
+    const int cw = warp - kNCW;
+    const int ctid = tid - kNC;  // 0 .. kCW*32-1
+    uint32_t lv = 0;
+    for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
+      const uint32_t xb = lv & 1u, xu = lv >> 1;
+      if (xu > 0) mbar_wait(&x_empty[xb], (xu - 1) & 1u);
+      T* xs = xbuf + xb * dx;
+      const T* xv = A.X + v * A.ldx;
+      for (int64_t p = ctid; p < A.d; p += kCW * 32) xs[p] = (p < A.n) ? xv[p] : T(0);
+      named_bar_sync(2, kCW * 32);
+      if (ctid == 0) mbar_arrive(&x_full[xb]);
+      const uint32_t* vidx = A.idx + v * A.N;
+      const uint64_t g0 = uint64_t(lv) * uint64_t(A.N);
+      if constexpr (STRICT) {
+        // One producing thread per ring slot (stride = kTRing): a slot's uses are
+        // then produced in order by the same thread, so a parity wait can never
+        // be two phases ahead.
+        static_assert(kCW * 32 >= kTRing, "strict producers need kTRing threads");
+        for (int64_t j = ctid; ctid < kTRing && j < A.N; j += kTRing) {
+          const uint64_t g = g0 + uint64_t(j);
+          const uint32_t slot = static_cast<uint32_t>(g % kTRing), u = static_cast<uint32_t>(g / kTRing);
+          const T t = coeff_strict<T>(A, xs, __ldg(vidx + j));
+          if (u > 0) mbar_wait(&t_empty[slot], (u - 1) & 1u);
+          tring[slot] = t;
+          mbar_arrive(&t_full[slot]);
+        }
+      } else if (A.d >= 128) {
+        // groups of kNS samples j = cw + kCW * (kNS * grp + k)
+        uint32_t nxt[kNS];
+#pragma unroll
+        for (int k = 0; k < kNS; ++k) {
+          const int64_t j = cw + int64_t(kCW) * k;
+          nxt[k] = j < A.N ? __ldg(vidx + j) : 0u;
+        }
+        for (int64_t j0 = cw; j0 < A.N; j0 += int64_t(kCW) * kNS) {
+          uint32_t ells[kNS];
+          T t[kNS];
+#pragma unroll
+          for (int k = 0; k < kNS; ++k) {
+            ells[k] = nxt[k];
+            const int64_t jn = j0 + int64_t(kCW) * (kNS + k);  // prefetch the next group's indices
+            nxt[k] = jn < A.N ? __ldg(vidx + jn) : 0u;
+          }
+          coeff_fast_multi<T, kNS>(A, xs, wbase, ells, lane, t);
+#pragma unroll
+          for (int k = 0; k < kNS; ++k) {
+            const int64_t j = j0 + int64_t(kCW) * k;
+            if (j < A.N) {
+              const uint64_t g = g0 + uint64_t(j);
+              const uint32_t slot = static_cast<uint32_t>(g % kTRing), u = static_cast<uint32_t>(g / kTRing);
+              if (u > 0) mbar_wait(&t_empty[slot], (u - 1) & 1u);
+              if (lane == 0) {
+                tring[slot] = t[k];
+                mbar_arrive(&t_full[slot]);
+              }
+            }
+          }
+          __syncwarp();
+        }
+      } else {
+        for (int64_t j = cw; j < A.N; j += kCW) {
+          const uint64_t g = g0 + uint64_t(j);
+          const uint32_t slot = static_cast<uint32_t>(g % kTRing), u = static_cast<uint32_t>(g / kTRing);
+          const T t = coeff_generic<T>(A, xs, __ldg(vidx + j), lane);
+          if (u > 0) mbar_wait(&t_empty[slot], (u - 1) & 1u);
+          if (lane == 0) {
+            tring[slot] = t;
+            mbar_arrive(&t_full[slot]);
+          }
+          __syncwarp();
+        }
+      }
+      // keep the coefficient warps' x reads ordered before the buffer is reloaded
+      named_bar_sync(2, kCW * 32);
+    }
+    return;
+  }
+
   // ======================= consumer warps =======================
   const uint64_t pol_keep = policy_evict_last();
-  const T sqrt_dummy = T(0);
-  (void)sqrt_dummy;
-  uint64_t g = 0;
   T* means = A.means + int64_t(blockIdx.x) * A.K * A.m_pad;
+  int stage = 0;
+  uint32_t phase = 0;
+  uint32_t lv = 0;
 
-  for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x) {
-    // ---- x into shared memory, zero padded to d ----
-    const T* xv = A.X + v * A.ldx;
-    for (int64_t p = tid; p < A.d; p += kNC) xs[p] = (p < A.n) ? xv[p] : T(0);
+  for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
+    const uint32_t xb = lv & 1u, xu = lv >> 1;
+    const T* xs = xbuf + xb * dx;
+    const uint64_t g0 = uint64_t(lv) * uint64_t(A.N);
 
     T acc[NSEG][CPT][VEC];
 #pragma unroll
@@ -321,84 +501,71 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
 #pragma unroll
         for (int e = 0; e < VEC; ++e) acc[sg][c][e] = T(0);
 
-    const uint32_t* vidx = A.idx + v * A.N;
-    for (int64_t c0 = 0; c0 < A.N; c0 += kChunk) {
-      const int cn = static_cast<int>((A.N - c0) < kChunk ? (A.N - c0) : kChunk);
-      for (int i = tid; i < cn; i += kNC) ibuf[i] = __ldg(vidx + c0 + i);
-      named_bar_sync(1, kNC);  // ibuf + xs ready; previous chunk fully consumed
-      // ---- sample coefficients t_j ----
-      if constexpr (STRICT) {
-        for (int i = tid; i < cn; i += kNC) tbuf[i] = coeff_strict<T>(A, xs, ibuf[i]);
-      } else {
-        if (A.d >= 128) {
-          for (int i = warp; i < cn; i += kNCW) {
-            const T t = coeff_fast<T>(A, xs, wbase, ibuf[i], lane);
-            if (lane == 0) tbuf[i] = t;
+    int64_t jb = 0, b = 0;  // position inside the batch, batch index
+    uint32_t tslot = static_cast<uint32_t>(g0 % kTRing), tphase = static_cast<uint32_t>((g0 / kTRing) & 1);
+    for (int64_t j = 0; j < A.N; ++j) {
+      mbar_wait(&t_full[tslot], tphase);
+      const T t = tring[tslot];
+#pragma unroll
+      for (int sg = 0; sg < NSEG; ++sg) {
+        if (sg < A.nseg) {
+          mbar_wait(&full[stage], phase);
+          const typename Vec<T>::V* src = reinterpret_cast<const typename Vec<T>::V*>(ring + size_t(stage) * A.stage_stride);
+          const int64_t rows_here = (sg == A.nseg - 1) ? seg_last_rows : SEG;
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) {
+            const int chunk = tid + c * kNC;
+            if (int64_t(chunk) * VEC < rows_here) {
+              T vv[VEC];
+              Vec<T>::get(src[chunk], vv);
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) {
+                if constexpr (STRICT) {
+                  if constexpr (sizeof(T) == 8)
+                    acc[sg][c][e] = __dadd_rn(acc[sg][c][e], __dmul_rn(t, vv[e]));
+                  else
+                    acc[sg][c][e] = __fadd_rn(acc[sg][c][e], __fmul_rn(t, vv[e]));
+                } else {
+                  acc[sg][c][e] = fma(t, vv[e], acc[sg][c][e]);
+                }
+              }
+            }
           }
-        } else {
-          for (int i = warp; i < cn; i += kNCW) {
-            const T t = coeff_generic<T>(A, xs, ibuf[i], lane);
-            if (lane == 0) tbuf[i] = t;
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
           }
         }
       }
-      named_bar_sync(1, kNC);
-      // ---- accumulate t_j * C[:, ell_j] over the ring ----
-      for (int i = 0; i < cn; ++i) {
-        const T t = tbuf[i];
-        const int64_t j = c0 + i;
+      if (lane == 0) mbar_arrive(&t_empty[tslot]);
+      if (++tslot == kTRing) {
+        tslot = 0;
+        tphase ^= 1u;
+      }
+      if (++jb == A.J) {
+        // batch b complete: mean = sum / J (IEEE division, stream.hpp:237)
+        T* mb = means + b * A.m_pad;
+        const T Jt = static_cast<T>(A.J);
 #pragma unroll
-        for (int sg = 0; sg < NSEG; ++sg) {
-          if (sg < A.nseg) {
-            const int stage = static_cast<int>(g % S);
-            mbar_wait(&full[stage], static_cast<uint32_t>((g / S) & 1));
-            const typename Vec<T>::V* src = reinterpret_cast<const typename Vec<T>::V*>(ring + size_t(stage) * A.stage_stride);
-            const int64_t rows_here = (sg == A.nseg - 1) ? seg_last_rows : SEG;
+        for (int sg = 0; sg < NSEG; ++sg)
 #pragma unroll
-            for (int c = 0; c < CPT; ++c) {
-              const int chunk = tid + c * kNC;
-              if (int64_t(chunk) * VEC < rows_here) {
-                T vv[VEC];
-                Vec<T>::get(src[chunk], vv);
+          for (int c = 0; c < CPT; ++c) {
+            const int64_t row0 = int64_t(sg) * SEG + int64_t(tid + c * kNC) * VEC;
+            if (sg < A.nseg && row0 < A.m_pad) {
 #pragma unroll
-                for (int e = 0; e < VEC; ++e) {
-                  if constexpr (STRICT) {
-                    if constexpr (sizeof(T) == 8)
-                      acc[sg][c][e] = __dadd_rn(acc[sg][c][e], __dmul_rn(t, vv[e]));
-                    else
-                      acc[sg][c][e] = __fadd_rn(acc[sg][c][e], __fmul_rn(t, vv[e]));
-                  } else {
-                    acc[sg][c][e] = fma(t, vv[e], acc[sg][c][e]);
-                  }
-                }
+              for (int e = 0; e < VEC; ++e) {
+                mb[row0 + e] = acc[sg][c][e] / Jt;
+                acc[sg][c][e] = T(0);
               }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
-            ++g;
           }
-        }
-        if ((j + 1) % A.J == 0) {
-          // batch b complete: mean = sum / J (IEEE division, stream.hpp:237)
-          const int64_t b = j / A.J;
-          T* mb = means + b * A.m_pad;
-          const T Jt = static_cast<T>(A.J);
-#pragma unroll
-          for (int sg = 0; sg < NSEG; ++sg)
-#pragma unroll
-            for (int c = 0; c < CPT; ++c) {
-              const int64_t row0 = int64_t(sg) * SEG + int64_t(tid + c * kNC) * VEC;
-              if (sg < A.nseg && row0 < A.m_pad) {
-#pragma unroll
-                for (int e = 0; e < VEC; ++e) {
-                  mb[row0 + e] = acc[sg][c][e] / Jt;
-                  acc[sg][c][e] = T(0);
-                }
-              }
-            }
-        }
+        jb = 0;
+        ++b;
       }
     }
+
 
     // ---- median of the K batch means (stream.hpp:126-143), keys |mu| ----
     KT keys[NSEG][CPT][VEC];
@@ -543,6 +710,7 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
     named_bar_sync(1, kNC);
 
     // ---- refinement: v_i = a_i . x, fp64 accumulation (stream.hpp:259-266) ----
+    mbar_wait(&x_full[xb], xu & 1u);
     for (int64_t ci = warp; ci < A.want; ci += kNCW) {
       const int64_t row = cand[ci];
       const T* arow = A.a + row * A.lda;
@@ -596,7 +764,8 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
       out_base += total;
     }
     if (tid == 0) A.counts[v] = static_cast<int32_t>(out_base);
-    named_bar_sync(1, kNC);  // cand/cval/xs reuse by the next vector
+    named_bar_sync(1, kNC);  // cand/cval reuse by the next vector; xs reads done
+    if (lane == 0) mbar_arrive(&x_empty[xb]);
   }
 }
 

@@ -1,7 +1,7 @@
 set -x
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
 nvidia-smi -L
-timeout 900 python -m pytest tests -m gpu -x -q --durations=15 > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc=$?"
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 300 --durations=15 > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc=$?"
 tail -30 gpurun_out/gpu_tests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 tail -5 gpurun_out/smoke.log
