@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -447,6 +448,10 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   if (smem > 227 * 1024) throw NotSupported("transform: shared-memory plan exceeds 227 KiB (d or want too large)");
   args.stages = stages;
   args.stage_stride = stage_stride;
+  {
+    const char* dbg = std::getenv("FSTG_STREAM_DEBUG");
+    args.debug = dbg ? std::atoi(dbg) : 0;
+  }
 
   const int nbuf = all_dev ? 1 : 2;
   cudaStream_t copy_st = nullptr;
@@ -455,7 +460,7 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
     DevBuf X, idx, counts, support, values, cands, mu, seeds, idx64;
   };
   std::vector<Bufs> bufs(nbuf);
-  DevBuf means(size_t(grid_max) * p->K * sk->ldc * sizeof(T), st);
+  DevBuf means(size_t(stream_scratch_elems<T>(args, grid_max)) * sizeof(T), st);
   DevBuf bad(sizeof(int), st);
   cuda_check(cudaMemsetAsync(bad.p, 0, sizeof(int), st), "memset");
   std::vector<cudaEvent_t> ev_in(nbuf), ev_done(nbuf), ev_out(nbuf);

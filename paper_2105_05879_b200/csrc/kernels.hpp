@@ -54,7 +54,7 @@ struct StreamArgs {
   T* values;         // B x want
   int32_t* cands;    // optional B x want
   T* mu;             // optional B x m
-  // scratch: gridDim.x x K x m_pad batch means
+  // scratch: gridDim.x x 2 slots x (K + 1) x m_pad (batch means + mu)
   T* means;
   int64_t m_pad;
   // pipeline
@@ -62,10 +62,17 @@ struct StreamArgs {
   int stage_stride;  // bytes between ring stages (>= one segment, 128-byte multiple)
   int nseg;
   int chunk;
+  // experiment switches (env FSTG_STREAM_DEBUG; 0 in production):
+  // bit 0: column pipeline only (coefficient warps idle, t = 1)
+  // bit 1: coefficient pipeline only (no column loads, consumers skip the ring)
+  int debug;
 };
 
 template <typename T>
 cudaError_t launch_stream(const StreamArgs<T>& args, bool strict, int grid, cudaStream_t st);
+// Elements of the `means` scratch the kernel needs for `grid` CTAs.
+template <typename T>
+int64_t stream_scratch_elems(const StreamArgs<T>& args, int grid);
 // Persistent grid size the stream kernel wants for this configuration.
 template <typename T>
 int stream_grid_size(const StreamArgs<T>& args, bool strict, int64_t B, size_t* smem_bytes, int* stages,

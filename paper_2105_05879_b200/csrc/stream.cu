@@ -29,15 +29,20 @@
 
 namespace fstg {
 
-constexpr int kNC = 256;                    // consumer threads
-constexpr int kNCW = kNC / 32;              // consumer warps
-constexpr int kCW = 4;                      // coefficient warps
-constexpr int kThreads = kNC + kCW * 32 + 32;  // + coefficient warps + producer warp
+constexpr int kNCW = 8;                     // consumer warps
+constexpr int kNC = kNCW * 32;              // consumer threads
+constexpr int kCW = 8;                      // coefficient warps
+constexpr int kTLW = 7;                     // tail warps (median / select / refine / compact); 24 warps total
+constexpr int kTL = kTLW * 32;              // tail threads
+constexpr int kThreads = kNC + kCW * 32 + kTL + 32;  // + producer warp = 768 (80 regs/thread)
+constexpr int kWarpCoef = kNCW, kWarpTail = kNCW + kCW, kWarpProd = kNCW + kCW + kTLW;
 constexpr int kTRing = 64;                  // slots of the coefficient ring
 constexpr int kNS = 4;                      // samples per coefficient-warp group
 constexpr int kSegBytes = 16384;            // one ring stage at most
-constexpr int kRingBytes = 65536;           // ring budget
 constexpr int kMaxStages = 64;
+constexpr int kXBuf = 3;                    // x buffers: coefficients on v+2 while the tail refines v
+constexpr int kSmemBudget = 227 * 1024;
+constexpr int kBarCoef = 2, kBarTail = 3;   // named barrier ids
 
 template <typename T>
 struct KeyOf;
@@ -78,7 +83,7 @@ struct Vec<double> {
 };
 
 struct SmemLayout {
-  size_t ring, x, tbuf, ibuf, bars, hist, scan, misc, cand, cval, cflag, total;
+  size_t ring, x, tbuf, bars, hist, scan, misc, cand, cval, cflag, total;
 };
 
 template <typename T>
@@ -92,10 +97,9 @@ __host__ __device__ inline SmemLayout smem_layout(int64_t d, int stages, int sta
     return at;
   };
   L.ring = take(size_t(stages) * stage_stride, 1024);
-  L.x = take(2 * size_t(d < 4 ? 4 : d) * sizeof(T), 16);
+  L.x = take(kXBuf * size_t(d < 4 ? 4 : d) * sizeof(T), 16);
   L.tbuf = take(kTRing * sizeof(T), 16);
-  L.ibuf = take(16, 16);
-  L.bars = take((2 * kMaxStages + 2 * kTRing + 4) * sizeof(uint64_t), 8);
+  L.bars = take((2 * kMaxStages + 2 * kTRing + 2 * kXBuf + 4) * sizeof(uint64_t), 8);
   L.hist = take(256 * sizeof(uint32_t), 16);
   L.scan = take(2 * 32 * sizeof(uint32_t), 16);
   L.misc = take(16 * sizeof(unsigned long long), 16);
@@ -106,10 +110,12 @@ __host__ __device__ inline SmemLayout smem_layout(int64_t d, int stages, int sta
   return L;
 }
 
-// Block-wide (consumer threads only) exclusive scan of a uint32 value.
-// Returns the exclusive prefix; *total gets the sum over all consumers.
-__device__ __forceinline__ uint32_t consumer_scan(uint32_t v, uint32_t* scan_smem, int parity, uint32_t* total) {
-  const int lane = threadIdx.x % 32, warp = threadIdx.x / 32;
+// Exclusive scan of a uint32 over the NWARPS warps of one role (named barrier
+// `bar`, local warp index `lw`). *total gets the sum over the group.
+template <int NWARPS>
+__device__ __forceinline__ uint32_t group_scan(uint32_t v, uint32_t* scan_smem, int parity, uint32_t bar, int lw,
+                                               uint32_t* total) {
+  const int lane = threadIdx.x % 32;
   uint32_t inc = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -117,13 +123,13 @@ __device__ __forceinline__ uint32_t consumer_scan(uint32_t v, uint32_t* scan_sme
     if (lane >= o) inc += y;
   }
   uint32_t* tot = scan_smem + parity * 32;
-  if (lane == 31) tot[warp] = inc;
-  named_bar_sync(1, kNC);
+  if (lane == 31) tot[lw] = inc;
+  named_bar_sync(bar, NWARPS * 32);
   uint32_t wpre = 0, all = 0;
 #pragma unroll
-  for (int w = 0; w < kNCW; ++w) {
+  for (int w = 0; w < NWARPS; ++w) {
     const uint32_t t = tot[w];
-    wpre += (w < warp) ? t : 0u;
+    wpre += (w < lw) ? t : 0u;
     all += t;
   }
   *total = all;
@@ -314,9 +320,16 @@ __device__ __forceinline__ T coeff_strict(const StreamArgs<T>& A, const T* xs, u
 }
 
 // --------------------------------------------------------------- kernel ----
-// Warp roles: [0, kNCW) consumers, [kNCW, kNCW + kCW) coefficient warps, last = producer.
+// One persistent CTA per SM; warp roles:
+//   [0, 8)   consumers   : wait t_j and the column ring, acc += t_j * C[:, ell_j],
+//                          per-batch means -> L2 scratch slot (lv & 1)
+//   [8, 16)  coefficients: x -> smem (3 buffers), t_j -> 64-slot ring
+//   [16, 24) tail        : median, radix select, candidate compaction,
+//                          refinement, support compaction for vector lv while
+//                          the consumers already stream lv + 1
+//   24       producer    : bulk copies of the sampled columns (16 KiB stages)
 template <typename T, bool STRICT, int NSEG>
-__global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T> A) {
+__global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T> A) {
   using KT = typename KeyOf<T>::K;
   constexpr int VEC = Vec<T>::N;
   constexpr int SEG = kSegBytes / static_cast<int>(sizeof(T));  // rows per segment
@@ -326,14 +339,16 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
   extern __shared__ __align__(1024) unsigned char smem[];
   const SmemLayout Ls = smem_layout<T>(A.d, A.stages, A.stage_stride, A.want);
   unsigned char* ring = smem + Ls.ring;
-  T* xbuf = reinterpret_cast<T*>(smem + Ls.x);  // two x buffers of d values (double-buffered over vectors)
+  T* xbuf = reinterpret_cast<T*>(smem + Ls.x);
   T* tring = reinterpret_cast<T*>(smem + Ls.tbuf);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + Ls.bars);
   uint64_t* empty = full + kMaxStages;
   uint64_t* t_full = empty + kMaxStages;
   uint64_t* t_empty = t_full + kTRing;
   uint64_t* x_full = t_empty + kTRing;
-  uint64_t* x_empty = x_full + 2;
+  uint64_t* x_empty = x_full + kXBuf;
+  uint64_t* m_full = x_empty + kXBuf;
+  uint64_t* m_empty = m_full + 2;
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + Ls.hist);
   uint32_t* scan = reinterpret_cast<uint32_t*>(smem + Ls.scan);
   unsigned long long* misc = reinterpret_cast<unsigned long long*>(smem + Ls.misc);
@@ -348,6 +363,8 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
   const int64_t seg_last_rows = A.m_pad - int64_t(A.nseg - 1) * SEG;
   const uint32_t stage_bytes_full = static_cast<uint32_t>((A.nseg > 1 ? SEG : A.m_pad) * sizeof(T));
   const uint32_t stage_bytes_last = static_cast<uint32_t>(seg_last_rows * sizeof(T));
+  const int64_t slot_elems = (A.K + 1) * A.m_pad;  // K batch means + mu
+  T* scratch = A.means + int64_t(blockIdx.x) * 2 * slot_elems;
 
   if (tid < S) {
     mbar_init(&full[tid], 1);
@@ -357,9 +374,13 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
     mbar_init(&t_full[tid], 1);
     mbar_init(&t_empty[tid], kNCW);
   }
-  if (tid < 2) {
+  if (tid < kXBuf) {
     mbar_init(&x_full[tid], 1);
-    mbar_init(&x_empty[tid], kNCW);
+    mbar_init(&x_empty[tid], 1);
+  }
+  if (tid < 2) {
+    mbar_init(&m_full[tid], kNCW);
+    mbar_init(&m_empty[tid], 1);
   }
   if (tid < 32) {
     // Walsh base masks: bit f (i' = f/4, e = f%4) = parity(hi3 & i') ^ parity(lo2 & e).
@@ -372,9 +393,9 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
   fence_mbar_init();
   __syncthreads();
 
-  if (warp == kNCW + kCW) {
+  if (warp == kWarpProd) {
     // ======================= producer warp =======================
-    if (lane == 0) {
+    if (lane == 0 && !(A.debug & 2)) {
       const uint64_t pol = policy_evict_first();
       int stage = 0;
       uint32_t phase = 0, used = 0;
@@ -399,27 +420,27 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
     return;
   }
 
-  if (warp >= kNCW) {
+  if (warp >= kWarpCoef && warp < kWarpTail) {
     // ======================= coefficient warps =======================
-    // Load x of each vector into its x buffer, then produce t_j for samples
-    // j = cw, cw + kCW, ... into the t ring (one writer per slot).
-    const int cw = warp - kNCW;
-    const int ctid = tid - kNC;  // 0 .. kCW*32-1
+    const int cw = warp - kWarpCoef;
+    const int ctid = tid - kWarpCoef * 32;  // 0 .. kCW*32-1
     uint32_t lv = 0;
     for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
-      const uint32_t xb = lv & 1u, xu = lv >> 1;
+      const uint32_t xb = lv % kXBuf, xu = lv / kXBuf;
       if (xu > 0) mbar_wait(&x_empty[xb], (xu - 1) & 1u);
       T* xs = xbuf + xb * dx;
       const T* xv = A.X + v * A.ldx;
       for (int64_t p = ctid; p < A.d; p += kCW * 32) xs[p] = (p < A.n) ? xv[p] : T(0);
-      named_bar_sync(2, kCW * 32);
+      named_bar_sync(kBarCoef, kCW * 32);
       if (ctid == 0) mbar_arrive(&x_full[xb]);
       const uint32_t* vidx = A.idx + v * A.N;
       const uint64_t g0 = uint64_t(lv) * uint64_t(A.N);
-      if constexpr (STRICT) {
+      if (A.debug & 1) {
+        // column-pipeline experiment: no coefficients
+      } else if constexpr (STRICT) {
         // One producing thread per ring slot (stride = kTRing): a slot's uses are
-        // then produced in order by the same thread, so a parity wait can never
-        // be two phases ahead.
+        // produced in order by the same thread, so a parity wait is never two
+        // phases ahead.
         static_assert(kCW * 32 >= kTRing, "strict producers need kTRing threads");
         for (int64_t j = ctid; ctid < kTRing && j < A.N; j += kTRing) {
           const uint64_t g = g0 + uint64_t(j);
@@ -475,22 +496,244 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
           __syncwarp();
         }
       }
-      // keep the coefficient warps' x reads ordered before the buffer is reloaded
-      named_bar_sync(2, kCW * 32);
+      named_bar_sync(kBarCoef, kCW * 32);
+    }
+    return;
+  }
+
+  if (warp >= kWarpTail) {
+    // ======================= tail warps =======================
+    const int ttid = tid - kWarpTail * 32, tw = warp - kWarpTail;
+    const uint64_t pol_keep = policy_evict_last();
+    int parity = 0;
+    uint32_t lv = 0;
+    for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
+      const uint32_t slot = lv & 1u, su = lv >> 1, xb = lv % kXBuf, xu = lv / kXBuf;
+      T* means = scratch + slot * slot_elems;
+      T* mus = means + A.K * A.m_pad;
+      mbar_wait(&m_full[slot], su & 1u);
+
+      // ---- median of the K batch means (stream.hpp:126-143) ----
+      for (int64_t c = ttid; int64_t(c) * VEC < A.m_pad; c += kTL) {
+        const int64_t row0 = c * VEC;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const int64_t row = row0 + e;
+          T mu = T(0);
+          if (row < A.m) {
+            if (A.K == 1) {
+              mu = means[row];
+            } else if (A.K == 2) {
+              const T x0 = means[row], x1 = means[A.m_pad + row];
+              const T lo = x0 < x1 ? x0 : x1, hi = x0 < x1 ? x1 : x0;
+              mu = T(0.5) * (lo + hi);
+            } else {
+              // order statistics K/2 (and K/2-1 for even K), ties by batch index
+              const int64_t hK = A.K / 2;
+              T up = T(0), lo = T(0);
+              for (int64_t i = 0; i < A.K; ++i) {
+                const T xi = means[i * A.m_pad + row];
+                int64_t rank = 0;
+                for (int64_t q = 0; q < A.K; ++q) {
+                  const T xq = means[q * A.m_pad + row];
+                  rank += (xq < xi || (xq == xi && q < i)) ? 1 : 0;
+                }
+                if (rank == hK) up = xi;
+                if (rank == hK - 1) lo = xi;
+              }
+              mu = (A.K % 2 == 1) ? up : T(0.5) * (lo + up);
+            }
+            if (A.mu != nullptr) A.mu[v * A.m + row] = mu;
+          }
+          mus[row] = mu;
+        }
+      }
+      named_bar_sync(kBarTail, kTL);
+      if (ttid == 0) mbar_arrive(&m_empty[slot]);  // batch means consumed; mus stays private
+
+      // ---- MSB radix select of the want-th largest |mu| ----
+      KT prefix = 0, kmask = 0;
+      int64_t remaining = A.want;
+      for (int shift = KeyOf<T>::BITS - 8; shift >= 0; shift -= 8) {
+        for (int b = ttid; b < 256; b += kTL) hist[b] = 0;
+        named_bar_sync(kBarTail, kTL);
+        for (int64_t row = ttid; row < A.m_pad + kTL; row += kTL) {
+          // uniform trip count across the warp (row bound checked inside)
+          if (row - ttid >= A.m_pad) break;
+          const bool inr = row < A.m;
+          const KT key = inr ? KeyOf<T>::key(mus[row]) : KT(0);
+          const bool act = inr && ((key & kmask) == prefix);
+          const uint32_t digit = static_cast<uint32_t>((key >> shift) & 0xffu);
+          const uint32_t am = __ballot_sync(0xffffffffu, act);
+          if (act) {
+            const uint32_t peers = __match_any_sync(am, digit);
+            if (lane == __ffs(peers) - 1) atomicAdd(&hist[digit], static_cast<uint32_t>(__popc(peers)));
+          }
+        }
+        named_bar_sync(kBarTail, kTL);
+        if (tw == 0) {
+          uint32_t h[8], sum = 0;
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            h[b] = hist[255 - 8 * lane - b];
+            sum += h[b];
+          }
+          uint32_t inc = sum;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+          }
+          const uint32_t exc = inc - sum;
+          if (exc < static_cast<uint32_t>(remaining) && inc >= static_cast<uint32_t>(remaining)) {
+            uint32_t cum = exc;
+            int b = 0;
+            for (; b < 8; ++b) {
+              if (cum + h[b] >= static_cast<uint32_t>(remaining)) break;
+              cum += h[b];
+            }
+            misc[0] = static_cast<unsigned long long>(255 - 8 * lane - b);
+            misc[1] = static_cast<unsigned long long>(remaining - cum);
+          }
+        }
+        named_bar_sync(kBarTail, kTL);
+        const KT dg = static_cast<KT>(misc[0]);
+        remaining = static_cast<int64_t>(misc[1]);
+        prefix |= dg << shift;
+        kmask |= static_cast<KT>(0xff) << shift;
+      }
+      const KT thr = prefix;
+      const uint32_t quota = static_cast<uint32_t>(remaining);
+
+      // ---- index-ordered compaction of the candidate set (sorted ascending) ----
+      {
+        uint32_t base_gt = 0, base_eq = 0;
+        for (int64_t r0 = 0; r0 < A.m_pad; r0 += int64_t(kTL) * VEC) {
+          const int64_t row0 = r0 + int64_t(ttid) * VEC;
+          uint32_t ngt = 0, neq = 0;
+          KT kk[VEC];
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const int64_t row = row0 + e;
+            kk[e] = (row < A.m) ? KeyOf<T>::key(mus[row]) : KT(0);
+            if (row < A.m) {
+              ngt += kk[e] > thr;
+              neq += kk[e] == thr;
+            }
+          }
+          uint32_t total;
+          const uint32_t pre = group_scan<kTLW>((neq << 16) | ngt, scan, parity, kBarTail, tw, &total);
+          parity ^= 1;
+          uint32_t gt_before = base_gt + (pre & 0xffffu), eq_before = base_eq + (pre >> 16);
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            const int64_t row = row0 + e;
+            if (row < A.m) {
+              if (kk[e] > thr) {
+                cand[gt_before + (eq_before < quota ? eq_before : quota)] = static_cast<int32_t>(row);
+                ++gt_before;
+              } else if (kk[e] == thr) {
+                if (eq_before < quota) cand[gt_before + eq_before] = static_cast<int32_t>(row);
+                ++eq_before;
+              }
+            }
+          }
+          base_gt += total & 0xffffu;
+          base_eq += total >> 16;
+        }
+      }
+      named_bar_sync(kBarTail, kTL);
+
+      // ---- refinement: v_i = a_i . x, fp64 accumulation (stream.hpp:259-266) ----
+      mbar_wait(&x_full[xb], xu & 1u);
+      const T* xs = xbuf + xb * dx;
+      for (int64_t ci = tw; ci < A.want; ci += kTLW) {
+        const int64_t row = cand[ci];
+        const T* arow = A.a + row * A.lda;
+        double dot = 0.0, dot2 = 0.0;
+        if constexpr (sizeof(T) == 4) {
+          constexpr int kRB = 4;  // independent 16-byte loads in flight per lane
+          const int64_t nv = (A.n + 3) / 4;
+          const float4* a4 = reinterpret_cast<const float4*>(arow);
+          const float4* x4 = reinterpret_cast<const float4*>(xs);
+          for (int64_t q0 = lane; q0 < nv; q0 += 32 * kRB) {
+            float4 av[kRB];
+#pragma unroll
+            for (int u = 0; u < kRB; ++u)
+              av[u] = (q0 + 32 * u < nv) ? ldg_f4_policy(a4 + q0 + 32 * u, pol_keep) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < kRB; ++u) {
+              if (q0 + 32 * u < nv) {
+                const float4 xv4 = x4[q0 + 32 * u];
+                double& acc = (u & 1) ? dot2 : dot;
+                acc = fma(static_cast<double>(av[u].x), static_cast<double>(xv4.x), acc);
+                acc = fma(static_cast<double>(av[u].y), static_cast<double>(xv4.y), acc);
+                acc = fma(static_cast<double>(av[u].z), static_cast<double>(xv4.z), acc);
+                acc = fma(static_cast<double>(av[u].w), static_cast<double>(xv4.w), acc);
+              }
+            }
+          }
+        } else {
+          constexpr int kRB = 8;
+          const int64_t nv = (A.n + 1) / 2;
+          const double2* a2 = reinterpret_cast<const double2*>(arow);
+          const double2* x2 = reinterpret_cast<const double2*>(xs);
+          for (int64_t q0 = lane; q0 < nv; q0 += 32 * kRB) {
+            double2 av[kRB];
+#pragma unroll
+            for (int u = 0; u < kRB; ++u)
+              av[u] = (q0 + 32 * u < nv) ? ldg_d2_policy(a2 + q0 + 32 * u, pol_keep) : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < kRB; ++u) {
+              if (q0 + 32 * u < nv) {
+                const double2 xv2 = x2[q0 + 32 * u];
+                double& acc = (u & 1) ? dot2 : dot;
+                acc = fma(av[u].x, xv2.x, acc);
+                acc = fma(av[u].y, xv2.y, acc);
+              }
+            }
+          }
+        }
+        dot += dot2;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        if (lane == 0) {
+          cval[ci] = static_cast<T>(dot);
+          cflag[ci] = fabs(dot) >= A.epsilon ? 1 : 0;
+        }
+      }
+      named_bar_sync(kBarTail, kTL);
+      if (ttid == 0) mbar_arrive(&x_empty[xb]);
+
+      // ---- ordered compaction of the support ----
+      uint32_t out_base = 0;
+      for (int64_t c0 = 0; c0 < A.want; c0 += kTL) {
+        const int64_t ci = c0 + ttid;
+        const uint32_t f = (ci < A.want) ? cflag[ci] : 0u;
+        uint32_t total;
+        const uint32_t pre = group_scan<kTLW>(f, scan, parity, kBarTail, tw, &total);
+        parity ^= 1;
+        if (f) {
+          const int64_t o = v * A.want + out_base + pre;
+          A.support[o] = cand[ci];
+          A.values[o] = cval[ci];
+        }
+        if (A.cands != nullptr && ci < A.want) A.cands[v * A.want + ci] = cand[ci];
+        out_base += total;
+      }
+      if (ttid == 0) A.counts[v] = static_cast<int32_t>(out_base);
+      named_bar_sync(kBarTail, kTL);  // cand/cval/cflag reuse by the next vector
     }
     return;
   }
 
   // ======================= consumer warps =======================
-  const uint64_t pol_keep = policy_evict_last();
-  T* means = A.means + int64_t(blockIdx.x) * A.K * A.m_pad;
   int stage = 0;
   uint32_t phase = 0;
   uint32_t lv = 0;
-
   for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
-    const uint32_t xb = lv & 1u, xu = lv >> 1;
-    const T* xs = xbuf + xb * dx;
+    const uint32_t slot = lv & 1u, su = lv >> 1;
+    T* means = scratch + slot * slot_elems;
     const uint64_t g0 = uint64_t(lv) * uint64_t(A.N);
 
     T acc[NSEG][CPT][VEC];
@@ -504,11 +747,14 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
     int64_t jb = 0, b = 0;  // position inside the batch, batch index
     uint32_t tslot = static_cast<uint32_t>(g0 % kTRing), tphase = static_cast<uint32_t>((g0 / kTRing) & 1);
     for (int64_t j = 0; j < A.N; ++j) {
-      mbar_wait(&t_full[tslot], tphase);
-      const T t = tring[tslot];
+      T t = T(1);
+      if (!(A.debug & 1)) {
+        mbar_wait(&t_full[tslot], tphase);
+        t = tring[tslot];
+      }
 #pragma unroll
       for (int sg = 0; sg < NSEG; ++sg) {
-        if (sg < A.nseg) {
+        if (sg < A.nseg && !(A.debug & 2)) {
           mbar_wait(&full[stage], phase);
           const typename Vec<T>::V* src = reinterpret_cast<const typename Vec<T>::V*>(ring + size_t(stage) * A.stage_stride);
           const int64_t rows_here = (sg == A.nseg - 1) ? seg_last_rows : SEG;
@@ -539,13 +785,14 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
           }
         }
       }
-      if (lane == 0) mbar_arrive(&t_empty[tslot]);
+      if (lane == 0 && !(A.debug & 1)) mbar_arrive(&t_empty[tslot]);
       if (++tslot == kTRing) {
         tslot = 0;
         tphase ^= 1u;
       }
       if (++jb == A.J) {
         // batch b complete: mean = sum / J (IEEE division, stream.hpp:237)
+        if (b == 0 && su > 0) mbar_wait(&m_empty[slot], (su - 1) & 1u);
         T* mb = means + b * A.m_pad;
         const T Jt = static_cast<T>(A.J);
 #pragma unroll
@@ -565,207 +812,8 @@ __global__ void __launch_bounds__(kThreads, 2) stream_kernel(const StreamArgs<T>
         ++b;
       }
     }
-
-
-    // ---- median of the K batch means (stream.hpp:126-143), keys |mu| ----
-    KT keys[NSEG][CPT][VEC];
-    T muv[NSEG][CPT][VEC];
-#pragma unroll
-    for (int sg = 0; sg < NSEG; ++sg)
-#pragma unroll
-      for (int c = 0; c < CPT; ++c)
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const int64_t row = int64_t(sg) * SEG + int64_t(tid + c * kNC) * VEC + e;
-          T mu = T(0);
-          KT key = 0;
-          if (sg < A.nseg && row < A.m) {
-            if (A.K == 1) {
-              mu = means[row];
-            } else if (A.K == 2) {
-              const T x0 = means[row], x1 = means[A.m_pad + row];
-              const T lo = x0 < x1 ? x0 : x1, hi = x0 < x1 ? x1 : x0;
-              mu = T(0.5) * (lo + hi);
-            } else {
-              // rank selection of order statistics K/2 (and K/2-1 for even K)
-              const int64_t hK = A.K / 2;
-              T up = T(0), lo = T(0);
-              for (int64_t i = 0; i < A.K; ++i) {
-                const T xi = means[i * A.m_pad + row];
-                int64_t rank = 0;
-                for (int64_t q = 0; q < A.K; ++q) {
-                  const T xq = means[q * A.m_pad + row];
-                  rank += (xq < xi || (xq == xi && q < i)) ? 1 : 0;
-                }
-                if (rank == hK) up = xi;
-                if (rank == hK - 1) lo = xi;
-              }
-              mu = (A.K % 2 == 1) ? up : T(0.5) * (lo + up);
-            }
-            key = KeyOf<T>::key(mu);
-          }
-          muv[sg][c][e] = mu;
-          keys[sg][c][e] = key;
-          if (A.mu != nullptr && sg < A.nseg && row < A.m) A.mu[v * A.m + row] = mu;
-        }
-
-    // ---- MSB radix select of the want-th largest key ----
-    KT prefix = 0, kmask = 0;
-    int64_t remaining = A.want;
-    for (int shift = KeyOf<T>::BITS - 8; shift >= 0; shift -= 8) {
-      hist[tid] = 0;  // kNC == 256 bins
-      named_bar_sync(1, kNC);
-#pragma unroll
-      for (int sg = 0; sg < NSEG; ++sg)
-#pragma unroll
-        for (int c = 0; c < CPT; ++c)
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            const int64_t row = int64_t(sg) * SEG + int64_t(tid + c * kNC) * VEC + e;
-            const bool act = (sg < A.nseg) && (row < A.m) && ((keys[sg][c][e] & kmask) == prefix);
-            const uint32_t digit = static_cast<uint32_t>((keys[sg][c][e] >> shift) & 0xffu);
-            const uint32_t am = __ballot_sync(0xffffffffu, act);
-            if (act) {
-              const uint32_t peers = __match_any_sync(am, digit);
-              if (lane == __ffs(peers) - 1) atomicAdd(&hist[digit], static_cast<uint32_t>(__popc(peers)));
-            }
-          }
-      named_bar_sync(1, kNC);
-      if (warp == 0) {
-        // lane l owns bins [255-8l-7, 255-8l], scanned from the top digit down
-        uint32_t h[8], sum = 0;
-#pragma unroll
-        for (int b = 0; b < 8; ++b) {
-          h[b] = hist[255 - 8 * lane - b];
-          sum += h[b];
-        }
-        uint32_t inc = sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-          if (lane >= o) inc += y;
-        }
-        const uint32_t exc = inc - sum;
-        const bool here = exc < static_cast<uint32_t>(remaining) && inc >= static_cast<uint32_t>(remaining);
-        if (here) {
-          uint32_t cum = exc;
-          int b = 0;
-          for (; b < 8; ++b) {
-            if (cum + h[b] >= static_cast<uint32_t>(remaining)) break;
-            cum += h[b];
-          }
-          misc[0] = static_cast<unsigned long long>(255 - 8 * lane - b);
-          misc[1] = static_cast<unsigned long long>(remaining - cum);
-        }
-      }
-      named_bar_sync(1, kNC);
-      const KT dg = static_cast<KT>(misc[0]);
-      remaining = static_cast<int64_t>(misc[1]);
-      prefix |= dg << shift;
-      kmask |= static_cast<KT>(0xff) << shift;
-    }
-    // prefix = threshold key T; `remaining` keys equal to T are taken (smallest indices first).
-    const KT thr = prefix;
-    const uint32_t quota = static_cast<uint32_t>(remaining);
-
-    // ---- index-ordered compaction of the candidate set (sorted ascending) ----
-    uint32_t base_gt = 0, base_eq = 0;
-    int parity = 0;
-#pragma unroll
-    for (int sg = 0; sg < NSEG; ++sg)
-#pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        if (sg < A.nseg) {
-          uint32_t ngt = 0, neq = 0;
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            const int64_t row = int64_t(sg) * SEG + int64_t(tid + c * kNC) * VEC + e;
-            if (row < A.m) {
-              ngt += keys[sg][c][e] > thr;
-              neq += keys[sg][c][e] == thr;
-            }
-          }
-          uint32_t total;
-          const uint32_t pre = consumer_scan((neq << 16) | ngt, scan, parity, &total);
-          parity ^= 1;
-          uint32_t gt_before = base_gt + (pre & 0xffffu), eq_before = base_eq + (pre >> 16);
-#pragma unroll
-          for (int e = 0; e < VEC; ++e) {
-            const int64_t row = int64_t(sg) * SEG + int64_t(tid + c * kNC) * VEC + e;
-            if (row < A.m) {
-              const KT kk = keys[sg][c][e];
-              if (kk > thr) {
-                cand[gt_before + (eq_before < quota ? eq_before : quota)] = static_cast<int32_t>(row);
-                ++gt_before;
-              } else if (kk == thr) {
-                if (eq_before < quota) cand[gt_before + eq_before] = static_cast<int32_t>(row);
-                ++eq_before;
-              }
-            }
-          }
-          base_gt += total & 0xffffu;
-          base_eq += total >> 16;
-        }
-      }
-    named_bar_sync(1, kNC);
-
-    // ---- refinement: v_i = a_i . x, fp64 accumulation (stream.hpp:259-266) ----
-    mbar_wait(&x_full[xb], xu & 1u);
-    for (int64_t ci = warp; ci < A.want; ci += kNCW) {
-      const int64_t row = cand[ci];
-      const T* arow = A.a + row * A.lda;
-      double dot = 0.0;
-      if constexpr (sizeof(T) == 4) {
-        const int64_t nv = (A.n + 3) / 4;
-        const float4* a4 = reinterpret_cast<const float4*>(arow);
-        const float4* x4 = reinterpret_cast<const float4*>(xs);
-        for (int64_t q = lane; q < nv; q += 32) {
-          const float4 av = ldg_f4_policy(a4 + q, pol_keep);
-          const float4 xv4 = x4[q];
-          dot = fma(static_cast<double>(av.x), static_cast<double>(xv4.x), dot);
-          dot = fma(static_cast<double>(av.y), static_cast<double>(xv4.y), dot);
-          dot = fma(static_cast<double>(av.z), static_cast<double>(xv4.z), dot);
-          dot = fma(static_cast<double>(av.w), static_cast<double>(xv4.w), dot);
-        }
-      } else {
-        const int64_t nv = (A.n + 1) / 2;
-        const double2* a2 = reinterpret_cast<const double2*>(arow);
-        const double2* x2 = reinterpret_cast<const double2*>(xs);
-        for (int64_t q = lane; q < nv; q += 32) {
-          const double2 av = ldg_d2_policy(a2 + q, pol_keep);
-          const double2 xv2 = x2[q];
-          dot = fma(av.x, xv2.x, dot);
-          dot = fma(av.y, xv2.y, dot);
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-      if (lane == 0) {
-        cval[ci] = static_cast<T>(dot);
-        cflag[ci] = fabs(dot) >= A.epsilon ? 1 : 0;
-      }
-    }
-    named_bar_sync(1, kNC);
-
-    // ---- ordered compaction of the support ----
-    uint32_t out_base = 0;
-    for (int64_t c0 = 0; c0 < A.want; c0 += kNC) {
-      const int64_t ci = c0 + tid;
-      const uint32_t f = (ci < A.want) ? cflag[ci] : 0u;
-      uint32_t total;
-      const uint32_t pre = consumer_scan(f, scan, parity, &total);
-      parity ^= 1;
-      if (f) {
-        const int64_t o = v * A.want + out_base + pre;
-        A.support[o] = cand[ci];
-        A.values[o] = cval[ci];
-      }
-      if (A.cands != nullptr && ci < A.want) A.cands[v * A.want + ci] = cand[ci];
-      out_base += total;
-    }
-    if (tid == 0) A.counts[v] = static_cast<int32_t>(out_base);
-    named_bar_sync(1, kNC);  // cand/cval reuse by the next vector; xs reads done
-    if (lane == 0) mbar_arrive(&x_empty[xb]);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&m_full[slot]);
   }
 }
 
@@ -775,7 +823,8 @@ int stream_grid_size(const StreamArgs<T>& args, bool strict, int64_t B, size_t* 
                      int* stage_stride) {
   const int64_t stage_bytes = (args.m_pad * int64_t(sizeof(T)) < kSegBytes) ? args.m_pad * int64_t(sizeof(T)) : kSegBytes;
   const int stride = static_cast<int>((stage_bytes + 127) / 128 * 128);
-  int S = static_cast<int>(kRingBytes / stride);
+  const SmemLayout L0 = smem_layout<T>(args.d, 0, stride, args.want);
+  int S = static_cast<int>((kSmemBudget - static_cast<int64_t>(L0.total) - 1024) / stride);
   if (S > kMaxStages) S = kMaxStages;
   if (S < 2) S = 2;
   const SmemLayout L = smem_layout<T>(args.d, S, stride, args.want);
@@ -783,13 +832,17 @@ int stream_grid_size(const StreamArgs<T>& args, bool strict, int64_t B, size_t* 
   *stages = S;
   *stage_stride = stride;
   (void)strict;
-  int per_sm = (L.total <= 100 * 1024) ? 2 : 1;
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t grid = int64_t(sms) * per_sm;
+  int64_t grid = sms;
   if (grid > B) grid = B;
   if (grid < 1) grid = 1;
   return static_cast<int>(grid);
+}
+
+template <typename T>
+int64_t stream_scratch_elems(const StreamArgs<T>& args, int grid) {
+  return int64_t(grid) * 2 * (args.K + 1) * args.m_pad;
 }
 
 template <typename T, bool STRICT, int NSEG>
@@ -804,7 +857,7 @@ static cudaError_t launch_one(const StreamArgs<T>& args, int grid, size_t smem, 
 template <typename T>
 cudaError_t launch_stream(const StreamArgs<T>& args, bool strict, int grid, cudaStream_t st) {
   const SmemLayout L = smem_layout<T>(args.d, args.stages, args.stage_stride, args.want);
-  if (L.total > 227 * 1024) return cudaErrorInvalidConfiguration;
+  if (L.total > static_cast<size_t>(kSmemBudget)) return cudaErrorInvalidConfiguration;
   if (args.nseg <= 1) {
     return strict ? launch_one<T, true, 1>(args, grid, L.total, st) : launch_one<T, false, 1>(args, grid, L.total, st);
   }
@@ -818,5 +871,7 @@ template cudaError_t launch_stream<float>(const StreamArgs<float>&, bool, int, c
 template cudaError_t launch_stream<double>(const StreamArgs<double>&, bool, int, cudaStream_t);
 template int stream_grid_size<float>(const StreamArgs<float>&, bool, int64_t, size_t*, int*, int*);
 template int stream_grid_size<double>(const StreamArgs<double>&, bool, int64_t, size_t*, int*, int*);
+template int64_t stream_scratch_elems<float>(const StreamArgs<float>&, int);
+template int64_t stream_scratch_elems<double>(const StreamArgs<double>&, int);
 
 }  // namespace fstg
