@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--replicate", default="recompute", choices=["recompute", "allgather"],
+                    help="sketch replica per GPU: local recompute after the A broadcast, or basis-sharded "
+                         "preprocessing + NVLink all-gather")
     return ap.parse_args()
 
 
@@ -157,7 +160,7 @@ def cpu_sample(a64: np.ndarray, X64: np.ndarray, seeds: np.ndarray, J: int, K: i
 def run_b200(args):
     import torch
     import torch.distributed as dist
-    from paper_2105_05879_b200 import fst, generators
+    from paper_2105_05879_b200 import fst, generators, parallel
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -167,27 +170,42 @@ def run_b200(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(dev))
 
-    # ---- A: built on rank 0, broadcast over NCCL (the only collective) ----
+    # ---- A: built on rank 0, broadcast over NCCL ----
     if rank == 0:
         A64 = generators.haar_orthogonal(N_DIM, A_SEED, dev)
     else:
         A64 = torch.empty((N_DIM, N_DIM), dtype=torch.float64, device=dev)
     if world > 1:
-        dist.broadcast(A64, src=0)
+        parallel.broadcast_matrix(A64, src=0)
     A32 = A64.float().contiguous()
 
-    # ---- preprocess (replica per GPU; device time) ----
+    # ---- sketch replica per GPU (device time) ----
     fst.profile_enable(True)
     fst.profile_reset()
-    sk = fst.preprocess(A32, device=local)
+    gather_ms = 0.0
+    if args.replicate == "allgather" and world > 1:
+        nk = fst.design_params(fst.even_log2_ceil(N_DIM))[0] // 2
+        first, count = parallel.basis_shards(nk, world)[rank]
+        sk = fst.preprocess_shard(A32, first, first + count, True, device=local)
+        full = parallel.sketch_tensor(sk)
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        parallel.allgather_basis_shards(full, world, rank, nk, sk.d, sk.column_stride)
+        g1.record()
+        torch.cuda.synchronize()
+        gather_ms = g0.elapsed_time(g1)
+    else:
+        sk = fst.preprocess(A32, device=local)
     fwht_ms, _ = fst.profile_read("preprocess_fwht")
     ident_ms, _ = fst.profile_read("preprocess_identity")
-    pre_ms = sk.preprocess_ms
+    pre_ms = parallel.max_over_ranks(sk.preprocess_ms + gather_ms, device=dev)
     sketch_bytes = sk.L * sk.m * 4
 
     # ---- this rank's shard of the vector stream ----
     B = args.batch
-    prob = generators.config3_problem(B=B, seed=X_SEED, device=dev, first=rank * B, A64=A64)
+    first, _ = parallel.vector_shard(rank, world, B)
+    prob = generators.config3_problem(B=B, seed=X_SEED, device=dev, first=first, A64=A64)
     X = prob.X
     seeds_dev = torch.from_numpy(prob.seeds.view(np.int64)).to(dev)
     p = fst.StreamParams(epsilon=EPS, s=S, J=args.J, K=args.K, widen=WIDEN)
@@ -225,10 +243,7 @@ def run_b200(args):
     stream_ms, stream_launches = fst.profile_read("stream")
     draw_ms, draw_launches = fst.profile_read("draw")
     fst.profile_enable(False)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = parallel.max_over_ranks(ms, device=dev)
     counts = out.counts.cpu().numpy()
     value = world * B * args.steps / (ms_max / 1e3)
 
@@ -258,10 +273,7 @@ def run_b200(args):
             fst.transform_batch(sk, Xh, p, seeds_h, out=oh, stream=sptr)
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
-        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * B * args.steps / float(te.item()), "unit": "vectors/s",
+        e2e = {"value": world * B * args.steps / parallel.max_over_ranks(e2e_s, device=dev), "unit": "vectors/s",
                "h2d_bytes_per_step": int(B * N_DIM * 4 + B * 8),
                "d2h_bytes_per_step": int(B * 4 + B * want * 8)}
         assert np.array_equal(oh.counts.numpy(), counts), "host-buffer path disagrees with device path"
@@ -299,7 +311,8 @@ def run_b200(args):
                    "parallelism": f"vector-sharded x{world}, sketch replicated per GPU",
                    "l2": "inputs larger than L2 (137.5 GB sketch; 1 GiB of x per step)",
                    "mean_support": float(np.mean(counts))},
-        "preprocess": {"ms": pre_ms, "fwht_ms": fwht_ms, "identity_ms": ident_ms,
+        "preprocess": {"ms": pre_ms, "fwht_ms": fwht_ms, "identity_ms": ident_ms, "allgather_ms": gather_ms,
+                       "replicate": args.replicate,
                        "sketch_bytes": sketch_bytes,
                        "roofline": {"bound": "hbm", "achieved": pre_achieved, "peak": peak, "unit": "GB/s",
                                     "frac": (pre_achieved / peak) if pre_achieved else None,

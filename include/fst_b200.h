@@ -109,7 +109,10 @@ int fstg_preprocess(const void* a, int dtype, int64_t m, int64_t n, int device, 
                     fstg_sketch** out);
 /* Builds only Kerdock bases [basis_begin, basis_end) (and the identity block
  * when include_identity != 0) into a full-size sketch: the basis-sharded
- * preprocessing of a multi-GPU replica. */
+ * preprocessing of a multi-GPU replica. The columns of
+ * the other bases are left unwritten; they are filled in place by the NVLink
+ * all-gather (paper_2105_05879_b200/parallel.py) through
+ * fstg_sketch_device_columns. */
 int fstg_preprocess_shard(const void* a, int dtype, int64_t m, int64_t n, int device, void* stream,
                           int64_t basis_begin, int64_t basis_end, int include_identity, fstg_sketch** out);
 int fstg_sketch_info_get(const fstg_sketch* sk, fstg_sketch_info* info);

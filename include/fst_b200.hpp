@@ -1,0 +1,214 @@
+// fst_b200.hpp — C++ mirror of the reference `fst` API for the thresholded-Ax
+// hot path, implemented over the C-ABI in fst_b200.h (libfst_b200.so).
+//
+// Same names, argument meaning and exception classes as
+// /root/reference/proj/include/fst/{sketch,stream}.hpp, minus Eigen: matrices
+// are row-major spans (pointer + m + n), vectors are std::vector<double>.
+//   fst::preprocess              sketch.hpp:149   -> fst_b200::preprocess
+//   fst::Sketch                  sketch.hpp:70    -> fst_b200::Sketch (device-resident, move-only)
+//   fst::StreamParams            stream.hpp:22    -> fst_b200::StreamParams
+//   fst::choose_params           stream.hpp:58    -> fst_b200::choose_params
+//   fst::draw_samples            stream.hpp:173   -> fst_b200::draw_samples
+//   fst::transform               stream.hpp:272   -> fst_b200::transform
+//   fst::transform_with_samples  stream.hpp:197   -> fst_b200::transform_with_samples
+//   fst::TransformResult         stream.hpp:53    -> fst_b200::TransformResult
+// plus the batched stream entry point transform_batch. Errors are rethrown as
+// std::invalid_argument / std::out_of_range / std::overflow_error /
+// std::runtime_error exactly where the reference throws them; CUDA failures
+// (no CPU fallback exists) throw fst_b200::cuda_error.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "fst_b200.h"
+
+namespace fst_b200 {
+
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct not_supported : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+  if (rc == FSTG_OK) return;
+  const std::string msg = fstg_last_error();
+  switch (rc) {
+    case FSTG_ERR_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case FSTG_ERR_OUT_OF_RANGE: throw std::out_of_range(msg);
+    case FSTG_ERR_OVERFLOW: throw std::overflow_error(msg);
+    case FSTG_ERR_RUNTIME: throw std::runtime_error(msg);
+    case FSTG_ERR_NOT_SUPPORTED: throw not_supported(msg);
+    default: throw cuda_error(msg);
+  }
+}
+
+/// stream.hpp:22-39
+struct StreamParams {
+  double epsilon = 0;
+  double delta = 0;
+  std::int64_t s = 1;
+  std::int64_t J = 1;
+  std::int64_t K = 1;
+  std::int64_t widen = 10;
+  std::uint64_t seed = 0;
+  int mode = FSTG_MODE_DEFAULT;
+
+  fstg_stream_params c() const { return {epsilon, delta, s, J, K, widen, seed, mode, 0}; }
+  void validate() const {
+    const fstg_stream_params p = c();
+    check(fstg_validate_params(&p));
+  }
+};
+
+/// stream.hpp:41-54 (values are double for an fp64 sketch, widened from fp32 otherwise)
+struct TransformResult {
+  std::vector<std::int64_t> support;
+  std::vector<double> values;
+  std::vector<std::int64_t> candidate_set;
+  std::vector<double> mu;
+  std::int64_t samples_used = 0;
+};
+
+/// sketch.hpp:70-142 — owns the device-resident sketch; immutable, move-only.
+class Sketch {
+ public:
+  Sketch() = default;
+  explicit Sketch(fstg_sketch* h) : h_(h) { check(fstg_sketch_info_get(h_, &info_)); }
+  Sketch(Sketch&& o) noexcept : h_(o.h_), info_(o.info_) { o.h_ = nullptr; }
+  Sketch& operator=(Sketch&& o) noexcept {
+    if (this != &o) {
+      reset();
+      h_ = o.h_;
+      info_ = o.info_;
+      o.h_ = nullptr;
+    }
+    return *this;
+  }
+  Sketch(const Sketch&) = delete;
+  Sketch& operator=(const Sketch&) = delete;
+  ~Sketch() { reset(); }
+
+  std::int64_t m() const { return info_.m; }
+  std::int64_t n() const { return info_.n; }
+  int k() const { return info_.k; }
+  std::int64_t d() const { return info_.d; }
+  std::int64_t L() const { return info_.L; }
+  bool is_f64() const { return info_.dtype == FSTG_F64; }
+  double row_norm_max() const { return info_.row_norm_max; }
+  double preprocess_ms() const { return info_.preprocess_ms; }
+  const fstg_sketch* handle() const { return h_; }
+
+  /// Sketch::column (sketch.hpp:114-117), copied to the host as double.
+  std::vector<double> column(std::int64_t ell) const {
+    std::vector<double> out(static_cast<std::size_t>(m()));
+    if (is_f64()) {
+      check(fstg_sketch_column(h_, ell, out.data()));
+    } else {
+      std::vector<float> f(out.size());
+      check(fstg_sketch_column(h_, ell, f.data()));
+      for (std::size_t i = 0; i < f.size(); ++i) out[i] = f[i];
+    }
+    return out;
+  }
+
+ private:
+  void reset() {
+    if (h_) fstg_destroy(h_);
+    h_ = nullptr;
+  }
+  fstg_sketch* h_ = nullptr;
+  fstg_sketch_info info_{};
+};
+
+/// sketch.hpp:149-211 on device `device`; `a` is m x n row-major double.
+inline Sketch preprocess(const double* a, std::int64_t m, std::int64_t n, int device = 0) {
+  fstg_sketch* h = nullptr;
+  check(fstg_preprocess(a, FSTG_F64, m, n, device, nullptr, &h));
+  return Sketch(h);
+}
+/// fp32 sketch (the B200 headline configuration).
+inline Sketch preprocess(const float* a, std::int64_t m, std::int64_t n, int device = 0) {
+  fstg_sketch* h = nullptr;
+  check(fstg_preprocess(a, FSTG_F32, m, n, device, nullptr, &h));
+  return Sketch(h);
+}
+
+/// stream.hpp:58-69
+inline std::pair<std::int64_t, std::int64_t> choose_params(double row_norm_max, double gamma, double eta,
+                                                           std::int64_t m) {
+  std::int64_t J = 0, K = 0;
+  check(fstg_choose_params(row_norm_max, gamma, eta, m, &J, &K));
+  return {J, K};
+}
+
+/// stream.hpp:173-182
+inline std::vector<std::int64_t> draw_samples(const Sketch& sk, const StreamParams& p) {
+  p.validate();
+  std::vector<std::int64_t> out(static_cast<std::size_t>(p.J * p.K));
+  const fstg_stream_params c = p.c();
+  check(fstg_draw_samples(sk.handle(), &c, &p.seed, 1, out.data(), nullptr));
+  return out;
+}
+
+namespace detail {
+template <typename T>
+TransformResult run_one(const Sketch& sk, const std::vector<T>& x, const StreamParams& p,
+                        const std::vector<std::int64_t>* indices) {
+  if (static_cast<std::int64_t>(x.size()) != sk.n())
+    throw std::invalid_argument("transform: vector length does not match sketch");
+  p.validate();
+  const std::int64_t want = fstg_candidate_count(p.s, p.widen, sk.m());
+  std::int32_t count = 0;
+  std::vector<std::int32_t> support(static_cast<std::size_t>(want)), cand(static_cast<std::size_t>(want));
+  std::vector<T> values(static_cast<std::size_t>(want)), mu(static_cast<std::size_t>(sk.m()));
+  const fstg_stream_params c = p.c();
+  if (indices)
+    check(fstg_transform_with_samples_batch(sk.handle(), x.data(), 1, &c, indices->data(), &count, support.data(),
+                                            values.data(), cand.data(), mu.data(), nullptr));
+  else
+    check(fstg_transform_batch(sk.handle(), x.data(), 1, &c, &p.seed, &count, support.data(), values.data(),
+                               cand.data(), mu.data(), nullptr));
+  TransformResult r;
+  r.support.assign(support.begin(), support.begin() + count);
+  r.values.assign(values.begin(), values.begin() + count);
+  r.candidate_set.assign(cand.begin(), cand.end());
+  r.mu.assign(mu.begin(), mu.end());
+  r.samples_used = p.J * p.K;
+  return r;
+}
+}  // namespace detail
+
+/// stream.hpp:272-275 (x must match the sketch dtype: double for fp64, float for fp32)
+inline TransformResult transform(const Sketch& sk, const std::vector<double>& x, const StreamParams& p) {
+  if (!sk.is_f64()) throw std::invalid_argument("transform: fp32 sketch needs a float vector");
+  return detail::run_one(sk, x, p, nullptr);
+}
+inline TransformResult transform(const Sketch& sk, const std::vector<float>& x, const StreamParams& p) {
+  if (sk.is_f64()) throw std::invalid_argument("transform: fp64 sketch needs a double vector");
+  return detail::run_one(sk, x, p, nullptr);
+}
+
+/// stream.hpp:197-268
+inline TransformResult transform_with_samples(const Sketch& sk, const std::vector<double>& x, const StreamParams& p,
+                                              const std::vector<std::int64_t>& indices) {
+  if (static_cast<std::int64_t>(indices.size()) != p.J * p.K)
+    throw std::invalid_argument("transform: drawn sample count does not match J*K");
+  return detail::run_one(sk, x, p, &indices);
+}
+
+/// The batched stream: X is B x n row-major (host or device memory, sketch
+/// dtype); per-vector seeds; outputs as documented in fst_b200.h.
+inline void transform_batch(const Sketch& sk, const void* X, std::int64_t B, const StreamParams& p,
+                            const std::uint64_t* seeds, std::int32_t* counts, std::int32_t* support, void* values,
+                            void* stream = nullptr) {
+  const fstg_stream_params c = p.c();
+  check(fstg_transform_batch(sk.handle(), X, B, &c, seeds, counts, support, values, nullptr, nullptr, stream));
+}
+
+}  // namespace fst_b200

@@ -270,8 +270,9 @@ void build_sketch(fstg_sketch* sk, const void* a_in, cudaStream_t st, int64_t b0
     }
   }
   sk->device_bytes += col_bytes;
-  if (sk->ldc != m || b0 != 0 || b1 != nk || !identity)
-    cuda_check(cudaMemsetAsync(sk->cols, 0, col_bytes, st), "memset sketch");
+  // Row padding (ldc > m) is zeroed; a basis-sharded build leaves the other
+  // ranks' Kerdock blocks unwritten (they are filled by the all-gather).
+  if (sk->ldc != m) cuda_check(cudaMemsetAsync(sk->cols, 0, col_bytes, st), "memset sketch");
 
   // Kerdock sign tables
   const std::vector<uint32_t> rev = reversed_row_table(D);

@@ -1,0 +1,97 @@
+"""Multi-GPU plumbing for the thresholded-Ax stream (one process per GPU).
+
+The path shards naturally: every vector is an independent
+unit with its own seed, so the stream is split by global vector index with no
+data-path collective; the representation is replicated per GPU. The only
+collectives are in preparation:
+
+  * ``broadcast_matrix``   — A from rank 0 to every rank (NCCL over NVLink).
+  * ``allgather_sketch``   — basis-sharded preprocessing: rank r builds Kerdock
+    bases ``basis_shards(nk, world)[r]`` (a contiguous byte range of the
+    column-major sketch) and an in-place all-gather over NVLink completes every
+    replica (option (ii) of §8(e); option (i), local recompute after the
+    broadcast, is the default because it moves 64 MB instead of ~120 GB).
+  * ``max_over_ranks``     — step time = max over ranks (device-timed).
+
+Everything here is host logic; it is tested on CPU with the gloo backend
+(tests/test_parallel_gloo.py) and runs on NCCL in bench.py.
+"""
+from __future__ import annotations
+
+from typing import List, Tuple
+
+import numpy as np
+
+
+def vector_shard(rank: int, world: int, per_rank: int) -> Tuple[int, int]:
+    """Weak scaling: rank r streams global vectors [r * per_rank, (r + 1) * per_rank)."""
+    if not (0 <= rank < world) or per_rank < 0:
+        raise ValueError("vector_shard: bad rank/world/per_rank")
+    return rank * per_rank, per_rank
+
+
+def strong_shard(rank: int, world: int, total: int) -> Tuple[int, int]:
+    """Strong scaling split of `total` vectors (contiguous, sizes differ by at most 1)."""
+    if not (0 <= rank < world) or total < 0:
+        raise ValueError("strong_shard: bad rank/world/total")
+    base, extra = divmod(total, world)
+    first = rank * base + min(rank, extra)
+    return first, base + (1 if rank < extra else 0)
+
+
+def basis_shards(nk: int, world: int) -> List[Tuple[int, int]]:
+    """Contiguous Kerdock-basis ranges per rank covering [0, nk) (sizes differ by at most 1)."""
+    if nk < 0 or world < 1:
+        raise ValueError("basis_shards: bad nk/world")
+    return [strong_shard(r, world, nk) for r in range(world)]
+
+
+def shard_element_range(basis_range: Tuple[int, int], d: int, ldc: int) -> Tuple[int, int]:
+    """Element offsets [lo, hi) of a basis range inside the column-major sketch."""
+    first, count = basis_range
+    return first * d * ldc, (first + count) * d * ldc
+
+
+class _CudaView:
+    """Zero-copy device buffer exposed through __cuda_array_interface__ (for NCCL)."""
+
+    def __init__(self, ptr: int, nelem: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (nelem,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def sketch_tensor(sk, torch_mod=None):
+    """A flat torch view of the sketch's device columns (no copy)."""
+    import torch
+    nelem = sk.L * sk.column_stride
+    typestr = "<f8" if sk.dtype == np.float64 else "<f4"
+    return torch.as_tensor(_CudaView(sk.device_columns_ptr(), nelem, typestr), device=f"cuda:{sk.device}")
+
+
+def allgather_basis_shards(full, world: int, rank: int, nk: int, d: int, ldc: int, group=None) -> None:
+    """In-place all-gather of the Kerdock block of a flat sketch tensor `full`.
+
+    Requires equal shard sizes (nk % world == 0; true for every config with
+    world a power of two); each rank's own shard must already be filled."""
+    import torch.distributed as dist
+    if nk % world:
+        raise ValueError("allgather_basis_shards: nk must divide evenly across ranks")
+    per = (nk // world) * d * ldc
+    kerdock = full[: nk * d * ldc]
+    mine = kerdock[rank * per:(rank + 1) * per]
+    dist.all_gather_into_tensor(kerdock, mine, group=group)
+
+
+def broadcast_matrix(a, src: int = 0, group=None):
+    import torch.distributed as dist
+    dist.broadcast(a, src=src, group=group)
+    return a
+
+
+def max_over_ranks(value: float, device=None, group=None) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())

@@ -322,3 +322,25 @@ def test_config3_full_size_vs_gathered_oracle(fst, orc):
         assert g.support.tolist() == r.support.tolist()
         np.testing.assert_allclose(g.values, r.values, rtol=1e-5)
     sk.close()
+
+
+# ---------------------------------------------------- basis-sharded build ----
+def test_preprocess_shards_assemble_full_sketch(fst, orc):
+    """Two basis shards (as two ranks would build them) assembled through the
+    zero-copy sketch views equal the single-GPU sketch bit for bit; this is the
+    data movement the NVLink all-gather performs in parallel.allgather_basis_shards."""
+    import torch
+    from paper_2105_05879_b200 import parallel
+    a = _rand(40, 256, 11, np.float32)
+    full = fst.preprocess(a)
+    nk = full.d // 2
+    (f0, c0), (f1, c1) = parallel.basis_shards(nk, 2)
+    s0 = fst.preprocess_shard(a, f0, f0 + c0, True)
+    s1 = fst.preprocess_shard(a, f1, f1 + c1, True)
+    t_full, t0, t1 = parallel.sketch_tensor(full), parallel.sketch_tensor(s0), parallel.sketch_tensor(s1)
+    lo, hi = parallel.shard_element_range((f1, c1), full.d, full.column_stride)
+    t0[lo:hi].copy_(t1[lo:hi])  # "receive" rank 1's shard into rank 0's replica
+    torch.cuda.synchronize()
+    assert torch.equal(t0, t_full)
+    with pytest.raises(IndexError):
+        fst.preprocess_shard(a, 0, nk + 1, True)
