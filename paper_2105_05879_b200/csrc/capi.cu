@@ -199,6 +199,24 @@ __global__ void gather_kernel(const T* __restrict__ cols, int64_t ldc, int64_t m
   }
 }
 
+// Per-call scratch comes from the device's stream-ordered pool. The pool's
+// release threshold is raised once per device so memory freed at the end of a
+// call stays cached for the next one (the default threshold returns it to the
+// driver at every synchronisation, which made every step re-allocate).
+void keep_pool_warm(int device) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), device) != done.end()) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t threshold = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold);
+  }
+  cudaGetLastError();
+  done.push_back(device);
+}
+
 // Device scratch released at scope exit (stream-ordered).
 struct DevBuf {
   void* p = nullptr;
@@ -406,6 +424,7 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   const bool strict = p->mode == FSTG_MODE_STRICT || (p->mode == FSTG_MODE_DEFAULT && sk->dtype == FSTG_F64);
   if (p->mode < 0 || p->mode > 2) throw InvalidArgument("StreamParams: unknown mode");
   cuda_check(cudaSetDevice(sk->device), "cudaSetDevice");
+  keep_pool_warm(sk->device);
 
   const int64_t n = sk->n, m = sk->m;
   const bool x_dev = is_device_ptr(X);

@@ -15,7 +15,10 @@
 //  * identity_kernel — column (d/2)*d + w = sqrt(d) * A[:, w] (sketch.hpp:200-208).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <string>
 
 #include "fst_common.cuh"
 #include "kernels.hpp"
@@ -318,7 +321,7 @@ __global__ void __launch_bounds__(512, 1) fwht12_tmem_kernel(const float* __rest
                                                              int64_t n, const uint32_t* __restrict__ qplain,
                                                              int64_t basis_begin, int64_t basis_end,
                                                              int bases_per_cta, float* __restrict__ cols,
-                                                             int64_t ldc) {
+                                                             int64_t ldc, int store_mode) {
   constexpr int E = 64, R = 8, RS = 4096 + 4, D = 4096, WPB = 128;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* tile = reinterpret_cast<float*>(smem_raw);
@@ -328,7 +331,6 @@ __global__ void __launch_bounds__(512, 1) fwht12_tmem_kernel(const float* __rest
   const int64_t i0 = int64_t(blockIdx.x) * R;
   const int64_t s_first = basis_begin + int64_t(blockIdx.y) * bases_per_cta;
   const int64_t s_last = min(basis_end, s_first + bases_per_cta);
-  const uint64_t pol_stream = policy_evict_first();
 
   const int r1 = tid / E, p1 = tid % E;
   const int64_t row1 = i0 + r1;
@@ -373,11 +375,21 @@ __global__ void __launch_bounds__(512, 1) fwht12_tmem_kernel(const float* __rest
     tmem_wait_st();
   }
 
+  // sign words of the next basis are prefetched one iteration ahead (L2 latency)
+  uint32_t q0n = 0, q1n = 0;
+  if (s_first < s_last) {
+    q0n = __ldg(qplain + s_first * WPB + 2 * p1);
+    q1n = __ldg(qplain + s_first * WPB + 2 * p1 + 1);
+  }
   for (int64_t s = s_first; s < s_last; ++s) {
     float v[E];
     tmem_ld_x32(taddr, v);
     tmem_ld_x32(taddr + 32, v + 32);
-    const uint32_t q0 = __ldg(qplain + s * WPB + 2 * p1), q1 = __ldg(qplain + s * WPB + 2 * p1 + 1);
+    const uint32_t q0 = q0n, q1 = q1n;
+    if (s + 1 < s_last) {
+      q0n = __ldg(qplain + (s + 1) * WPB + 2 * p1);
+      q1n = __ldg(qplain + (s + 1) * WPB + 2 * p1 + 1);
+    }
     tmem_wait_ld();
     // sign mask (sketch.hpp:185): flip the sign bit where Q_s(pos) = 1 (exact)
 #pragma unroll
@@ -385,7 +397,7 @@ __global__ void __launch_bounds__(512, 1) fwht12_tmem_kernel(const float* __rest
 #pragma unroll
     for (int e = 0; e < 32; ++e)
       v[32 + e] = __uint_as_float(__float_as_uint(v[32 + e]) ^ ((q1 << (31 - e)) & 0x80000000u));
-    reg_fwht64_packed(v);  // position bits 0..5
+    if (store_mode < 2) reg_fwht64_packed(v);  // position bits 0..5 (store_mode 2: write-path experiment)
     __syncthreads();       // previous basis' phase-2 reads done
     {
       float* dst = tile + r1 * RS + p1 * E;
@@ -401,14 +413,183 @@ __global__ void __launch_bounds__(512, 1) fwht12_tmem_kernel(const float* __rest
 #pragma unroll
       for (int e = 0; e < E; ++e) v[e] = src[e * E + 4 * (cq ^ (e & 15))];
     }
-    reg_fwht64_packed(v);  // position bits 6..11
+    if (store_mode < 2) reg_fwht64_packed(v);  // position bits 6..11
     if (row2 < m) {
       // incremental addressing keeps 64 hoisted 64-bit offsets out of registers
       float* ptr = cols + (s * D + q2) * ldc + row2;
       const int64_t step = int64_t(E) * ldc;
+      if (store_mode == 0) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          ptr[0] = v[e];  // default policy: L2 merges the 4 CTAs' 32-byte sectors of a line
+          ptr += step;
+          asm volatile("" : "+l"(ptr));
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+          __stcs(ptr, v[e]);  // streaming store (evict-first)
+          ptr += step;
+          asm volatile("" : "+l"(ptr));
+        }
+      }
+    }
+  }
+
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_base_slot) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// k = 12 fp32, row-pair variant: 256 threads, 8 rows per CTA; thread (rp, p)
+// owns rows (2rp, 2rp+1) x positions p*64 .. p*64+63 as 64 float2 pairs, so
+// every butterfly stage is one FADD2 (x+y) + one FFMA2(y, -1, x) per pair
+// butterfly on natural register pairs, the Kerdock sign mask is shared by the
+// two rows, and the write-back is STG.64 (two consecutive rows of a column).
+// smem tile: row-pair block rp at rp * RSP floats, pair of position pos at
+// 2*pos, 16-byte chunk c of thread p stored at chunk c ^ (p & 7);
+// RSP = 8192 + 8 makes both the STS.128 and the LDS.64 patterns conflict-free.
+// TMEM: warp w owns lanes 32*(w%4) .. +31, columns 128*(w/4) .. +127.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256, 1) fwht12_pairs_kernel(const float* __restrict__ a, int64_t lda, int64_t m,
+                                                              int64_t n, const uint32_t* __restrict__ qplain,
+                                                              int64_t basis_begin, int64_t basis_end,
+                                                              int bases_per_cta, float* __restrict__ cols,
+                                                              int64_t ldc) {
+  constexpr int E = 64, D = 4096, WPB = 128, RSP = 8192 + 8;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* tile = reinterpret_cast<float*>(smem_raw);
+  __shared__ uint32_t tmem_base_slot;
+
+  const int tid = threadIdx.x, warp = tid / 32;
+  const int64_t i0 = int64_t(blockIdx.x) * 8;
+  const int64_t s_first = basis_begin + int64_t(blockIdx.y) * bases_per_cta;
+  const int64_t s_last = min(basis_end, s_first + bases_per_cta);
+
+  const int rp = tid / E, p1 = tid % E;    // phase 1: row pair, position group
+  const int rp2 = tid % 4, q2 = tid / 4;   // phase 2: row pair, position residue
+  const int64_t row_a = i0 + 2 * rp, row2 = i0 + 2 * rp2;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t taddr = tmem_base_slot + (static_cast<uint32_t>(32 * (warp % 4)) << 16) +
+                         static_cast<uint32_t>(128 * (warp / 4));
+  {
+    // park the two rows' 64 values as interleaved pairs (v[2e], v[2e+1]) = (row_a, row_a+1)
+    float v[2 * E];
+    const int64_t pos0 = int64_t(p1) * E;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int64_t row = row_a + r;
+      if (row < m && pos0 + E <= n) {
+        const float* arow = a + row * lda + pos0;
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(arow + e));
+          v[2 * e + r] = f.x;
+          v[2 * (e + 1) + r] = f.y;
+          v[2 * (e + 2) + r] = f.z;
+          v[2 * (e + 3) + r] = f.w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[2 * e + r] = (row < m && pos0 + e < n) ? a[row * lda + pos0 + e] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_st_x32(taddr + 32 * c, v + 32 * c);
+    tmem_wait_st();
+  }
+
+  uint32_t q0n = 0, q1n = 0;
+  if (s_first < s_last) {
+    q0n = __ldg(qplain + s_first * WPB + 2 * p1);
+    q1n = __ldg(qplain + s_first * WPB + 2 * p1 + 1);
+  }
+  for (int64_t s = s_first; s < s_last; ++s) {
+    float2 V[E];
+    {
+      float* vf = reinterpret_cast<float*>(V);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_x32(taddr + 32 * c, vf + 32 * c);
+    }
+    const uint32_t q0 = q0n, q1 = q1n;
+    if (s + 1 < s_last) {
+      q0n = __ldg(qplain + (s + 1) * WPB + 2 * p1);
+      q1n = __ldg(qplain + (s + 1) * WPB + 2 * p1 + 1);
+    }
+    tmem_wait_ld();
+    // Kerdock sign mask (sketch.hpp:185), shared by both rows of the pair
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t msk = ((e < 32 ? q0 : q1) << (31 - (e & 31))) & 0x80000000u;
+      V[e].x = __uint_as_float(__float_as_uint(V[e].x) ^ msk);
+      V[e].y = __uint_as_float(__float_as_uint(V[e].y) ^ msk);
+    }
+    // position bits 0..5 (h = 1 .. 32), reference stage order
+#pragma unroll
+    for (int hb = 0; hb < 6; ++hb) {
+      const int h = 1 << hb;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        stg_f32_policy(ptr, v[e], pol_stream);
+        if ((e & h) == 0) {
+          const float2 x = V[e], y = V[e + h];
+          V[e] = __fadd2_rn(x, y);
+          V[e + h] = __ffma2_rn(y, make_float2(-1.f, -1.f), x);
+        }
+      }
+    }
+    __syncthreads();  // previous basis' phase-2 reads done
+    {
+      float* dst = tile + rp * RSP + p1 * (2 * E);
+#pragma unroll
+      for (int c = 0; c < 32; ++c)
+        *reinterpret_cast<float4*>(dst + 4 * (c ^ (p1 & 7))) = make_float4(V[2 * c].x, V[2 * c].y, V[2 * c + 1].x,
+                                                                          V[2 * c + 1].y);
+    }
+    __syncthreads();
+    {
+      const float* src = tile + rp2 * RSP + 2 * (q2 & 1);
+      const int cq = q2 >> 1;
+#pragma unroll
+      for (int e = 0; e < E; ++e) V[e] = *reinterpret_cast<const float2*>(src + e * (2 * E) + 4 * (cq ^ (e & 7)));
+    }
+    // position bits 6..11 (h = 64 .. 2048)
+#pragma unroll
+    for (int hb = 0; hb < 6; ++hb) {
+      const int h = 1 << hb;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        if ((e & h) == 0) {
+          const float2 x = V[e], y = V[e + h];
+          V[e] = __fadd2_rn(x, y);
+          V[e + h] = __ffma2_rn(y, make_float2(-1.f, -1.f), x);
+        }
+      }
+    }
+    // transposed write-back (sketch.hpp:191-196): column s*d + e*64 + q2, rows row2, row2+1
+    if (row2 + 1 < m) {
+      float* ptr = cols + (s * D + q2) * ldc + row2;
+      const int64_t step = int64_t(E) * ldc;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        __stcs(reinterpret_cast<float2*>(ptr), V[e]);
+        ptr += step;
+        asm volatile("" : "+l"(ptr));
+      }
+    } else if (row2 < m) {
+      float* ptr = cols + (s * D + q2) * ldc + row2;
+      const int64_t step = int64_t(E) * ldc;
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        __stcs(ptr, V[e].x);
         ptr += step;
         asm volatile("" : "+l"(ptr));
       }
@@ -507,10 +688,30 @@ static cudaError_t launch_fwht12_tmem(const float* a, int64_t lda, int64_t m, in
   if (nb <= 0) return cudaSuccess;
   const int64_t row_tiles = (m + 7) / 8;
   int bpc = 32;
+  if (const char* b = std::getenv("FSTG_FWHT_BPC")) bpc = std::max(1, std::atoi(b));  // A/B experiments only
   while (bpc > 1 && row_tiles * ((nb + bpc - 1) / bpc) < 148 * 8) bpc /= 2;
   const int64_t gy = (nb + bpc - 1) / bpc;
   if (row_tiles > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
+  const char* sm = std::getenv("FSTG_FWHT_STORE");  // A/B experiments only
+  const int store_mode = (sm && std::string(sm) == "cs") ? 1 : (sm && std::string(sm) == "nofwht") ? 2 : 0;
   fwht12_tmem_kernel<<<dim3(static_cast<unsigned>(row_tiles), static_cast<unsigned>(gy)), 512, smem, st>>>(
+      a, lda, m, n, qplain, b0, b1, bpc, cols, ldc, store_mode);
+  return cudaGetLastError();
+}
+
+static cudaError_t launch_fwht12_pairs(const float* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
+                                       int64_t b0, int64_t b1, float* cols, int64_t ldc, cudaStream_t st) {
+  constexpr size_t smem = size_t(4) * (8192 + 8) * sizeof(float);
+  cudaError_t e = cudaFuncSetAttribute(fwht12_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  if (e != cudaSuccess) return e;
+  const int64_t nb = b1 - b0;
+  if (nb <= 0) return cudaSuccess;
+  const int64_t row_tiles = (m + 7) / 8;
+  int bpc = 32;
+  while (bpc > 1 && row_tiles * ((nb + bpc - 1) / bpc) < 148 * 8) bpc /= 2;
+  const int64_t gy = (nb + bpc - 1) / bpc;
+  if (row_tiles > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
+  fwht12_pairs_kernel<<<dim3(static_cast<unsigned>(row_tiles), static_cast<unsigned>(gy)), 256, smem, st>>>(
       a, lda, m, n, qplain, b0, b1, bpc, cols, ldc);
   return cudaGetLastError();
 }
@@ -519,7 +720,11 @@ template <typename T>
 cudaError_t launch_fwht_sketch(int k, const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
                                int64_t b0, int64_t b1, T* cols, int64_t ldc, cudaStream_t st) {
   if constexpr (sizeof(T) == 4) {
-    if (k == 12 && (lda % 4) == 0) return launch_fwht12_tmem(a, lda, m, n, qplain, b0, b1, cols, ldc, st);
+    if (k == 12 && (lda % 4) == 0) {
+      const char* var = std::getenv("FSTG_FWHT_VARIANT");  // A/B experiments only
+      if (var && std::string(var) == "pairs") return launch_fwht12_pairs(a, lda, m, n, qplain, b0, b1, cols, ldc, st);
+      return launch_fwht12_tmem(a, lda, m, n, qplain, b0, b1, cols, ldc, st);
+    }
   }
   switch (k) {
     case 2: return launch_fwht_k<T, 2>(a, lda, m, n, qplain, b0, b1, cols, ldc, st);

@@ -22,7 +22,9 @@
 // sequential coefficient sums and separately-rounded multiply/add.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "fst_common.cuh"
 #include "kernels.hpp"
@@ -42,6 +44,7 @@ constexpr int kSegBytes = 16384;            // one ring stage at most
 constexpr int kMaxStages = 64;
 constexpr int kXBuf = 3;                    // x buffers: coefficients on v+2 while the tail refines v
 constexpr int kSmemBudget = 227 * 1024;
+constexpr int kInflightBytes = 5 * 16384;    // column bytes in flight per SM
 constexpr int kBarCoef = 2, kBarTail = 3;   // named barrier ids
 
 template <typename T>
@@ -825,6 +828,9 @@ int stream_grid_size(const StreamArgs<T>& args, bool strict, int64_t B, size_t* 
   const int stride = static_cast<int>((stage_bytes + 127) / 128 * 128);
   const SmemLayout L0 = smem_layout<T>(args.d, 0, stride, args.want);
   int S = static_cast<int>((kSmemBudget - static_cast<int64_t>(L0.total) - 1024) / stride);
+  // ~64 KiB in flight per SM is enough (profiles/r01_stream_stages.txt: 3-5 x 16 KiB stages beat 10)
+  S = std::min(S, std::max(4, static_cast<int>(kInflightBytes / stride)));
+  if (const char* e = std::getenv("FSTG_STREAM_STAGES")) S = std::min(S, std::max(2, std::atoi(e)));  // experiments
   if (S > kMaxStages) S = kMaxStages;
   if (S < 2) S = 2;
   const SmemLayout L = smem_layout<T>(args.d, S, stride, args.want);
