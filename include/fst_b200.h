@@ -39,7 +39,13 @@ typedef enum fstg_status {
   FSTG_ERR_OVERFLOW = 3,         /* std::overflow_error (stream.hpp:340-341) */
   FSTG_ERR_RUNTIME = 4,          /* std::runtime_error: allocation (sketch.hpp:162-165) */
   FSTG_ERR_CUDA = 5,             /* CUDA runtime failure / no sm_100 device */
-  FSTG_ERR_NOT_SUPPORTED = 6     /* shape outside this build's GPU limits */
+  FSTG_ERR_NOT_SUPPORTED = 6,    /* shape outside this build's GPU limits */
+  FSTG_ERR_IO = 7,               /* IoError (io.hpp:23): open/read/write failure */
+  FSTG_ERR_MAGIC = 8,            /* MagicMismatchError (io.hpp:26) */
+  FSTG_ERR_VERSION = 9,          /* VersionUnsupportedError (io.hpp:29) */
+  FSTG_ERR_TRUNCATED = 10,       /* TruncatedPayloadError (io.hpp:32) */
+  FSTG_ERR_MALFORMED = 11,       /* MalformedHeaderError (io.hpp:35) */
+  FSTG_ERR_NO_MATRIX = 12        /* std::logic_error "Sketch: no embedded matrix" (sketch.hpp:109) */
 } fstg_status;
 
 typedef enum fstg_dtype { FSTG_F32 = 0, FSTG_F64 = 1 } fstg_dtype;
@@ -129,6 +135,21 @@ int fstg_sketch_gather(const fstg_sketch* sk, const int64_t* indices, int64_t co
 /* Device time of the last preprocess (ms, CUDA events). */
 int fstg_sketch_preprocess_ms(const fstg_sketch* sk, double* ms);
 void fstg_destroy(fstg_sketch* sk);
+
+/* ---------------------------------------------------- FSTK persistence ---- */
+/* save (sketch.hpp:213-232): FSTK, little-endian: "FSTK", u32 version, u64 m n
+ * k d L, u8 hasEmbeddedA, L columns of m values, then the m x n row-major A.
+ * version 1 = the reference's format (float64 payload; an fp32 sketch is
+ * widened exactly), readable by fst::load. version 2 = the same layout with a
+ * float32 payload (half the bytes; the reference rejects it with
+ * VersionUnsupportedError). Columns stream device -> pinned host -> file. */
+int fstg_save(const fstg_sketch* sk, const char* path, int version);
+/* load (sketch.hpp:241-302) straight into HBM on `device`, with the
+ * reference's header validation and error classes. `dtype` selects the
+ * device representation (FSTG_F64 keeps a v1 payload as is; FSTG_F32 rounds it
+ * to float32 on the GPU; a v2 file is always fp32). A file without an embedded
+ * A loads, but transforms on it fail with FSTG_ERR_NO_MATRIX (sketch.hpp:109). */
+int fstg_load(const char* path, int dtype, int device, void* stream, fstg_sketch** out);
 
 /* ------------------------------------------------------------ streaming ---- */
 /* draw_samples (stream.hpp:173-182) for B vectors: vector v uses seeds[v] in

@@ -18,7 +18,28 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libfst_oracle.so")
 _lib = None
 
-_ERRORS = {1: ValueError, 2: IndexError, 3: OverflowError, 4: RuntimeError, 5: RuntimeError}
+class IoError(OSError):
+    pass
+
+
+class MagicMismatchError(IoError):
+    pass
+
+
+class VersionUnsupportedError(IoError):
+    pass
+
+
+class TruncatedPayloadError(IoError):
+    pass
+
+
+class MalformedHeaderError(IoError):
+    pass
+
+
+_ERRORS = {1: ValueError, 2: IndexError, 3: OverflowError, 4: RuntimeError, 5: RuntimeError, 7: IoError,
+           8: MagicMismatchError, 9: VersionUnsupportedError, 10: TruncatedPayloadError, 11: MalformedHeaderError}
 
 
 def build() -> str:
@@ -197,6 +218,20 @@ def preprocess(a, dtype=np.float64, threads: int = 1) -> Sketch:
     _check(lib().orc_preprocess(_ptr(a), C.c_int(code), C.c_int64(a.shape[0]), C.c_int64(a.shape[1]),
                                 C.c_int(threads), C.byref(h)))
     return Sketch(h.value, a)
+
+
+def save(sk: Sketch, path: str, with_a: bool = True) -> None:
+    """sketch.hpp:215-232 (FSTK v1, fp64)."""
+    _check(lib().orc_save(sk._h, str(path).encode(), C.c_int(1 if with_a else 0)))
+
+
+def load(path: str) -> Sketch:
+    """sketch.hpp:241-302."""
+    h = C.c_void_p()
+    _check(lib().orc_load(str(path).encode(), C.byref(h)))
+    sk = Sketch(h.value, np.zeros((0, 0)))
+    sk.dtype = np.float64
+    return sk
 
 
 # ------------------------------------------------------------------ rng ----

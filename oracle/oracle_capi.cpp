@@ -5,6 +5,7 @@
 //   4 std::runtime_error, 5 std::logic_error / other.
 #include <atomic>
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <exception>
@@ -383,6 +384,83 @@ int orc_bench_gathered(const double* a, std::int64_t m, std::int64_t n, const do
     if (failed) throw std::runtime_error("bench_gathered: worker failed");
     *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   });
+}
+
+// ---- FSTK save/load (sketch.hpp:213-302), fp64 reference format ----
+// status: 7 IoError, 8 MagicMismatch, 9 VersionUnsupported, 10 TruncatedPayload, 11 MalformedHeader
+static void put_le(std::FILE* f, std::uint64_t v, int bytes) {
+  unsigned char b[8];
+  for (int i = 0; i < bytes; ++i) b[i] = static_cast<unsigned char>(v >> (8 * i));
+  std::fwrite(b, 1, bytes, f);
+}
+
+int orc_save(void* hv, const char* path, int with_a) {
+  auto* h = static_cast<OrcSketch*>(hv);
+  if (h->dtype != 1) { g_err = "oracle save: fp64 sketches only"; return 1; }
+  std::FILE* f = std::fopen(path, "wb");
+  if (!f) { g_err = std::string("cannot open for writing: ") + path; return 7; }
+  const auto& sk = h->d;
+  std::fwrite("FSTK", 1, 4, f);
+  put_le(f, 1, 4);
+  put_le(f, sk.m, 8); put_le(f, sk.n, 8); put_le(f, sk.design.k, 8); put_le(f, sk.design.d, 8); put_le(f, sk.design.L, 8);
+  const unsigned char flag = with_a ? 1 : 0;
+  std::fwrite(&flag, 1, 1, f);
+  std::fwrite(sk.columns.data(), 8, sk.columns.size(), f);
+  if (with_a) std::fwrite(sk.a.data(), 8, sk.a.size(), f);
+  const bool ok = std::fclose(f) == 0;
+  if (!ok) { g_err = std::string("write failed: ") + path; return 7; }
+  return 0;
+}
+
+int orc_load(const char* path, void** out) {
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) { g_err = std::string("cannot open for reading: ") + path; return 7; }
+  std::fseek(f, 0, SEEK_END);
+  const std::uint64_t fsize = static_cast<std::uint64_t>(std::ftell(f));
+  std::fseek(f, 0, SEEK_SET);
+  auto fail = [&](int code, const std::string& msg) { std::fclose(f); g_err = msg; return code; };
+  if (fsize < 49) return fail(10, std::string("sketch file shorter than its header: ") + path);
+  unsigned char hd[49];
+  if (std::fread(hd, 1, 49, f) != 49) return fail(10, "short header");
+  auto get = [&](int off, int bytes) { std::uint64_t v = 0; for (int i = 0; i < bytes; ++i) v |= std::uint64_t(hd[off + i]) << (8 * i); return v; };
+  if (std::memcmp(hd, "FSTK", 4) != 0) return fail(8, std::string("not an FSTK sketch file: ") + path);
+  const std::uint64_t version = get(4, 4);
+  if (version != 1) return fail(9, "unsupported FSTK version " + std::to_string(version));
+  const std::uint64_t m = get(8, 8), n = get(16, 8), k = get(24, 8), d = get(32, 8), L = get(40, 8);
+  const int flag = hd[48];
+  if (m == 0 || n == 0 || k < 2 || k > 16 || k % 2 != 0 || d != (std::uint64_t{1} << k) || L != d * (d / 2 + 1) || n > d ||
+      (flag != 0 && flag != 1))
+    return fail(11, std::string("inconsistent FSTK header fields: ") + path);
+  const std::uint64_t expected = 49 + 8 * m * L + (flag ? 8 * m * n : 0);
+  if (fsize < expected) return fail(10, std::string("FSTK payload truncated: ") + path);
+  if (fsize > expected) return fail(11, "FSTK file larger than its header declares");
+  auto* h = new OrcSketch();
+  h->dtype = 1;
+  h->d.design = DesignParams::make(static_cast<int>(k));
+  h->d.m = static_cast<std::int64_t>(m);
+  h->d.n = static_cast<std::int64_t>(n);
+  h->d.columns.resize(m * L);
+  bool ok = std::fread(h->d.columns.data(), 8, m * L, f) == m * L;
+  if (flag) {
+    h->d.a.resize(m * n);
+    ok = ok && std::fread(h->d.a.data(), 8, m * n, f) == m * n;
+  }
+  std::fclose(f);
+  if (!ok) {
+    delete h;
+    g_err = std::string("FSTK payload truncated: ") + path;
+    return 10;
+  }
+  for (std::int64_t s = 0; s < h->d.design.kerdock_bases(); ++s) h->d.kerdock.push_back(kerdock_matrix(h->d.design, s));
+  double rn = 0;
+  for (std::uint64_t i = 0; i < (flag ? m : 0); ++i) {
+    double acc = 0;
+    for (std::uint64_t j = 0; j < n; ++j) acc += h->d.a[i * n + j] * h->d.a[i * n + j];
+    rn = std::max(rn, std::sqrt(acc));
+  }
+  h->d.row_norm_max = rn;
+  *out = h;
+  return 0;
 }
 
 // ---- generators ----

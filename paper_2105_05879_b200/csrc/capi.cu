@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <filesystem>
 #include <map>
 #include <mutex>
 #include <string>
@@ -32,11 +33,19 @@ struct fstg_sketch {
   double row_norm_max = 0;
   double preprocess_ms = 0;
   uint64_t device_bytes = 0;
+  bool has_a = true;  // false for an FSTK file saved without the embedded A
 };
 
 namespace {
 
 thread_local std::string g_error;
+
+// IoError family (io.hpp:23-37) and the reference's logic_error for a sketch
+// without its embedded matrix (sketch.hpp:109), each with its status code.
+struct CodedError : std::runtime_error {
+  int code;
+  CodedError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
 
 int set_error(int code, const std::string& msg) {
   g_error = msg;
@@ -56,6 +65,8 @@ int guarded(Fn&& fn) {
   try {
     fn();
     return FSTG_OK;
+  } catch (const CodedError& e) {
+    return set_error(e.code, e.what());
   } catch (const InvalidArgument& e) {
     return set_error(FSTG_ERR_INVALID_ARGUMENT, e.what());
   } catch (const OutOfRange& e) {
@@ -362,6 +373,226 @@ void destroy_sketch(fstg_sketch* sk) {
   delete sk;
 }
 
+// --------------------------------------------------------- persistence ----
+// FSTK (sketch.hpp:213-302): "FSTK", u32 version, u64 m n k d L, u8 flag,
+// L columns of m values, then m*n row-major A; little-endian; 49-byte header.
+constexpr uint64_t kFstkHeader = 49;
+constexpr size_t kChunkBytes = size_t(64) << 20;
+
+__global__ void f64_to_f32_pitched(const double* __restrict__ src, int64_t rows, int64_t cols_src, float* __restrict__ dst,
+                                   int64_t ld_dst) {
+  const int64_t total = rows * cols_src;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols_src, c = i % cols_src;
+    dst[r * ld_dst + c] = static_cast<float>(src[i]);
+  }
+}
+
+struct PinnedBuf {
+  void* p = nullptr;
+  explicit PinnedBuf(size_t bytes) { cuda_check(cudaMallocHost(&p, bytes), "cudaMallocHost"); }
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+};
+
+struct File {
+  FILE* f = nullptr;
+  File(const char* path, const char* mode) : f(std::fopen(path, mode)) {}
+  ~File() {
+    if (f) std::fclose(f);
+  }
+};
+
+void put_le(std::vector<unsigned char>& h, uint64_t v, int bytes) {
+  for (int i = 0; i < bytes; ++i) h.push_back(static_cast<unsigned char>(v >> (8 * i)));
+}
+
+uint64_t get_le(const unsigned char* p, int bytes) {
+  uint64_t v = 0;
+  for (int i = 0; i < bytes; ++i) v |= static_cast<uint64_t>(p[i]) << (8 * i);
+  return v;
+}
+
+// Streams a device matrix (rows x cols, pitch ld elements of size es_dev) to
+// the file as rows x cols values of size es_file (widening f32 -> f64 exactly).
+void write_device_matrix(FILE* f, const void* dev, int64_t rows, int64_t cols, int64_t ld, size_t es_dev,
+                         size_t es_file, PinnedBuf& buf, const std::string& path) {
+  const size_t row_bytes_dev = size_t(cols) * es_dev;
+  const int64_t rows_per_chunk = std::max<int64_t>(1, int64_t(kChunkBytes / (size_t(cols) * 8)));
+  std::vector<double> wide;
+  for (int64_t r0 = 0; r0 < rows; r0 += rows_per_chunk) {
+    const int64_t rc = std::min(rows_per_chunk, rows - r0);
+    cuda_check(cudaMemcpy2D(buf.p, row_bytes_dev, static_cast<const char*>(dev) + size_t(r0) * ld * es_dev, size_t(ld) * es_dev,
+                            row_bytes_dev, size_t(rc), cudaMemcpyDeviceToHost),
+               "D2H sketch chunk");
+    const size_t count = size_t(rc) * size_t(cols);
+    size_t wrote;
+    if (es_dev == es_file) {
+      wrote = std::fwrite(buf.p, es_file, count, f);
+    } else {  // f32 device -> f64 file (exact)
+      wide.resize(count);
+      const float* src = static_cast<const float*>(buf.p);
+      for (size_t i = 0; i < count; ++i) wide[i] = static_cast<double>(src[i]);
+      wrote = std::fwrite(wide.data(), 8, count, f);
+    }
+    if (wrote != count) throw CodedError(FSTG_ERR_IO, "write failed: " + path);
+  }
+}
+
+void save_impl(const fstg_sketch* sk, const char* path, int version) {
+  if (!sk || !path) throw InvalidArgument("save: null argument");
+  if (version != 1 && version != 2) throw InvalidArgument("save: FSTK version must be 1 (float64) or 2 (float32)");
+  if (version == 2 && sk->dtype != FSTG_F32) throw InvalidArgument("save: FSTK v2 holds float32 sketches");
+  cuda_check(cudaSetDevice(sk->device), "cudaSetDevice");
+  File file(path, "wb");
+  if (!file.f) throw CodedError(FSTG_ERR_IO, std::string("cannot open for writing: ") + path);
+  std::vector<unsigned char> h = {'F', 'S', 'T', 'K'};
+  put_le(h, static_cast<uint64_t>(version), 4);
+  put_le(h, static_cast<uint64_t>(sk->m), 8);
+  put_le(h, static_cast<uint64_t>(sk->n), 8);
+  put_le(h, static_cast<uint64_t>(sk->design.k), 8);
+  put_le(h, static_cast<uint64_t>(sk->design.d), 8);
+  put_le(h, static_cast<uint64_t>(sk->design.L), 8);
+  h.push_back(sk->has_a ? 1 : 0);
+  if (std::fwrite(h.data(), 1, h.size(), file.f) != h.size()) throw CodedError(FSTG_ERR_IO, std::string("write failed: ") + path);
+  const size_t es_dev = dtype_size(sk->dtype), es_file = version == 1 ? 8 : 4;
+  PinnedBuf buf(kChunkBytes);
+  cuda_check(cudaDeviceSynchronize(), "sync before save");
+  write_device_matrix(file.f, sk->cols, sk->design.L, sk->m, sk->ldc, es_dev, es_file, buf, path);
+  if (sk->has_a) write_device_matrix(file.f, sk->a, sk->m, sk->n, sk->lda, es_dev, es_file, buf, path);
+  if (std::fflush(file.f) != 0) throw CodedError(FSTG_ERR_IO, std::string("write failed: ") + path);
+}
+
+// Reads rows x cols values of es_file bytes from the file into a device matrix
+// (pitch ld elements of the sketch dtype), rounding f64 -> f32 on the GPU.
+void read_device_matrix(FILE* f, void* dev, int64_t rows, int64_t cols, int64_t ld, size_t es_file, size_t es_dev,
+                        PinnedBuf& buf, void* staging, cudaStream_t st, const std::string& path) {
+  const int64_t rows_per_chunk = std::max<int64_t>(1, int64_t(kChunkBytes / (size_t(cols) * es_file)));
+  for (int64_t r0 = 0; r0 < rows; r0 += rows_per_chunk) {
+    const int64_t rc = std::min(rows_per_chunk, rows - r0);
+    const size_t count = size_t(rc) * size_t(cols);
+    cuda_check(cudaStreamSynchronize(st), "sync");  // previous chunk's copy out of `buf` is done
+    if (std::fread(buf.p, es_file, count, f) != count)
+      throw CodedError(FSTG_ERR_TRUNCATED, "FSTK payload truncated: " + path);
+    if (es_file == es_dev) {
+      cuda_check(cudaMemcpy2DAsync(static_cast<char*>(dev) + size_t(r0) * ld * es_dev, size_t(ld) * es_dev, buf.p,
+                                   size_t(cols) * es_file, size_t(cols) * es_file, size_t(rc), cudaMemcpyHostToDevice,
+                                   st),
+                 "H2D sketch chunk");
+    } else {
+      cuda_check(cudaMemcpyAsync(staging, buf.p, count * es_file, cudaMemcpyHostToDevice, st), "H2D sketch chunk");
+      f64_to_f32_pitched<<<148 * 8, 256, 0, st>>>(static_cast<const double*>(staging), rc, cols,
+                                                 static_cast<float*>(dev) + size_t(r0) * ld, ld);
+      cuda_check(cudaGetLastError(), "f64->f32");
+    }
+  }
+  cuda_check(cudaStreamSynchronize(st), "sync");
+}
+
+void load_impl(const char* path, int dtype, int device, void* stream, fstg_sketch** out) {
+  if (!path || !out) throw InvalidArgument("load: null argument");
+  *out = nullptr;
+  const std::string p(path);
+  std::error_code ec;
+  const uint64_t fsize = std::filesystem::file_size(p, ec);
+  if (ec) throw CodedError(FSTG_ERR_IO, "cannot open for reading: " + p);
+  if (fsize < kFstkHeader) throw CodedError(FSTG_ERR_TRUNCATED, "sketch file shorter than its header: " + p);
+  File file(path, "rb");
+  if (!file.f) throw CodedError(FSTG_ERR_IO, "cannot open for reading: " + p);
+  unsigned char h[kFstkHeader];
+  if (std::fread(h, 1, kFstkHeader, file.f) != kFstkHeader)
+    throw CodedError(FSTG_ERR_TRUNCATED, "sketch file shorter than its header: " + p);
+  if (std::memcmp(h, "FSTK", 4) != 0) throw CodedError(FSTG_ERR_MAGIC, "not an FSTK sketch file: " + p);
+  const uint64_t version = get_le(h + 4, 4);
+  if (version != 1 && version != 2)
+    throw CodedError(FSTG_ERR_VERSION, "unsupported FSTK version " + std::to_string(version));
+  const uint64_t m = get_le(h + 8, 8), n = get_le(h + 16, 8), k = get_le(h + 24, 8), d = get_le(h + 32, 8),
+                 L = get_le(h + 40, 8);
+  const int flag = h[48];
+  if (m == 0 || n == 0 || k < 2 || k > 16 || k % 2 != 0 || d != (uint64_t{1} << k) || L != d * (d / 2 + 1) || n > d ||
+      (flag != 0 && flag != 1))
+    throw CodedError(FSTG_ERR_MALFORMED, "inconsistent FSTK header fields: " + p);
+  const size_t es_file = version == 1 ? 8 : 4;
+  const uint64_t col_bytes = es_file * m * L;
+  const uint64_t expected = kFstkHeader + col_bytes + (flag ? es_file * m * n : 0);
+  if (fsize < expected) throw CodedError(FSTG_ERR_TRUNCATED, "FSTK payload truncated: " + p);
+  if (fsize > expected) throw CodedError(FSTG_ERR_MALFORMED, "FSTK file larger than its header declares");
+  if (version == 2 && dtype == FSTG_F64) throw InvalidArgument("load: an FSTK v2 file holds a float32 sketch");
+  dtype_size(dtype);
+  if (k > 14) throw NotSupported("load: k > 14 exceeds this GPU build");
+  require_device(device);
+  keep_pool_warm(device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+  auto* sk = new fstg_sketch();
+  try {
+    sk->device = device;
+    sk->dtype = dtype;
+    sk->design = Design::make(static_cast<int>(k));
+    sk->m = static_cast<int64_t>(m);
+    sk->n = static_cast<int64_t>(n);
+    sk->has_a = flag != 0;
+    const size_t es = dtype_size(dtype);
+    const int64_t VEC = int64_t(16 / es);
+    sk->ldc = round_up(sk->m, VEC);
+    sk->lda = round_up(sk->n, VEC);
+    const uint64_t dev_col_bytes = uint64_t(L) * uint64_t(sk->ldc) * es;
+    if (cudaMalloc(&sk->cols, dev_col_bytes) != cudaSuccess) {
+      cudaGetLastError();
+      sk->cols = nullptr;
+      throw std::runtime_error("load: cannot allocate sketch of " + std::to_string(dev_col_bytes) + " bytes");
+    }
+    sk->device_bytes += dev_col_bytes;
+    if (sk->ldc != sk->m) cuda_check(cudaMemsetAsync(sk->cols, 0, dev_col_bytes, st), "memset sketch");
+    const size_t a_bytes = size_t(sk->m) * sk->lda * es;
+    cuda_check(cudaMalloc(&sk->a, a_bytes), "allocate embedded A");
+    sk->device_bytes += a_bytes;
+    cuda_check(cudaMemsetAsync(sk->a, 0, a_bytes, st), "memset A");
+
+    PinnedBuf buf(kChunkBytes);
+    DevBuf staging(es_file != es ? kChunkBytes : 0, st);
+    read_device_matrix(file.f, sk->cols, static_cast<int64_t>(L), sk->m, sk->ldc, es_file, es, buf, staging.p, st, p);
+    if (flag) read_device_matrix(file.f, sk->a, sk->m, sk->n, sk->lda, es_file, es, buf, staging.p, st, p);
+
+    // design tables (the Sketch constructor rebuilds the Kerdock set, sketch.hpp:130)
+    const Design& D = sk->design;
+    const std::vector<uint32_t> rev = reversed_row_table(D);
+    const int64_t nk = D.kerdock_bases();
+    const int64_t wpb = D.d >= 32 ? D.d / 32 : 1;
+    const int64_t twords = (D.d >= 128) ? (D.d >= 1024 ? D.d / 1024 : 1) * 32 : 0;
+    cuda_check(cudaMalloc(&sk->revtab, rev.size() * sizeof(uint32_t)), "allocate tables");
+    cuda_check(cudaMalloc(&sk->qplain, size_t(nk) * wpb * sizeof(uint32_t)), "allocate tables");
+    if (twords) cuda_check(cudaMalloc(&sk->qtrans, size_t(nk) * twords * sizeof(uint32_t)), "allocate tables");
+    cuda_check(cudaMemcpyAsync(sk->revtab, rev.data(), rev.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st),
+               "upload tables");
+    cuda_check(launch_qtables(sk->revtab, D.k, nk, sk->qplain, sk->qtrans, st), "qtable kernel");
+    // row_norm_max (sketch.hpp:126-131; 0 without an embedded matrix)
+    double rn = 0;
+    if (flag) {
+      DevBuf norms(size_t(sk->m) * sizeof(double), st);
+      if (dtype == FSTG_F32)
+        cuda_check(launch_row_norms<float>(static_cast<const float*>(sk->a), sk->lda, sk->m, sk->n, norms.as<double>(), st),
+                   "row norms");
+      else
+        cuda_check(launch_row_norms<double>(static_cast<const double*>(sk->a), sk->lda, sk->m, sk->n, norms.as<double>(), st),
+                   "row norms");
+      std::vector<double> hn(static_cast<size_t>(sk->m));
+      cuda_check(cudaMemcpyAsync(hn.data(), norms.p, hn.size() * sizeof(double), cudaMemcpyDeviceToHost, st), "norms");
+      cuda_check(cudaStreamSynchronize(st), "sync");
+      for (double v : hn) rn = std::max(rn, v);
+    }
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    sk->row_norm_max = rn;
+  } catch (...) {
+    destroy_sketch(sk);
+    throw;
+  }
+  *out = sk;
+}
+
 int preprocess_impl(const void* a, int dtype, int64_t m, int64_t n, int device, void* stream, int64_t b0, int64_t b1,
                     bool full, int include_identity, fstg_sketch** out) {
   return guarded([&] {
@@ -420,6 +651,7 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   const Design& D = sk->design;
   const int64_t N = p->J * p->K;
   if (N > (int64_t(1) << 40)) throw NotSupported("transform: J*K too large for this build");
+  if (!sk->has_a) throw CodedError(FSTG_ERR_NO_MATRIX, "Sketch: no embedded matrix");
   const int64_t want = candidate_count(p->s, p->widen, sk->m);
   const bool strict = p->mode == FSTG_MODE_STRICT || (p->mode == FSTG_MODE_DEFAULT && sk->dtype == FSTG_F64);
   if (p->mode < 0 || p->mode > 2) throw InvalidArgument("StreamParams: unknown mode");
@@ -751,6 +983,14 @@ int fstg_sketch_preprocess_ms(const fstg_sketch* sk, double* ms) {
 }
 
 void fstg_destroy(fstg_sketch* sk) { destroy_sketch(sk); }
+
+int fstg_save(const fstg_sketch* sk, const char* path, int version) {
+  return guarded([&] { save_impl(sk, path, version); });
+}
+
+int fstg_load(const char* path, int dtype, int device, void* stream, fstg_sketch** out) {
+  return guarded([&] { load_impl(path, dtype, device, stream, out); });
+}
 
 int fstg_draw_samples(const fstg_sketch* sk, const fstg_stream_params* p, const uint64_t* seeds, int64_t B,
                       int64_t* indices, void* stream) {

@@ -38,7 +38,33 @@ class NotSupportedError(RuntimeError):
     """Shape outside this build's GPU limits."""
 
 
-_ERRORS = {1: ValueError, 2: IndexError, 3: OverflowError, 4: MemoryError, 5: CudaError, 6: NotSupportedError}
+class IoError(OSError):
+    """io.hpp:23 IoError."""
+
+
+class MagicMismatchError(IoError):
+    """io.hpp:26"""
+
+
+class VersionUnsupportedError(IoError):
+    """io.hpp:29"""
+
+
+class TruncatedPayloadError(IoError):
+    """io.hpp:32"""
+
+
+class MalformedHeaderError(IoError):
+    """io.hpp:35"""
+
+
+class NoMatrixError(RuntimeError):
+    """sketch.hpp:109 logic_error: the sketch has no embedded matrix."""
+
+
+_ERRORS = {1: ValueError, 2: IndexError, 3: OverflowError, 4: MemoryError, 5: CudaError, 6: NotSupportedError,
+           7: IoError, 8: MagicMismatchError, 9: VersionUnsupportedError, 10: TruncatedPayloadError,
+           11: MalformedHeaderError, 12: NoMatrixError}
 
 
 class _Params(C.Structure):
@@ -64,7 +90,7 @@ EXPORTED = [
     "fstg_sketch_column", "fstg_sketch_gather", "fstg_sketch_device_columns", "fstg_sketch_preprocess_ms", "fstg_destroy",
     "fstg_draw_samples", "fstg_transform_batch", "fstg_transform_with_samples_batch", "fstg_profile_enable",
     "fstg_profile_reset", "fstg_profile_read", "fstg_launch_count", "fstg_gen_gaussian",
-    "fstg_gen_sparse_targets",
+    "fstg_gen_sparse_targets", "fstg_save", "fstg_load",
 ]
 
 
@@ -309,6 +335,26 @@ def preprocess_shard(a, basis_begin: int, basis_end: int, include_identity: bool
     _check(lib().fstg_preprocess_shard(_ptr(a), C.c_int(_dtype_code(a.dtype)), C.c_int64(m), C.c_int64(n),
                                        C.c_int(device), C.c_void_p(stream), C.c_int64(basis_begin),
                                        C.c_int64(basis_end), C.c_int(1 if include_identity else 0), C.byref(h)))
+    return Sketch(h.value)
+
+
+def save(sk: Sketch, path, version: int = 1) -> None:
+    """sketch.hpp:215-232: FSTK v1 (float64, the reference's format) or v2 (float32)."""
+    _check(lib().fstg_save(sk.handle, str(path).encode(), C.c_int(version)))
+
+
+def load(path, dtype=None, device: int = 0, stream: Optional[int] = None) -> Sketch:
+    """sketch.hpp:241-302 straight into HBM. dtype None: keep the file's precision."""
+    if dtype is None:
+        try:
+            with open(path, "rb") as f:
+                head = f.read(8)
+        except OSError:
+            head = b""  # the library reports the IoError
+        dtype = np.float32 if len(head) == 8 and head[:4] == b"FSTK" and head[4] == 2 else np.float64
+    h = C.c_void_p()
+    _check(lib().fstg_load(str(path).encode(), C.c_int(_dtype_code(np.dtype(dtype))), C.c_int(device),
+                           C.c_void_p(stream), C.byref(h)))
     return Sketch(h.value)
 
 
