@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--config", default="3", choices=["1", "2", "3", "5"],
+                    help="BASELINE.json configs: 3 = headline (default); 1, 2 = parity-case workloads; "
+                         "5 = s x eps sweep with the dense-GEMM crossover")
     ap.add_argument("--replicate", default="recompute", choices=["recompute", "allgather"],
                     help="sketch replica per GPU: local recompute after the A broadcast, or basis-sharded "
                          "preprocessing + NVLink all-gather")
@@ -157,6 +160,29 @@ def cpu_sample(a64: np.ndarray, X64: np.ndarray, seeds: np.ndarray, J: int, K: i
 
 
 # ------------------------------------------------------------ GPU arm ----
+WORKLOADS = {
+    "3": dict(n=4096, dtype="fp32", s=32, eps=0.1, B=65536, a="haar", a_seed=4096,
+              desc="config3: n=m=4096, s=32, eps=0.1, J=375, K=2, widen=10 (N=750, want=320)",
+              data="synthetic (seeded config-3 generator: Haar-orthogonal A, y 32-sparse +-1/sqrt(32) + N(0,1e-6), "
+                   "x = A^T y / |.|)"),
+    "1": dict(n=256, dtype="fp64", s=8, eps=0.1, B=64, a="haar", a_seed=777,
+              desc="config1: n=m=256 fp64, s=8, eps=0.1, 64 vectors/step, J=375, K=2, widen=10",
+              data="synthetic (Haar-orthogonal A, y 8-sparse +-1/sqrt(8), x = A^T y)"),
+    "2": dict(n=1024, dtype="fp32", s=16, eps=0.05, B=4096, a="iid", a_seed=1024,
+              desc="config2: n=m=1024 fp32, A iid N(0,1/n), s=16, eps=0.05, 4096 vectors/step, J=375, K=2",
+              data="synthetic (A iid N(0,1/n), y 16-sparse N(0,1), x = A^-1 y / |.|)"),
+}
+
+
+def make_problem(cfg, A64, B, first, dev):
+    from paper_2105_05879_b200 import generators
+    if cfg is WORKLOADS["1"]:
+        return generators.config1_problem(B=B, seed=X_SEED, device=dev, a_seed=cfg["a_seed"])
+    if cfg is WORKLOADS["2"]:
+        return generators.config2_problem(B=B, seed=X_SEED, device=dev, a_seed=cfg["a_seed"], first=first)
+    return generators.config3_problem(B=B, seed=X_SEED, device=dev, first=first, A64=A64)
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -170,21 +196,25 @@ def run_b200(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(dev))
 
+    cfg = WORKLOADS[args.config]
+    n_dim = cfg["n"]
+    es = 8 if cfg["dtype"] == "fp64" else 4
     # ---- A: built on rank 0, broadcast over NCCL ----
     if rank == 0:
-        A64 = generators.haar_orthogonal(N_DIM, A_SEED, dev)
+        A64 = (generators.haar_orthogonal(n_dim, cfg["a_seed"], dev) if cfg["a"] == "haar"
+               else generators.iid_gaussian(n_dim, cfg["a_seed"], dev))
     else:
-        A64 = torch.empty((N_DIM, N_DIM), dtype=torch.float64, device=dev)
+        A64 = torch.empty((n_dim, n_dim), dtype=torch.float64, device=dev)
     if world > 1:
         parallel.broadcast_matrix(A64, src=0)
-    A32 = A64.float().contiguous()
+    A32 = A64.contiguous() if es == 8 else A64.float().contiguous()
 
     # ---- sketch replica per GPU (device time) ----
     fst.profile_enable(True)
     fst.profile_reset()
     gather_ms = 0.0
     if args.replicate == "allgather" and world > 1:
-        nk = fst.design_params(fst.even_log2_ceil(N_DIM))[0] // 2
+        nk = fst.design_params(fst.even_log2_ceil(n_dim))[0] // 2
         first, count = parallel.basis_shards(nk, world)[rank]
         sk = fst.preprocess_shard(A32, first, first + count, True, device=local)
         full = parallel.sketch_tensor(sk)
@@ -200,20 +230,22 @@ def run_b200(args):
     fwht_ms, _ = fst.profile_read("preprocess_fwht")
     ident_ms, _ = fst.profile_read("preprocess_identity")
     pre_ms = parallel.max_over_ranks(sk.preprocess_ms + gather_ms, device=dev)
-    sketch_bytes = sk.L * sk.m * 4
+    sketch_bytes = sk.L * sk.m * es
 
     # ---- this rank's shard of the vector stream ----
-    B = args.batch
+    B = args.batch if args.config == "3" else cfg["B"]
     first, _ = parallel.vector_shard(rank, world, B)
-    prob = generators.config3_problem(B=B, seed=X_SEED, device=dev, first=first, A64=A64)
+    prob = make_problem(cfg, A64, B, first, dev)
     X = prob.X
     seeds_dev = torch.from_numpy(prob.seeds.view(np.int64)).to(dev)
-    p = fst.StreamParams(epsilon=EPS, s=S, J=args.J, K=args.K, widen=WIDEN)
+    s_val, eps_val = cfg["s"], cfg["eps"]
+    p = fst.StreamParams(epsilon=eps_val, s=s_val, J=args.J, K=args.K, widen=WIDEN)
     N = args.J * args.K
-    want = fst.candidate_count(S, WIDEN, N_DIM)
+    want = fst.candidate_count(s_val, WIDEN, n_dim)
+    vdt = torch.float64 if es == 8 else torch.float32
     out = fst.BatchResult(torch.zeros(B, dtype=torch.int32, device=dev),
                           torch.zeros((B, want), dtype=torch.int32, device=dev),
-                          torch.zeros((B, want), dtype=torch.float32, device=dev))
+                          torch.zeros((B, want), dtype=vdt, device=dev))
     stream = torch.cuda.current_stream()
     sptr = stream.cuda_stream
 
@@ -249,7 +281,7 @@ def run_b200(args):
 
     # ---- roofline of the dominant kernel (the fused stream kernel) ----
     peak, peak_kind = peaks()
-    bvec = bytes_per_vector(N, sk.m, sk.n, want)
+    bvec = bytes_per_vector(N, sk.m, sk.n, want, es)
     per_launch_ms = stream_ms / max(1, stream_launches)
     vec_per_launch = B * args.steps / max(1, stream_launches)
     achieved = bvec * vec_per_launch / (per_launch_ms / 1e3) / 1e9
@@ -262,7 +294,7 @@ def run_b200(args):
         seeds_h = torch.from_numpy(prob.seeds.view(np.int64).copy()).pin_memory()
         oh = fst.BatchResult(torch.zeros(B, dtype=torch.int32).pin_memory(),
                              torch.zeros((B, want), dtype=torch.int32).pin_memory(),
-                             torch.zeros((B, want), dtype=torch.float32).pin_memory())
+                             torch.zeros((B, want), dtype=vdt).pin_memory())
         for _ in range(max(1, args.warmup)):
             fst.transform_batch(sk, Xh, p, seeds_h, out=oh, stream=sptr)
         if world > 1:
@@ -274,13 +306,13 @@ def run_b200(args):
         torch.cuda.synchronize()
         e2e_s = time.perf_counter() - t0
         e2e = {"value": world * B * args.steps / parallel.max_over_ranks(e2e_s, device=dev), "unit": "vectors/s",
-               "h2d_bytes_per_step": int(B * N_DIM * 4 + B * 8),
-               "d2h_bytes_per_step": int(B * 4 + B * want * 8)}
+               "h2d_bytes_per_step": int(B * n_dim * es + B * 8),
+               "d2h_bytes_per_step": int(B * 4 + B * want * (4 + es))}
         assert np.array_equal(oh.counts.numpy(), counts), "host-buffer path disagrees with device path"
 
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and args.config == "3":
         P = 32
         a64 = A64.cpu().numpy()
         X64 = X[:P].double().cpu().numpy()
@@ -293,7 +325,7 @@ def run_b200(args):
                           f"exceeds host RAM")}
 
     line = {
-        "metric": METRIC,
+        "metric": METRIC if args.config == "3" else f"thresholded-Ax vectors/sec ({cfg['desc'].split(':')[0]})",
         "value": value,
         "unit": "vectors/s",
         "n_gpus": world,
@@ -303,13 +335,13 @@ def run_b200(args):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "fp32",
-        "data": "synthetic (seeded config-3 generator: Haar-orthogonal A, y 32-sparse +-1/sqrt(32) + N(0,1e-6), "
-                "x = A^T y / |.|)",
-        "config": {"workload": "config3: n=m=4096, s=32, eps=0.1, J=375, K=2, widen=10 (N=750, want=320)",
+        "dtype": cfg["dtype"],
+        "data": cfg["data"],
+        "config": {"workload": cfg["desc"],
                    "vectors_per_gpu_per_step": B, "J": args.J, "K": args.K, "widen": WIDEN,
                    "parallelism": f"vector-sharded x{world}, sketch replicated per GPU",
-                   "l2": "inputs larger than L2 (137.5 GB sketch; 1 GiB of x per step)",
+                   "l2": ("inputs larger than L2 (137.5 GB sketch; 1 GiB of x per step)" if args.config == "3"
+                          else "small config: sketch may be L2-resident"),
                    "mean_support": float(np.mean(counts))},
         "preprocess": {"ms": pre_ms, "fwht_ms": fwht_ms, "identity_ms": ident_ms, "allgather_ms": gather_ms,
                        "replicate": args.replicate,
@@ -332,6 +364,81 @@ def run_b200(args):
     sk.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+# ------------------------------------------------- config 5: sweep + GEMM ----
+def run_sweep(args):
+    """Config 5: s in {4,16,64,256} x eps in {0.2,0.1,0.05} at n = 4096 on one GPU; the stream path
+    against dense h_eps(A x) by one cuBLAS GEMM per batch (fp32 SGEMM and TF32) on the same batch."""
+    import torch
+    from paper_2105_05879_b200 import fst, generators
+    dev = "cuda:0"
+    torch.cuda.set_device(0)
+    A64 = generators.haar_orthogonal(N_DIM, A_SEED, dev)
+    A32 = A64.float().contiguous()
+    sk = fst.preprocess(A32)
+    B = 131072 // 2 if args.batch == 65536 else args.batch  # 1,048,576 / 8 GPUs would be 131,072 per GPU
+    stream = torch.cuda.current_stream()
+    peak, _ = peaks()
+
+    def timed(fn, reps):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    rows = []
+    for s_val in (4, 16, 64, 256):
+        prob = generators.config5_problem(s_val, 0.1, B, seed=X_SEED, device=dev, A64=A64)
+        X = prob.X
+        seeds_dev = torch.from_numpy(prob.seeds.view(np.int64)).to(dev)
+        for eps_val in (0.2, 0.1, 0.05):
+            p = fst.StreamParams(epsilon=eps_val, s=s_val, J=args.J, K=args.K, widen=WIDEN)
+            want = fst.candidate_count(s_val, WIDEN, N_DIM)
+            out = fst.transform_batch(sk, X, p, seeds_dev, stream=stream.cuda_stream)
+            fst.profile_enable(True)
+            fst.profile_reset()
+            ms_stream = timed(lambda: fst.transform_batch(sk, X, p, seeds_dev, out=out, stream=stream.cuda_stream),
+                              max(1, args.steps // 2))
+            k_ms, k_n = fst.profile_read("stream")
+            fst.profile_enable(False)
+            torch.backends.cuda.matmul.allow_tf32 = False
+            dense = lambda: torch.where((ax := X @ A32.T).abs() >= eps_val, ax, 0.0)  # noqa: E731
+            ms_sgemm = timed(dense, 3)
+            torch.backends.cuda.matmul.allow_tf32 = True
+            ms_tf32 = timed(dense, 3)
+            torch.backends.cuda.matmul.allow_tf32 = False
+            # support agreement of the stream with the exact dense threshold (fp64 reference)
+            sub = min(B, 4096)
+            ax = X[:sub].double() @ A64.T
+            dense_sup = ax.abs() >= eps_val
+            counts = out.counts[:sub].long()
+            stream_sup = torch.zeros_like(dense_sup)
+            valid = torch.arange(want, device=dev).unsqueeze(0) < counts.unsqueeze(1)
+            r_idx = torch.arange(sub, device=dev).unsqueeze(1).expand(-1, want)
+            stream_sup[r_idx[valid], out.support[:sub].long()[valid]] = True
+            match = float((stream_sup == dense_sup).all(dim=1).float().mean())
+            bvec = bytes_per_vector(args.J * args.K, N_DIM, N_DIM, want)
+            per_launch = k_ms / max(1, k_n)
+            rows.append({"s": s_val, "eps": eps_val, "want": want,
+                         "stream_vectors_per_s": B / (ms_stream / 1e3),
+                         "stream_roofline_frac": bvec * B / (per_launch / 1e3) / 1e9 / peak,
+                         "dense_sgemm_vectors_per_s": B / (ms_sgemm / 1e3),
+                         "dense_tf32_vectors_per_s": B / (ms_tf32 / 1e3),
+                         "support_match_vs_exact": match,
+                         "mean_true_support": float(dense_sup.sum(dim=1).float().mean()),
+                         "mean_stream_support": float(counts.float().mean())})
+    line = {"metric": "config5 sweep: thresholded-Ax vectors/sec vs dense GEMM (1 B200)", "n_gpus": 1,
+            "config": {"workload": f"config5: n=4096 fp32 Haar A, x = A^T y (s-sparse +-1/sqrt(s)), {B} vectors "
+                                   f"per batch, J={args.J}, K={args.K}, widen=10"},
+            "sweep": rows}
+    print(json.dumps(line), flush=True)
+    sk.close()
 
 
 # ------------------------------------------------------- reference arm ----
@@ -385,6 +492,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "5":
+        run_sweep(args)
     else:
         run_b200(args)
 

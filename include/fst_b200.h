@@ -187,6 +187,9 @@ int fstg_gen_gaussian(uint64_t seed, int64_t count, double* out);
 int fstg_gen_sparse_targets(const uint64_t* seeds, int64_t B, int64_t m, int64_t s, int value_kind,
                             double noise_sigma, double* Y);
 
+/* gen_mixture's target draw (generators.hpp:60-78), unnormalised. */
+int fstg_gen_mixture_targets(const uint64_t* seeds, int64_t B, int64_t m, double p, double* Y);
+
 /* ------------------------------------------------------------ profiling ---- */
 /* When enabled, the library brackets each launch of its kernels with CUDA
  * events on the launching stream; fstg_profile_read returns the accumulated

@@ -452,6 +452,17 @@ def gen_orthogonal(n: int, seed: int) -> np.ndarray:
     return out
 
 
+def gen_mixture(a: np.ndarray, p: float, seed: int):
+    """generators.hpp:60-85 -> (x, truth), both rescaled by |A^T y|."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    m, n = a.shape
+    x = np.zeros(n)
+    truth = np.zeros(m)
+    _check(lib().orc_gen_mixture(_ptr(a), C.c_int64(m), C.c_int64(n), C.c_double(p), C.c_uint64(seed), _ptr(x),
+                                 _ptr(truth)))
+    return x, truth
+
+
 def gen_exact_sparse(a: np.ndarray, s: int, seed: int):
     a = np.ascontiguousarray(a, dtype=np.float64)
     m, n = a.shape

@@ -463,6 +463,38 @@ int orc_load(const char* path, void** out) {
   return 0;
 }
 
+// generators.hpp:60-85 gen_mixture: returns x (n) and truth (m), both / |x|.
+int orc_gen_mixture(const double* a, std::int64_t m, std::int64_t n, double p, std::uint64_t seed, double* x_out,
+                    double* truth_out) {
+  return guarded([&] {
+    if (!(p > 0) || p > 1) throw std::invalid_argument("gen_mixture: need 0 < p <= 1");
+    std::vector<double> truth(static_cast<std::size_t>(m));
+    for (std::uint64_t attempt = 0;; ++attempt) {
+      SeededRng rng(mix_seed(seed) ^ (attempt * 0x9e3779b97f4a7c15ull));
+      bool any = false;
+      for (std::int64_t i = 0; i < m; ++i) {
+        if (rng.unit_double() <= p) {
+          truth[i] = rng.gaussian();
+          any = true;
+        } else {
+          truth[i] = 0.0;
+        }
+      }
+      if (any) break;
+    }
+    double nrm = 0;
+    for (std::int64_t j = 0; j < n; ++j) {
+      double acc = 0;
+      for (std::int64_t i = 0; i < m; ++i) acc += a[i * n + j] * truth[i];
+      x_out[j] = acc;
+      nrm += acc * acc;
+    }
+    nrm = std::sqrt(nrm);
+    for (std::int64_t j = 0; j < n; ++j) x_out[j] /= nrm;
+    for (std::int64_t i = 0; i < m; ++i) truth_out[i] = truth[i] / nrm;
+  });
+}
+
 // ---- generators ----
 int orc_gen_orthogonal(std::int64_t n, std::uint64_t seed, double* out) {
   return guarded([&] {

@@ -102,4 +102,38 @@ int fstg_gen_sparse_targets(const uint64_t* seeds, int64_t B, int64_t m, int64_t
   return FSTG_OK;
 }
 
+// gen_mixture's target draw (generators.hpp:60-78): entries are N(0,1) with
+// probability p (unit_double() <= p, then gaussian()), else 0; an all-zero draw
+// retries on SeededRng(mix_seed(seed) ^ attempt * 0x9e3779b97f4a7c15). The
+// caller forms x = A^T y and rescales both by |x| (generators.hpp:80-83).
+int fstg_gen_mixture_targets(const uint64_t* seeds, int64_t B, int64_t m, double p, double* Y) {
+  if (B < 0 || m < 1 || !(p > 0) || p > 1 || (B > 0 && (seeds == nullptr || Y == nullptr)))
+    return FSTG_ERR_INVALID_ARGUMENT;
+  auto mix = [](uint64_t z) {
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+  };
+  parallel_for(B, [&](int64_t first, int64_t last) {
+    for (int64_t v = first; v < last; ++v) {
+      double* y = Y + v * m;
+      for (uint64_t attempt = 0;; ++attempt) {
+        Rng r(mix(seeds[v]) ^ (attempt * 0x9e3779b97f4a7c15ull));
+        bool any = false;
+        for (int64_t i = 0; i < m; ++i) {
+          if (r.unit_double() <= p) {
+            y[i] = r.gaussian();
+            any = true;
+          } else {
+            y[i] = 0.0;
+          }
+        }
+        if (any) break;
+      }
+    }
+  });
+  return FSTG_OK;
+}
+
 }  // extern "C"

@@ -90,7 +90,7 @@ EXPORTED = [
     "fstg_sketch_column", "fstg_sketch_gather", "fstg_sketch_device_columns", "fstg_sketch_preprocess_ms", "fstg_destroy",
     "fstg_draw_samples", "fstg_transform_batch", "fstg_transform_with_samples_batch", "fstg_profile_enable",
     "fstg_profile_reset", "fstg_profile_read", "fstg_launch_count", "fstg_gen_gaussian",
-    "fstg_gen_sparse_targets", "fstg_save", "fstg_load",
+    "fstg_gen_sparse_targets", "fstg_save", "fstg_load", "fstg_gen_mixture_targets",
 ]
 
 
