@@ -695,11 +695,12 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   args.nseg = static_cast<int>((sk->ldc + SEG - 1) / SEG);
   if (args.nseg > 4) throw NotSupported("transform: m too large for this GPU build (m <= 4 * 16 KiB / sizeof(T))");
   size_t smem = 0;
-  int stages = 0, stage_stride = 0;
-  const int grid_max = stream_grid_size<T>(args, strict, chunk, &smem, &stages, &stage_stride);
+  int stages = 0, stage_stride = 0, rstride = 0;
+  const int grid_max = stream_grid_size<T>(args, strict, chunk, &smem, &stages, &stage_stride, &rstride);
   if (smem > 227 * 1024) throw NotSupported("transform: shared-memory plan exceeds 227 KiB (d or want too large)");
   args.stages = stages;
   args.stage_stride = stage_stride;
+  args.rstride = rstride;
   {
     const char* dbg = std::getenv("FSTG_STREAM_DEBUG");
     args.debug = dbg ? std::atoi(dbg) : 0;

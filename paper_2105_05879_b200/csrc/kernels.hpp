@@ -60,6 +60,7 @@ struct StreamArgs {
   // pipeline
   int stages;
   int stage_stride;  // bytes between ring stages (>= one segment, 128-byte multiple)
+  int rstride;       // bytes per refinement-ring stage (one row of A); 0 = direct loads
   int nseg;
   int chunk;
   // experiment switches (env FSTG_STREAM_DEBUG; 0 in production):
@@ -76,6 +77,6 @@ int64_t stream_scratch_elems(const StreamArgs<T>& args, int grid);
 // Persistent grid size the stream kernel wants for this configuration.
 template <typename T>
 int stream_grid_size(const StreamArgs<T>& args, bool strict, int64_t B, size_t* smem_bytes, int* stages,
-                     int* stage_stride);
+                     int* stage_stride, int* rstride);
 
 }  // namespace fstg

@@ -46,6 +46,7 @@ constexpr int kXBuf = 3;                    // x buffers: coefficients on v+2 wh
 constexpr int kSmemBudget = 227 * 1024;
 constexpr int kInflightBytes = 5 * 16384;    // column bytes in flight per SM
 constexpr int kBarCoef = 2, kBarTail = 3;   // named barrier ids
+constexpr int kRStages = kTLW - 1;          // refinement ring: tail warp 0 issues, warps 1..6 consume
 
 template <typename T>
 struct KeyOf;
@@ -86,11 +87,12 @@ struct Vec<double> {
 };
 
 struct SmemLayout {
-  size_t ring, x, tbuf, bars, hist, scan, misc, cand, cval, cflag, total;
+  size_t ring, x, tbuf, bars, hist, scan, misc, cand, cval, cflag, rring, total;
 };
 
 template <typename T>
-__host__ __device__ inline SmemLayout smem_layout(int64_t d, int stages, int stage_stride, int64_t want) {
+__host__ __device__ inline SmemLayout smem_layout(int64_t d, int stages, int stage_stride, int64_t want,
+                                                  int rstride) {
   SmemLayout L{};
   size_t off = 0;
   auto take = [&off](size_t bytes, size_t align) {
@@ -102,13 +104,14 @@ __host__ __device__ inline SmemLayout smem_layout(int64_t d, int stages, int sta
   L.ring = take(size_t(stages) * stage_stride, 1024);
   L.x = take(kXBuf * size_t(d < 4 ? 4 : d) * sizeof(T), 16);
   L.tbuf = take(kTRing * sizeof(T), 16);
-  L.bars = take((2 * kMaxStages + 2 * kTRing + 2 * kXBuf + 4) * sizeof(uint64_t), 8);
+  L.bars = take((2 * kMaxStages + 2 * kTRing + 2 * kXBuf + 4 + 2 * kRStages) * sizeof(uint64_t), 8);
   L.hist = take(256 * sizeof(uint32_t), 16);
   L.scan = take(2 * 32 * sizeof(uint32_t), 16);
   L.misc = take(16 * sizeof(unsigned long long), 16);
   L.cand = take(size_t(want) * sizeof(int32_t), 16);
   L.cval = take(size_t(want) * sizeof(T), 16);
   L.cflag = take(size_t(want) * sizeof(uint8_t), 16);
+  L.rring = take(size_t(kRStages) * rstride, 128);  // rstride 0: refinement reads A directly
   L.total = (off + 15) / 16 * 16;
   return L;
 }
@@ -340,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
   constexpr int CPT = CPS / kNC;                                  // chunks per consumer thread per segment
 
   extern __shared__ __align__(1024) unsigned char smem[];
-  const SmemLayout Ls = smem_layout<T>(A.d, A.stages, A.stage_stride, A.want);
+  const SmemLayout Ls = smem_layout<T>(A.d, A.stages, A.stage_stride, A.want, A.rstride);
   unsigned char* ring = smem + Ls.ring;
   T* xbuf = reinterpret_cast<T*>(smem + Ls.x);
   T* tring = reinterpret_cast<T*>(smem + Ls.tbuf);
@@ -352,6 +355,9 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
   uint64_t* x_empty = x_full + kXBuf;
   uint64_t* m_full = x_empty + kXBuf;
   uint64_t* m_empty = m_full + 2;
+  uint64_t* r_full = m_empty + 2;
+  uint64_t* r_empty = r_full + kRStages;
+  unsigned char* rring = smem + Ls.rring;
   uint32_t* hist = reinterpret_cast<uint32_t*>(smem + Ls.hist);
   uint32_t* scan = reinterpret_cast<uint32_t*>(smem + Ls.scan);
   unsigned long long* misc = reinterpret_cast<unsigned long long*>(smem + Ls.misc);
@@ -384,6 +390,10 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
   if (tid < 2) {
     mbar_init(&m_full[tid], kNCW);
     mbar_init(&m_empty[tid], 1);
+  }
+  if (tid < kRStages) {
+    mbar_init(&r_full[tid], 1);
+    mbar_init(&r_empty[tid], 1);
   }
   if (tid < 32) {
     // Walsh base masks: bit f (i' = f/4, e = f%4) = parity(hi3 & i') ^ parity(lo2 & e).
@@ -509,6 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     const int ttid = tid - kWarpTail * 32, tw = warp - kWarpTail;
     const uint64_t pol_keep = policy_evict_last();
     int parity = 0;
+    uint32_t rg = 0;  // running index of refinement rows through the ring (all tail threads agree)
     uint32_t lv = 0;
     for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
       const uint32_t slot = lv & 1u, su = lv >> 1, xb = lv % kXBuf, xu = lv / kXBuf;
@@ -650,59 +661,124 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
       // ---- refinement: v_i = a_i . x, fp64 accumulation (stream.hpp:259-266) ----
       mbar_wait(&x_full[xb], xu & 1u);
       const T* xs = xbuf + xb * dx;
-      for (int64_t ci = tw; ci < A.want; ci += kTLW) {
-        const int64_t row = cand[ci];
-        const T* arow = A.a + row * A.lda;
-        double dot = 0.0, dot2 = 0.0;
-        if constexpr (sizeof(T) == 4) {
-          constexpr int kRB = 4;  // independent 16-byte loads in flight per lane
-          const int64_t nv = (A.n + 3) / 4;
-          const float4* a4 = reinterpret_cast<const float4*>(arow);
-          const float4* x4 = reinterpret_cast<const float4*>(xs);
-          for (int64_t q0 = lane; q0 < nv; q0 += 32 * kRB) {
-            float4 av[kRB];
-#pragma unroll
-            for (int u = 0; u < kRB; ++u)
-              av[u] = (q0 + 32 * u < nv) ? ldg_f4_policy(a4 + q0 + 32 * u, pol_keep) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int u = 0; u < kRB; ++u) {
-              if (q0 + 32 * u < nv) {
-                const float4 xv4 = x4[q0 + 32 * u];
-                double& acc = (u & 1) ? dot2 : dot;
-                acc = fma(static_cast<double>(av[u].x), static_cast<double>(xv4.x), acc);
-                acc = fma(static_cast<double>(av[u].y), static_cast<double>(xv4.y), acc);
-                acc = fma(static_cast<double>(av[u].z), static_cast<double>(xv4.z), acc);
-                acc = fma(static_cast<double>(av[u].w), static_cast<double>(xv4.w), acc);
-              }
+      if (A.rstride > 0) {
+        // Gather-GEMV staged through TMA: tail warp 0 bulk-copies the candidate
+        // rows of A (L2-resident, evict-last) into a kRStages-deep ring; warp
+        // 1 + st owns stage st and takes the rows whose running index g
+        // satisfies g % kRStages == st, so each stage's uses stay in order on
+        // one warp (mbarrier parity never aliases).
+        const uint32_t rbytes = static_cast<uint32_t>(A.lda * sizeof(T));
+        if (tw == 0) {
+          if (lane == 0) {
+            for (int64_t ci = 0; ci < A.want; ++ci) {
+              const uint32_t g = rg + static_cast<uint32_t>(ci);
+              const uint32_t st = g % kRStages, u = g / kRStages;
+              if (u > 0) mbar_wait(&r_empty[st], (u - 1) & 1u);
+              mbar_arrive_expect_tx(&r_full[st], rbytes);
+              bulk_g2s(rring + size_t(st) * A.rstride, A.a + int64_t(cand[ci]) * A.lda, rbytes, &r_full[st], pol_keep);
             }
           }
+          __syncwarp();
         } else {
-          constexpr int kRB = 8;
-          const int64_t nv = (A.n + 1) / 2;
-          const double2* a2 = reinterpret_cast<const double2*>(arow);
-          const double2* x2 = reinterpret_cast<const double2*>(xs);
-          for (int64_t q0 = lane; q0 < nv; q0 += 32 * kRB) {
-            double2 av[kRB];
-#pragma unroll
-            for (int u = 0; u < kRB; ++u)
-              av[u] = (q0 + 32 * u < nv) ? ldg_d2_policy(a2 + q0 + 32 * u, pol_keep) : make_double2(0.0, 0.0);
-#pragma unroll
-            for (int u = 0; u < kRB; ++u) {
-              if (q0 + 32 * u < nv) {
-                const double2 xv2 = x2[q0 + 32 * u];
-                double& acc = (u & 1) ? dot2 : dot;
-                acc = fma(av[u].x, xv2.x, acc);
-                acc = fma(av[u].y, xv2.y, acc);
+          const uint32_t st = static_cast<uint32_t>(tw - 1);
+          const uint32_t first = (st + kRStages - rg % kRStages) % kRStages;  // first ci with (rg + ci) % kRS == st
+          for (int64_t ci = first; ci < A.want; ci += kRStages) {
+            const uint32_t g = rg + static_cast<uint32_t>(ci);
+            mbar_wait(&r_full[st], (g / kRStages) & 1u);
+            double dot = 0.0, dot2 = 0.0;
+            if constexpr (sizeof(T) == 4) {
+              const int64_t nv = (A.n + 3) / 4;
+              const float4* a4 = reinterpret_cast<const float4*>(rring + size_t(st) * A.rstride);
+              const float4* x4 = reinterpret_cast<const float4*>(xs);
+#pragma unroll 4
+              for (int64_t q = lane; q < nv; q += 32) {
+                const float4 av = a4[q], xv4 = x4[q];
+                double& acc = ((q >> 5) & 1) ? dot2 : dot;
+                acc = fma(static_cast<double>(av.x), static_cast<double>(xv4.x), acc);
+                acc = fma(static_cast<double>(av.y), static_cast<double>(xv4.y), acc);
+                acc = fma(static_cast<double>(av.z), static_cast<double>(xv4.z), acc);
+                acc = fma(static_cast<double>(av.w), static_cast<double>(xv4.w), acc);
               }
+            } else {
+              const int64_t nv = (A.n + 1) / 2;
+              const double2* a2 = reinterpret_cast<const double2*>(rring + size_t(st) * A.rstride);
+              const double2* x2 = reinterpret_cast<const double2*>(xs);
+#pragma unroll 4
+              for (int64_t q = lane; q < nv; q += 32) {
+                const double2 av = a2[q], xv2 = x2[q];
+                double& acc = ((q >> 5) & 1) ? dot2 : dot;
+                acc = fma(av.x, xv2.x, acc);
+                acc = fma(av.y, xv2.y, acc);
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&r_empty[st]);
+            dot += dot2;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+            if (lane == 0) {
+              cval[ci] = static_cast<T>(dot);
+              cflag[ci] = fabs(dot) >= A.epsilon ? 1 : 0;
             }
           }
         }
-        dot += dot2;
+        rg += static_cast<uint32_t>(A.want);
+      } else {
+        // rows longer than one stage: direct 16-byte loads from L2
+        for (int64_t ci = tw; ci < A.want; ci += kTLW) {
+          const int64_t row = cand[ci];
+          const T* arow = A.a + row * A.lda;
+          double dot = 0.0, dot2 = 0.0;
+          if constexpr (sizeof(T) == 4) {
+            constexpr int kRB = 4;
+            const int64_t nv = (A.n + 3) / 4;
+            const float4* a4 = reinterpret_cast<const float4*>(arow);
+            const float4* x4 = reinterpret_cast<const float4*>(xs);
+            for (int64_t q0 = lane; q0 < nv; q0 += 32 * kRB) {
+              float4 av[kRB];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
-        if (lane == 0) {
-          cval[ci] = static_cast<T>(dot);
-          cflag[ci] = fabs(dot) >= A.epsilon ? 1 : 0;
+              for (int u = 0; u < kRB; ++u)
+                av[u] = (q0 + 32 * u < nv) ? ldg_f4_policy(a4 + q0 + 32 * u, pol_keep) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+              for (int u = 0; u < kRB; ++u) {
+                if (q0 + 32 * u < nv) {
+                  const float4 xv4 = x4[q0 + 32 * u];
+                  double& acc = (u & 1) ? dot2 : dot;
+                  acc = fma(static_cast<double>(av[u].x), static_cast<double>(xv4.x), acc);
+                  acc = fma(static_cast<double>(av[u].y), static_cast<double>(xv4.y), acc);
+                  acc = fma(static_cast<double>(av[u].z), static_cast<double>(xv4.z), acc);
+                  acc = fma(static_cast<double>(av[u].w), static_cast<double>(xv4.w), acc);
+                }
+              }
+            }
+          } else {
+            constexpr int kRB = 4;
+            const int64_t nv = (A.n + 1) / 2;
+            const double2* a2 = reinterpret_cast<const double2*>(arow);
+            const double2* x2 = reinterpret_cast<const double2*>(xs);
+            for (int64_t q0 = lane; q0 < nv; q0 += 32 * kRB) {
+              double2 av[kRB];
+#pragma unroll
+              for (int u = 0; u < kRB; ++u)
+                av[u] = (q0 + 32 * u < nv) ? ldg_d2_policy(a2 + q0 + 32 * u, pol_keep) : make_double2(0.0, 0.0);
+#pragma unroll
+              for (int u = 0; u < kRB; ++u) {
+                if (q0 + 32 * u < nv) {
+                  const double2 xv2 = x2[q0 + 32 * u];
+                  double& acc = (u & 1) ? dot2 : dot;
+                  acc = fma(av[u].x, xv2.x, acc);
+                  acc = fma(av[u].y, xv2.y, acc);
+                }
+              }
+            }
+          }
+          dot += dot2;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+          if (lane == 0) {
+            cval[ci] = static_cast<T>(dot);
+            cflag[ci] = fabs(dot) >= A.epsilon ? 1 : 0;
+          }
         }
       }
       named_bar_sync(kBarTail, kTL);
@@ -823,17 +899,20 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
 // ------------------------------------------------------------- launching --
 template <typename T>
 int stream_grid_size(const StreamArgs<T>& args, bool strict, int64_t B, size_t* smem_bytes, int* stages,
-                     int* stage_stride) {
+                     int* stage_stride, int* rstride_out) {
   const int64_t stage_bytes = (args.m_pad * int64_t(sizeof(T)) < kSegBytes) ? args.m_pad * int64_t(sizeof(T)) : kSegBytes;
   const int stride = static_cast<int>((stage_bytes + 127) / 128 * 128);
-  const SmemLayout L0 = smem_layout<T>(args.d, 0, stride, args.want);
+  const int64_t row_bytes = args.lda * int64_t(sizeof(T));
+  const int rstride = row_bytes <= kSegBytes ? static_cast<int>((row_bytes + 127) / 128 * 128) : 0;
+  *rstride_out = rstride;
+  const SmemLayout L0 = smem_layout<T>(args.d, 0, stride, args.want, rstride);
   int S = static_cast<int>((kSmemBudget - static_cast<int64_t>(L0.total) - 1024) / stride);
   // ~64 KiB in flight per SM is enough (profiles/r01_stream_stages.txt: 3-5 x 16 KiB stages beat 10)
   S = std::min(S, std::max(4, static_cast<int>(kInflightBytes / stride)));
   if (const char* e = std::getenv("FSTG_STREAM_STAGES")) S = std::min(S, std::max(2, std::atoi(e)));  // experiments
   if (S > kMaxStages) S = kMaxStages;
   if (S < 2) S = 2;
-  const SmemLayout L = smem_layout<T>(args.d, S, stride, args.want);
+  const SmemLayout L = smem_layout<T>(args.d, S, stride, args.want, rstride);
   *smem_bytes = L.total;
   *stages = S;
   *stage_stride = stride;
@@ -862,7 +941,7 @@ static cudaError_t launch_one(const StreamArgs<T>& args, int grid, size_t smem, 
 
 template <typename T>
 cudaError_t launch_stream(const StreamArgs<T>& args, bool strict, int grid, cudaStream_t st) {
-  const SmemLayout L = smem_layout<T>(args.d, args.stages, args.stage_stride, args.want);
+  const SmemLayout L = smem_layout<T>(args.d, args.stages, args.stage_stride, args.want, args.rstride);
   if (L.total > static_cast<size_t>(kSmemBudget)) return cudaErrorInvalidConfiguration;
   if (args.nseg <= 1) {
     return strict ? launch_one<T, true, 1>(args, grid, L.total, st) : launch_one<T, false, 1>(args, grid, L.total, st);
@@ -875,8 +954,8 @@ cudaError_t launch_stream(const StreamArgs<T>& args, bool strict, int grid, cuda
 
 template cudaError_t launch_stream<float>(const StreamArgs<float>&, bool, int, cudaStream_t);
 template cudaError_t launch_stream<double>(const StreamArgs<double>&, bool, int, cudaStream_t);
-template int stream_grid_size<float>(const StreamArgs<float>&, bool, int64_t, size_t*, int*, int*);
-template int stream_grid_size<double>(const StreamArgs<double>&, bool, int64_t, size_t*, int*, int*);
+template int stream_grid_size<float>(const StreamArgs<float>&, bool, int64_t, size_t*, int*, int*, int*);
+template int stream_grid_size<double>(const StreamArgs<double>&, bool, int64_t, size_t*, int*, int*, int*);
 template int64_t stream_scratch_elems<float>(const StreamArgs<float>&, int);
 template int64_t stream_scratch_elems<double>(const StreamArgs<double>&, int);
 
