@@ -121,6 +121,13 @@ int fstg_preprocess(const void* a, int dtype, int64_t m, int64_t n, int device, 
  * fstg_sketch_device_columns. */
 int fstg_preprocess_shard(const void* a, int dtype, int64_t m, int64_t n, int device, void* stream,
                           int64_t basis_begin, int64_t basis_end, int include_identity, fstg_sketch** out);
+/* Design-only sketch: embedded A + Kerdock tables, NO materialised columns —
+ * for n where the m x L sketch cannot exist (n = 16384: 8.8 TB). Columns are
+ * then produced on demand by fstg_sample_columns (retain-sampled
+ * preprocessing) and consumed by
+ * fstg_transform_gathered_batch. */
+int fstg_preprocess_design(const void* a, int dtype, int64_t m, int64_t n, int device, void* stream,
+                           fstg_sketch** out);
 int fstg_sketch_info_get(const fstg_sketch* sk, fstg_sketch_info* info);
 /* Sketch::row_norm_max (sketch.hpp:105) */
 int fstg_row_norm_max(const fstg_sketch* sk, double* out);
@@ -132,6 +139,13 @@ int fstg_sketch_device_columns(const fstg_sketch* sk, void** columns);
 /* draw_and_gather (stream.hpp:184-191): copies columns indices[0..count) into
  * out (count x m, row j = column indices[j]); out may be host or device. */
 int fstg_sketch_gather(const fstg_sketch* sk, const int64_t* indices, int64_t count, void* out, void* stream);
+/* Retain-sampled preprocessing: computes only the requested columns A s_ell,
+ * ell = indices[0..count), by running the FWHT over every Kerdock basis that
+ * holds a request (requests radix-sorted by ell) and keeping the sampled
+ * outputs; out is count x column_stride (device or host), column j at
+ * j * column_stride — the draw_and_gather buffer of stream.hpp:184-191. Works
+ * for design-only and materialised sketches (identical values). */
+int fstg_sample_columns(const fstg_sketch* sk, const int64_t* indices, int64_t count, void* out, void* stream);
 /* Device time of the last preprocess (ms, CUDA events). */
 int fstg_sketch_preprocess_ms(const fstg_sketch* sk, double* ms);
 void fstg_destroy(fstg_sketch* sk);
@@ -189,6 +203,14 @@ int fstg_gen_sparse_targets(const uint64_t* seeds, int64_t B, int64_t m, int64_t
 
 /* gen_mixture's target draw (generators.hpp:60-78), unnormalised. */
 int fstg_gen_mixture_targets(const uint64_t* seeds, int64_t B, int64_t m, double p, double* Y);
+
+/* transform_with_samples with drawn.use_gathered (stream.hpp:197-268, 235-236):
+ * vector v's sample j reads its column from gathered[(v * J*K + j) *
+ * column_stride] (device memory, e.g. filled by fstg_sample_columns) instead of
+ * the sketch; indices (B x J*K int64) still drive the coefficients. */
+int fstg_transform_gathered_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p,
+                                  const int64_t* indices, const void* gathered, int32_t* counts, int32_t* support,
+                                  void* values, int32_t* candidates, void* mu, void* stream);
 
 /* ------------------------------------------------------------ profiling ---- */
 /* When enabled, the library brackets each launch of its kernels with CUDA

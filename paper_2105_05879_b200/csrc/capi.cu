@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <cub/cub.cuh>
+
 #include "../../include/fst_b200.h"
 #include "design.hpp"
 #include "kernels.hpp"
@@ -259,7 +261,8 @@ struct DevBuf {
 
 // ---------------------------------------------------------- preprocess ----
 template <typename T>
-void build_sketch(fstg_sketch* sk, const void* a_in, cudaStream_t st, int64_t b0, int64_t b1, bool identity) {
+void build_sketch(fstg_sketch* sk, const void* a_in, cudaStream_t st, int64_t b0, int64_t b1, bool identity,
+                  bool materialize = true) {
   const int64_t m = sk->m, n = sk->n;
   const Design& D = sk->design;
   const int64_t nk = D.kerdock_bases();
@@ -289,8 +292,8 @@ void build_sketch(fstg_sketch* sk, const void* a_in, cudaStream_t st, int64_t b0
   }
 
   // sketch columns
-  const uint64_t col_bytes = uint64_t(D.L) * uint64_t(sk->ldc) * sizeof(T);
-  {
+  const uint64_t col_bytes = materialize ? uint64_t(D.L) * uint64_t(sk->ldc) * sizeof(T) : 0;
+  if (materialize) {
     cudaError_t e = cudaMalloc(&sk->cols, col_bytes);
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -301,7 +304,7 @@ void build_sketch(fstg_sketch* sk, const void* a_in, cudaStream_t st, int64_t b0
   sk->device_bytes += col_bytes;
   // Row padding (ldc > m) is zeroed; a basis-sharded build leaves the other
   // ranks' Kerdock blocks unwritten (they are filled by the all-gather).
-  if (sk->ldc != m) cuda_check(cudaMemsetAsync(sk->cols, 0, col_bytes, st), "memset sketch");
+  if (materialize && sk->ldc != m) cuda_check(cudaMemsetAsync(sk->cols, 0, col_bytes, st), "memset sketch");
 
   // Kerdock sign tables
   const std::vector<uint32_t> rev = reversed_row_table(D);
@@ -322,7 +325,7 @@ void build_sketch(fstg_sketch* sk, const void* a_in, cudaStream_t st, int64_t b0
   cuda_check(cudaEventCreate(&e0), "event");
   cuda_check(cudaEventCreate(&e1), "event");
   cuda_check(cudaEventRecord(e0, st), "event");
-  if (b1 > b0) {
+  if (materialize && b1 > b0) {
     ProfScope ps("preprocess_fwht", st);
     const cudaError_t e = launch_fwht_sketch<T>(D.k, static_cast<const T*>(sk->a), sk->lda, m, n, sk->qplain, b0,
                                                 b1, static_cast<T*>(sk->cols), sk->ldc, st);
@@ -332,7 +335,7 @@ void build_sketch(fstg_sketch* sk, const void* a_in, cudaStream_t st, int64_t b0
     }
     cuda_check(e, "fwht sketch kernel");
   }
-  if (identity) {
+  if (materialize && identity) {
     ProfScope ps("preprocess_identity", st);
     cuda_check(launch_identity<T>(static_cast<const T*>(sk->a), sk->lda, m, n, D.d, nk, static_cast<T*>(sk->cols),
                                   sk->ldc, st),
@@ -371,6 +374,121 @@ void destroy_sketch(fstg_sketch* sk) {
   cudaFree(sk->revtab);
   cudaSetDevice(prev);
   delete sk;
+}
+
+// -------------------------------------------------- retain-sampled columns ----
+__global__ void basis_ranges_kernel(const uint64_t* __restrict__ sorted, int64_t count, int64_t nk, int64_t d,
+                                    int64_t* __restrict__ start) {
+  for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s <= nk; s += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t key = static_cast<uint64_t>(s) * static_cast<uint64_t>(d);
+    int64_t lo = 0, hi = count;  // lower_bound
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (sorted[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    start[s] = lo;
+  }
+}
+
+template <typename T>
+__global__ void identity_requests_kernel(const T* __restrict__ a, int64_t lda, int64_t m, int64_t n, int64_t kb, T sqrt_d,
+                                         const uint64_t* __restrict__ ell, const int64_t* __restrict__ pos,
+                                         int64_t first, int64_t count, T* __restrict__ out, int64_t ldc) {
+  for (int64_t r = first + blockIdx.x; r < count; r += gridDim.x) {
+    const int64_t w = static_cast<int64_t>(ell[r]) - kb;
+    T* dst = out + pos[r] * ldc;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) dst[i] = (w < n) ? sqrt_d * a[i * lda + w] : T(0);
+  }
+}
+
+__global__ void iota_kernel(int64_t* v, int64_t count) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) v[i] = i;
+}
+
+__global__ void check_range_kernel(const int64_t* in, int64_t count, int64_t L, uint64_t* keys, int* bad) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t v = in[i];
+    if (v < 0 || v >= L) {
+      atomicExch(bad, 1);
+      keys[i] = 0;
+    } else {
+      keys[i] = static_cast<uint64_t>(v);
+    }
+  }
+}
+
+template <typename T>
+void sample_columns_impl(const fstg_sketch* sk, const int64_t* indices, int64_t count, void* out, cudaStream_t st) {
+  if (!sk) throw InvalidArgument("sample_columns: null sketch");
+  if (count < 0 || (count > 0 && (!indices || !out))) throw InvalidArgument("sample_columns: bad arguments");
+  if (count == 0) return;
+  if (!sk->has_a) throw CodedError(FSTG_ERR_NO_MATRIX, "Sketch: no embedded matrix");
+  cuda_check(cudaSetDevice(sk->device), "cudaSetDevice");
+  keep_pool_warm(sk->device);
+  const Design& D = sk->design;
+  const int64_t nk = D.kerdock_bases();
+  DevBuf idx_in, keys(size_t(count) * 8, st), keys_sorted(size_t(count) * 8, st), pos(size_t(count) * 8, st),
+      pos_sorted(size_t(count) * 8, st), start(size_t(nk + 1) * 8, st), bad(sizeof(int), st), out_buf;
+  const int64_t* id = indices;
+  if (!is_device_ptr(indices)) {
+    idx_in = DevBuf(size_t(count) * 8, st);
+    cuda_check(cudaMemcpyAsync(idx_in.p, indices, size_t(count) * 8, cudaMemcpyHostToDevice, st), "H2D indices");
+    id = idx_in.as<int64_t>();
+  }
+  T* dst = static_cast<T*>(out);
+  const bool out_is_dev = is_device_ptr(out);
+  if (!out_is_dev) {
+    out_buf = DevBuf(size_t(count) * sk->ldc * sizeof(T), st);
+    dst = out_buf.as<T>();
+  }
+  cuda_check(cudaMemsetAsync(bad.p, 0, sizeof(int), st), "memset");
+  const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((count + 255) / 256, 148 * 32));
+  check_range_kernel<<<blocks, 256, 0, st>>>(id, count, D.L, keys.as<uint64_t>(), bad.as<int>());
+  iota_kernel<<<blocks, 256, 0, st>>>(pos.as<int64_t>(), count);
+  cuda_check(cudaGetLastError(), "request setup");
+  // sort requests by ell (CUB radix sort, 32 key bits: L < 2^32)
+  size_t temp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, keys.as<uint64_t>(), keys_sorted.as<uint64_t>(),
+                                  pos.as<int64_t>(), pos_sorted.as<int64_t>(), count, 0, 32, st);
+  DevBuf temp(temp_bytes, st);
+  cuda_check(cub::DeviceRadixSort::SortPairs(temp.p, temp_bytes, keys.as<uint64_t>(), keys_sorted.as<uint64_t>(),
+                                             pos.as<int64_t>(), pos_sorted.as<int64_t>(), count, 0, 32, st),
+             "sort requests");
+  basis_ranges_kernel<<<static_cast<unsigned>((nk + 256) / 256), 256, 0, st>>>(keys_sorted.as<uint64_t>(), count, nk,
+                                                                             D.d, start.as<int64_t>());
+  cuda_check(cudaGetLastError(), "basis ranges");
+  {
+    ProfScope ps("sample_columns_fwht", st);
+    const cudaError_t e = launch_fwht_retain<T>(D.k, static_cast<const T*>(sk->a), sk->lda, sk->m, sk->n, sk->qplain,
+                                                nk, dst, sk->ldc, start.as<int64_t>(),
+                                                reinterpret_cast<const int64_t*>(keys_sorted.p), pos_sorted.as<int64_t>(),
+                                                st);
+    if (e == cudaErrorNotSupported) {
+      cudaGetLastError();
+      throw NotSupported("sample_columns: this (k, dtype) needs more than 227 KiB of shared memory per CTA");
+    }
+    cuda_check(e, "retain fwht");
+  }
+  {
+    // identity-block requests: sqrt(d) * A[:, w] (sketch.hpp:200-208); first index = start[nk]
+    int64_t first = 0;
+    cuda_check(cudaMemcpyAsync(&first, start.as<int64_t>() + nk, 8, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    if (first < count) {
+      ProfScope ps("sample_columns_identity", st);
+      identity_requests_kernel<T><<<static_cast<unsigned>(std::min<int64_t>(count - first, 148 * 16)), 256, 0, st>>>(
+          static_cast<const T*>(sk->a), sk->lda, sk->m, sk->n, nk * D.d,
+          static_cast<T>(std::sqrt(static_cast<double>(D.d))), keys_sorted.as<uint64_t>(), pos_sorted.as<int64_t>(),
+          first, count, dst, sk->ldc);
+      cuda_check(cudaGetLastError(), "identity requests");
+    }
+  }
+  int h = 0;
+  cuda_check(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st), "flag");
+  if (!out_is_dev)
+    cuda_check(cudaMemcpyAsync(out, dst, size_t(count) * sk->ldc * sizeof(T), cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+  if (h) throw OutOfRange("Sketch::column: index out of range");
 }
 
 // --------------------------------------------------------- persistence ----
@@ -446,6 +564,7 @@ void save_impl(const fstg_sketch* sk, const char* path, int version) {
   if (!sk || !path) throw InvalidArgument("save: null argument");
   if (version != 1 && version != 2) throw InvalidArgument("save: FSTK version must be 1 (float64) or 2 (float32)");
   if (version == 2 && sk->dtype != FSTG_F32) throw InvalidArgument("save: FSTK v2 holds float32 sketches");
+  if (!sk->cols) throw InvalidArgument("save: design-only sketch has no columns to save");
   cuda_check(cudaSetDevice(sk->device), "cudaSetDevice");
   File file(path, "wb");
   if (!file.f) throw CodedError(FSTG_ERR_IO, std::string("cannot open for writing: ") + path);
@@ -594,7 +713,7 @@ void load_impl(const char* path, int dtype, int device, void* stream, fstg_sketc
 }
 
 int preprocess_impl(const void* a, int dtype, int64_t m, int64_t n, int device, void* stream, int64_t b0, int64_t b1,
-                    bool full, int include_identity, fstg_sketch** out) {
+                    bool full, int include_identity, fstg_sketch** out, bool materialize = true) {
   return guarded([&] {
     if (out == nullptr) throw InvalidArgument("preprocess: out is null");
     *out = nullptr;
@@ -619,9 +738,9 @@ int preprocess_impl(const void* a, int dtype, int64_t m, int64_t n, int device, 
     sk->n = n;
     try {
       if (dtype == FSTG_F32)
-        build_sketch<float>(sk, a, st, b0, b1, full || include_identity);
+        build_sketch<float>(sk, a, st, b0, b1, full || include_identity, materialize);
       else
-        build_sketch<double>(sk, a, st, b0, b1, full || include_identity);
+        build_sketch<double>(sk, a, st, b0, b1, full || include_identity, materialize);
     } catch (...) {
       destroy_sketch(sk);
       throw;
@@ -641,7 +760,7 @@ struct Outputs {
 
 template <typename T>
 void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p, const uint64_t* seeds,
-               const int64_t* indices, const Outputs& out, cudaStream_t st) {
+               const int64_t* indices, const Outputs& out, cudaStream_t st, const void* gathered = nullptr) {
   validate(p);
   if (B < 0) throw InvalidArgument("transform: negative batch size");
   if (B == 0) return;
@@ -652,6 +771,10 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   const int64_t N = p->J * p->K;
   if (N > (int64_t(1) << 40)) throw NotSupported("transform: J*K too large for this build");
   if (!sk->has_a) throw CodedError(FSTG_ERR_NO_MATRIX, "Sketch: no embedded matrix");
+  if (sk->cols == nullptr && gathered == nullptr)
+    throw InvalidArgument("transform: design-only sketch; columns must come from fstg_transform_gathered_batch");
+  if (gathered != nullptr && !is_device_ptr(gathered))
+    throw InvalidArgument("transform_gathered: the gathered columns must be device memory");
   const int64_t want = candidate_count(p->s, p->widen, sk->m);
   const bool strict = p->mode == FSTG_MODE_STRICT || (p->mode == FSTG_MODE_DEFAULT && sk->dtype == FSTG_F64);
   if (p->mode < 0 || p->mode > 2) throw InvalidArgument("StreamParams: unknown mode");
@@ -695,12 +818,13 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   args.nseg = static_cast<int>((sk->ldc + SEG - 1) / SEG);
   if (args.nseg > 4) throw NotSupported("transform: m too large for this GPU build (m <= 4 * 16 KiB / sizeof(T))");
   size_t smem = 0;
-  int stages = 0, stage_stride = 0, rstride = 0;
-  const int grid_max = stream_grid_size<T>(args, strict, chunk, &smem, &stages, &stage_stride, &rstride);
+  int stages = 0, stage_stride = 0, rstride = 0, xbufs = 0;
+  const int grid_max = stream_grid_size<T>(args, strict, chunk, &smem, &stages, &stage_stride, &rstride, &xbufs);
   if (smem > 227 * 1024) throw NotSupported("transform: shared-memory plan exceeds 227 KiB (d or want too large)");
   args.stages = stages;
   args.stage_stride = stage_stride;
   args.rstride = rstride;
+  args.xbufs = xbufs;
   {
     const char* dbg = std::getenv("FSTG_STREAM_DEBUG");
     args.debug = dbg ? std::atoi(dbg) : 0;
@@ -775,6 +899,7 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
     // ---- estimator ----
     args.X = Xd;
     args.idx = bf.idx.as<uint32_t>();
+    args.gathered = gathered ? static_cast<const T*>(gathered) + v0 * N * sk->ldc : nullptr;
     args.B = cb;
     args.counts = o_dev ? out.counts + v0 : bf.counts.as<int32_t>();
     args.support = o_dev ? out.support + v0 * want : bf.support.as<int32_t>();
@@ -885,6 +1010,36 @@ int fstg_preprocess(const void* a, int dtype, int64_t m, int64_t n, int device, 
   return preprocess_impl(a, dtype, m, n, device, stream, 0, 0, true, 1, out);
 }
 
+int fstg_preprocess_design(const void* a, int dtype, int64_t m, int64_t n, int device, void* stream,
+                           fstg_sketch** out) {
+  return preprocess_impl(a, dtype, m, n, device, stream, 0, 0, true, 1, out, false);
+}
+
+int fstg_sample_columns(const fstg_sketch* sk, const int64_t* indices, int64_t count, void* out, void* stream) {
+  return guarded([&] {
+    if (!sk) throw InvalidArgument("sample_columns: null sketch");
+    if (sk->dtype == FSTG_F32)
+      sample_columns_impl<float>(sk, indices, count, out, static_cast<cudaStream_t>(stream));
+    else
+      sample_columns_impl<double>(sk, indices, count, out, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fstg_transform_gathered_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p,
+                                  const int64_t* indices, const void* gathered, int32_t* counts, int32_t* support,
+                                  void* values, int32_t* candidates, void* mu, void* stream) {
+  return guarded([&] {
+    if (!sk) throw InvalidArgument("null sketch");
+    if ((indices == nullptr || gathered == nullptr) && B > 0)
+      throw InvalidArgument("transform_gathered: indices and gathered columns are required");
+    const Outputs o{counts, support, values, candidates, mu};
+    if (sk->dtype == FSTG_F32)
+      run_batch<float>(sk, X, B, p, nullptr, indices, o, static_cast<cudaStream_t>(stream), gathered);
+    else
+      run_batch<double>(sk, X, B, p, nullptr, indices, o, static_cast<cudaStream_t>(stream), gathered);
+  });
+}
+
 int fstg_preprocess_shard(const void* a, int dtype, int64_t m, int64_t n, int device, void* stream,
                           int64_t basis_begin, int64_t basis_end, int include_identity, fstg_sketch** out) {
   return preprocess_impl(a, dtype, m, n, device, stream, basis_begin, basis_end, false, include_identity, out);
@@ -919,6 +1074,7 @@ int fstg_sketch_column(const fstg_sketch* sk, int64_t ell, void* out) {
   return guarded([&] {
     if (!sk || !out) throw InvalidArgument("null");
     if (ell < 0 || ell >= sk->design.L) throw OutOfRange("Sketch::column: index out of range");
+    if (!sk->cols) throw InvalidArgument("Sketch::column: design-only sketch (use fstg_sample_columns)");
     cuda_check(cudaSetDevice(sk->device), "cudaSetDevice");
     const size_t es = dtype_size(sk->dtype);
     cuda_check(cudaMemcpy(out, static_cast<const char*>(sk->cols) + size_t(ell) * sk->ldc * es, size_t(sk->m) * es,
@@ -932,6 +1088,7 @@ int fstg_sketch_gather(const fstg_sketch* sk, const int64_t* indices, int64_t co
     if (!sk || (count > 0 && (!indices || !out))) throw InvalidArgument("sketch_gather: null argument");
     if (count < 0) throw InvalidArgument("sketch_gather: negative count");
     if (count == 0) return;
+    if (!sk->cols) throw InvalidArgument("sketch_gather: design-only sketch (use fstg_sample_columns)");
     cuda_check(cudaSetDevice(sk->device), "cudaSetDevice");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t es = dtype_size(sk->dtype);

@@ -13,6 +13,12 @@ cudaError_t launch_qtables(const uint32_t* revtab, int k, int64_t nbases, uint32
 template <typename T>
 cudaError_t launch_fwht_sketch(int k, const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
                                int64_t basis_begin, int64_t basis_end, T* cols, int64_t ldc, cudaStream_t st);
+// Retain-sampled FWHT: only requested columns (sorted by ell; basis s owns
+// [req_start[s], req_start[s+1])) are written, to out[req_pos[r] * ldc].
+template <typename T>
+cudaError_t launch_fwht_retain(int k, const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
+                               int64_t nbases, T* out, int64_t ldc, const int64_t* req_start, const int64_t* req_ell,
+                               const int64_t* req_pos, cudaStream_t st);
 template <typename T>
 cudaError_t launch_identity(const T* a, int64_t lda, int64_t m, int64_t n, int64_t d, int64_t nk, T* cols,
                             int64_t ldc, cudaStream_t st);
@@ -47,6 +53,7 @@ struct StreamArgs {
   const T* X;
   int64_t ldx;
   const uint32_t* idx;  // B x N
+  const T* gathered;    // optional: B x N x ldc columns (draw_and_gather buffer); null -> cols + ell * ldc
   int64_t B;
   // outputs (device)
   int32_t* counts;
@@ -61,6 +68,7 @@ struct StreamArgs {
   int stages;
   int stage_stride;  // bytes between ring stages (>= one segment, 128-byte multiple)
   int rstride;       // bytes per refinement-ring stage (one row of A); 0 = direct loads
+  int xbufs;         // x buffers in shared memory (3, or 2 when d is large)
   int nseg;
   int chunk;
   // experiment switches (env FSTG_STREAM_DEBUG; 0 in production):
@@ -77,6 +85,6 @@ int64_t stream_scratch_elems(const StreamArgs<T>& args, int grid);
 // Persistent grid size the stream kernel wants for this configuration.
 template <typename T>
 int stream_grid_size(const StreamArgs<T>& args, bool strict, int64_t B, size_t* smem_bytes, int* stages,
-                     int* stage_stride, int* rstride);
+                     int* stage_stride, int* rstride, int* xbufs);
 
 }  // namespace fstg

@@ -124,17 +124,18 @@ __device__ __forceinline__ void reg_fwht(T (&v)[1 << HALF]) {
   }
 }
 
-// fp32 specialisation with packed FADD2 for stages h >= 2 (pairs (i, i+1)).
-template <>
-__device__ __forceinline__ void reg_fwht<float, 6>(float (&v)[64]) {
-  // stage h = 1 (scalar)
+// fp32: stage h = 1 scalar, stages h >= 2 as packed pairs (i, i+1) with FADD2
+// (x + y) and FFMA2(y, -1, x) (x - y, one rounding) — same values as scalar.
+template <int HALF>
+__device__ __forceinline__ void reg_fwht_f32_packed(float (&v)[1 << HALF]) {
+  constexpr int E = 1 << HALF;
 #pragma unroll
-  for (int i = 0; i < 64; i += 2) bfly(v[i], v[i + 1]);
+  for (int i = 0; i < E; i += 2) bfly(v[i], v[i + 1]);
 #pragma unroll
-  for (int hb = 1; hb < 6; ++hb) {
+  for (int hb = 1; hb < HALF; ++hb) {
     const int h = 1 << hb;
 #pragma unroll
-    for (int i = 0; i < 64; i += 2) {
+    for (int i = 0; i < E; i += 2) {
       if ((i & h) == 0) {
         const float2 x = make_float2(v[i], v[i + 1]);
         const float2 y = make_float2(v[i + h], v[i + h + 1]);
@@ -149,11 +150,27 @@ __device__ __forceinline__ void reg_fwht<float, 6>(float (&v)[64]) {
   }
 }
 
-template <typename T, int KB, int NT>
+template <typename T, int HALF>
+__device__ __forceinline__ void reg_fwht_any(T (&v)[1 << HALF]) {
+  if constexpr (sizeof(T) == 4 && HALF >= 2)
+    reg_fwht_f32_packed<HALF>(v);
+  else
+    reg_fwht<T, HALF>(v);
+}
+
+// RETAIN = false: write every column s*d + w (the full sketch).
+// RETAIN = true (retain-sampled, SURVEY.md §8(e) for n = 16384): only the
+// requested columns are kept — requests sorted by ell, basis s owning
+// [req_start[s], req_start[s+1]); request r writes column ell_r into slot
+// req_pos[r] of `cols` (stride ldc), i.e. the draw_and_gather buffer
+// (stream.hpp:184-191). Bases without requests are skipped.
+template <typename T, int KB, int NT, bool RETAIN>
 __global__ void __launch_bounds__(NT) fwht_sketch_kernel(const T* __restrict__ a, int64_t lda, int64_t m, int64_t n,
                                                          const uint32_t* __restrict__ qplain, int64_t basis_begin,
                                                          int64_t basis_end, int bases_per_cta, T* __restrict__ cols,
-                                                         int64_t ldc) {
+                                                         int64_t ldc, const int64_t* __restrict__ req_start,
+                                                         const int64_t* __restrict__ req_ell,
+                                                         const int64_t* __restrict__ req_pos) {
   using C = FwhtCfg<T, KB, NT>;
   constexpr int E = C::E, R = C::R, RS = C::RS, D = C::D, SW = C::SW;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -175,6 +192,9 @@ __global__ void __launch_bounds__(NT) fwht_sketch_kernel(const T* __restrict__ a
   constexpr int WPB = D >= 32 ? D / 32 : 1;
 
   for (int64_t s = s_first; s < s_last; ++s) {
+    if constexpr (RETAIN) {
+      if (req_start[s] == req_start[s + 1]) continue;  // no sample in this basis (uniform per CTA)
+    }
     T v[E];
     // ---- load + sign mask + zero padding (sketch.hpp:182-186) ----
     uint32_t qw[(E + 31) / 32];
@@ -220,7 +240,7 @@ __global__ void __launch_bounds__(NT) fwht_sketch_kernel(const T* __restrict__ a
       v[e] = bit ? -v[e] : v[e];  // sign[j] * a_ij with sign = +-1 (exact)
     }
     // ---- stages h = 1 .. E/2 in registers ----
-    reg_fwht<T, C::HALF>(v);
+    reg_fwht_any<T, C::HALF>(v);
     // ---- transpose through shared memory ----
     __syncthreads();  // previous basis' phase-2 reads are done
     {
@@ -235,7 +255,23 @@ __global__ void __launch_bounds__(NT) fwht_sketch_kernel(const T* __restrict__ a
       for (int e = 0; e < E; ++e) v[e] = src[e * E + (q2 ^ (e & SW))];
     }
     // ---- stages h = E .. D/2 (register index bit j <-> position bit HALF + j) ----
-    reg_fwht<T, C::HALF>(v);
+    reg_fwht_any<T, C::HALF>(v);
+    if constexpr (RETAIN) {
+      // stage the R x D result as [w][r] in the (now free) tile, then copy the
+      // requested columns' R-row segments to their slots.
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < E; ++e) tile[(int64_t(e) * E + q2) * R + r2] = v[e];
+      __syncthreads();
+      const int64_t r_lo = req_start[s], r_hi = req_start[s + 1];
+      for (int64_t it = tid; it < (r_hi - r_lo) * R; it += NT) {
+        const int64_t r = r_lo + it / R;
+        const int rr = static_cast<int>(it % R);
+        const int64_t w = req_ell[r] - s * D;
+        if (i0 + rr < m) cols[req_pos[r] * ldc + i0 + rr] = tile[w * R + rr];
+      }
+      continue;  // the next basis' first __syncthreads orders the tile reuse
+    }
     // ---- transposed write-back: column s*d + w, row i0 + r2 (sketch.hpp:191-196) ----
     if (row2 < m) {
       T* ptr = cols + (s * D + q2) * ldc + row2;
@@ -254,14 +290,17 @@ __global__ void __launch_bounds__(NT) fwht_sketch_kernel(const T* __restrict__ a
 }
 
 // ---------------------------------------------------------------------------
-// k = 12 fp32 specialisation (the n = 4096 headline): the CTA's 8 rows of A
-// are parked in tensor memory (TMEM, 128 KiB of the SM's 256 KiB) once and
-// re-read with tcgen05.ld for every basis, so the per-basis loop has no
-// global loads; butterflies on register bits >= 1 use packed FADD2 / FFMA2
-// (x - y as fma(y, -1, x), exactly rounded like the reference's x - y); the
-// smem transpose uses 16-byte chunk-swizzled stores.
-// Thread layout as in the generic kernel: E = 64, R = 8 rows, 512 threads.
-// TMEM: warp w owns lanes 32*(w%4) .. +31 and columns 64*(w/4) .. +63.
+// fp32 TMEM-resident FWHT for k = 12 (n = 4096 headline) and k = 14 (n = 16384):
+// the CTA's R rows of A are parked in tensor memory once (tcgen05.st; 128 KiB
+// of the SM's 256 KiB) and re-read with tcgen05.ld for every basis, so the
+// per-basis loop issues no global loads (at k = 14 A is 1 GiB and would
+// otherwise be re-read from HBM for every basis). Butterflies on register bits
+// >= 1 are packed FADD2 / FFMA2(y, -1, x) (exactly rounded x - y); the smem
+// transpose uses 16-byte chunk swizzling (conflict-free both ways).
+//   k = 12: E = 64 elements/thread, R = 8 rows, 512 threads.
+//   k = 14: E = 128, R = 2 rows, 256 threads.
+// TMEM: warp w owns lanes 32*(w%4) .. +31 and columns E*(w/4) .. +E-1.
+// RETAIN: keep only requested columns (see fwht_sketch_kernel).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const float* v) {
   asm volatile(
@@ -289,40 +328,28 @@ __device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, float* v) {
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// Butterflies over register-index bits [0, 6) of v[64], ascending; bit 0
-// scalar, bits >= 1 as packed pairs (i, i+1) with FADD2 / FFMA2(-1).
-__device__ __forceinline__ void reg_fwht64_packed(float (&v)[64]) {
-#pragma unroll
-  for (int i = 0; i < 64; i += 2) {
-    const float a = v[i], b = v[i + 1];
-    v[i] = a + b;
-    v[i + 1] = a - b;
-  }
-#pragma unroll
-  for (int hb = 1; hb < 6; ++hb) {
-    const int h = 1 << hb;
-#pragma unroll
-    for (int i = 0; i < 64; i += 2) {
-      if ((i & h) == 0) {
-        const float2 x = make_float2(v[i], v[i + 1]);
-        const float2 y = make_float2(v[i + h], v[i + h + 1]);
-        const float2 s = __fadd2_rn(x, y);
-        const float2 d = __ffma2_rn(y, make_float2(-1.f, -1.f), x);
-        v[i] = s.x;
-        v[i + 1] = s.y;
-        v[i + h] = d.x;
-        v[i + h + 1] = d.y;
-      }
-    }
-  }
-}
+template <int KB>
+struct TmemCfg {
+  static constexpr int HALF = KB / 2;
+  static constexpr int E = 1 << HALF;
+  static constexpr int D = 1 << KB;
+  static constexpr int NT = (KB == 12) ? 512 : 256;
+  static constexpr int R = NT / E;
+  static constexpr int RS = D + 32 / R;          // row stride (floats): phase-2 reads conflict-free
+  static constexpr int WPT = E / 32;             // sign words per thread
+  static constexpr int CH = E / 4;               // 16-byte chunks per thread
+  static constexpr int SWC = CH - 1;             // chunk swizzle mask
+  static constexpr size_t SMEM = size_t(R) * RS * sizeof(float);
+};
 
-__global__ void __launch_bounds__(512, 1) fwht12_tmem_kernel(const float* __restrict__ a, int64_t lda, int64_t m,
-                                                             int64_t n, const uint32_t* __restrict__ qplain,
-                                                             int64_t basis_begin, int64_t basis_end,
-                                                             int bases_per_cta, float* __restrict__ cols,
-                                                             int64_t ldc, int store_mode) {
-  constexpr int E = 64, R = 8, RS = 4096 + 4, D = 4096, WPB = 128;
+template <int KB, bool RETAIN>
+__global__ void __launch_bounds__(TmemCfg<KB>::NT, 1) fwht_tmem_kernel(
+    const float* __restrict__ a, int64_t lda, int64_t m, int64_t n, const uint32_t* __restrict__ qplain,
+    int64_t basis_begin, int64_t basis_end, int bases_per_cta, float* __restrict__ cols, int64_t ldc,
+    const int64_t* __restrict__ req_start, const int64_t* __restrict__ req_ell, const int64_t* __restrict__ req_pos) {
+  using C = TmemCfg<KB>;
+  constexpr int E = C::E, R = C::R, RS = C::RS, D = C::D, NT = C::NT, WPT = C::WPT, CH = C::CH, SWC = C::SWC;
+  constexpr int WPB = D / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* tile = reinterpret_cast<float*>(smem_raw);
   __shared__ uint32_t tmem_base_slot;
@@ -331,13 +358,11 @@ __global__ void __launch_bounds__(512, 1) fwht12_tmem_kernel(const float* __rest
   const int64_t i0 = int64_t(blockIdx.x) * R;
   const int64_t s_first = basis_begin + int64_t(blockIdx.y) * bases_per_cta;
   const int64_t s_last = min(basis_end, s_first + bases_per_cta);
-
   const int r1 = tid / E, p1 = tid % E;
   const int64_t row1 = i0 + r1;
   const int r2 = tid % R, q2 = tid / R;
   const int64_t row2 = i0 + r2;
 
-  // ---- TMEM: allocate 256 columns, park the A tile ----
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base_slot))
                  : "memory");
@@ -347,63 +372,65 @@ __global__ void __launch_bounds__(512, 1) fwht12_tmem_kernel(const float* __rest
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t taddr = tmem_base_slot + (static_cast<uint32_t>(32 * (warp % 4)) << 16) +
-                         static_cast<uint32_t>(64 * (warp / 4));
+                         static_cast<uint32_t>(E * (warp / 4));
   {
     float v[E];
     const int64_t pos0 = int64_t(p1) * E;
-    if (row1 < m) {
+    if (row1 < m && pos0 + E <= n) {
       const float* arow = a + row1 * lda;
-      if (pos0 + E <= n) {
 #pragma unroll
-        for (int e = 0; e < E; e += 4) {
-          const float4 f = __ldg(reinterpret_cast<const float4*>(arow + pos0 + e));
-          v[e] = f.x;
-          v[e + 1] = f.y;
-          v[e + 2] = f.z;
-          v[e + 3] = f.w;
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) v[e] = (pos0 + e < n) ? arow[pos0 + e] : 0.f;
+      for (int e = 0; e < E; e += 4) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(arow + pos0 + e));
+        v[e] = f.x;
+        v[e + 1] = f.y;
+        v[e + 2] = f.z;
+        v[e + 3] = f.w;
       }
     } else {
 #pragma unroll
-      for (int e = 0; e < E; ++e) v[e] = 0.f;
+      for (int e = 0; e < E; ++e) v[e] = (row1 < m && pos0 + e < n) ? a[row1 * lda + pos0 + e] : 0.f;
     }
-    tmem_st_x32(taddr, v);
-    tmem_st_x32(taddr + 32, v + 32);
+#pragma unroll
+    for (int c = 0; c < E / 32; ++c) tmem_st_x32(taddr + 32 * c, v + 32 * c);
     tmem_wait_st();
   }
 
-  // sign words of the next basis are prefetched one iteration ahead (L2 latency)
-  uint32_t q0n = 0, q1n = 0;
-  if (s_first < s_last) {
-    q0n = __ldg(qplain + s_first * WPB + 2 * p1);
-    q1n = __ldg(qplain + s_first * WPB + 2 * p1 + 1);
-  }
-  for (int64_t s = s_first; s < s_last; ++s) {
+  // RETAIN visits only bases holding a requested column (uniform per CTA)
+  auto next_basis = [&](int64_t s) {
+    if constexpr (RETAIN) {
+      while (s < s_last && req_start[s] == req_start[s + 1]) ++s;
+    }
+    return s;
+  };
+  // sign words of the next visited basis are prefetched one iteration ahead (L2 latency)
+  int64_t s = next_basis(s_first);
+  uint32_t qn[WPT];
+#pragma unroll
+  for (int w = 0; w < WPT; ++w) qn[w] = (s < s_last) ? __ldg(qplain + s * WPB + WPT * p1 + w) : 0u;
+  while (s < s_last) {
+    const int64_t s_next = next_basis(s + 1);
     float v[E];
-    tmem_ld_x32(taddr, v);
-    tmem_ld_x32(taddr + 32, v + 32);
-    const uint32_t q0 = q0n, q1 = q1n;
-    if (s + 1 < s_last) {
-      q0n = __ldg(qplain + (s + 1) * WPB + 2 * p1);
-      q1n = __ldg(qplain + (s + 1) * WPB + 2 * p1 + 1);
+#pragma unroll
+    for (int c = 0; c < E / 32; ++c) tmem_ld_x32(taddr + 32 * c, v + 32 * c);
+    uint32_t q[WPT];
+#pragma unroll
+    for (int w = 0; w < WPT; ++w) q[w] = qn[w];
+    if (s_next < s_last) {
+#pragma unroll
+      for (int w = 0; w < WPT; ++w) qn[w] = __ldg(qplain + s_next * WPB + WPT * p1 + w);
     }
     tmem_wait_ld();
-    // sign mask (sketch.hpp:185): flip the sign bit where Q_s(pos) = 1 (exact)
+    // Kerdock sign mask (sketch.hpp:185): flip the sign bit where Q_s(pos) = 1 (exact)
 #pragma unroll
-    for (int e = 0; e < 32; ++e) v[e] = __uint_as_float(__float_as_uint(v[e]) ^ ((q0 << (31 - e)) & 0x80000000u));
-#pragma unroll
-    for (int e = 0; e < 32; ++e)
-      v[32 + e] = __uint_as_float(__float_as_uint(v[32 + e]) ^ ((q1 << (31 - e)) & 0x80000000u));
-    if (store_mode < 2) reg_fwht64_packed(v);  // position bits 0..5 (store_mode 2: write-path experiment)
-    __syncthreads();       // previous basis' phase-2 reads done
+    for (int e = 0; e < E; ++e)
+      v[e] = __uint_as_float(__float_as_uint(v[e]) ^ ((q[e / 32] << (31 - (e % 32))) & 0x80000000u));
+    reg_fwht_f32_packed<C::HALF>(v);  // position bits 0 .. HALF-1
+    __syncthreads();                  // previous basis' tile reads done
     {
       float* dst = tile + r1 * RS + p1 * E;
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
-        *reinterpret_cast<float4*>(dst + 4 * (c ^ (p1 & 15))) =
+      for (int c = 0; c < CH; ++c)
+        *reinterpret_cast<float4*>(dst + 4 * (c ^ (p1 & SWC))) =
             make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     }
     __syncthreads();
@@ -411,189 +438,33 @@ __global__ void __launch_bounds__(512, 1) fwht12_tmem_kernel(const float* __rest
       const float* src = tile + r2 * RS + (q2 & 3);
       const int cq = q2 >> 2;
 #pragma unroll
-      for (int e = 0; e < E; ++e) v[e] = src[e * E + 4 * (cq ^ (e & 15))];
+      for (int e = 0; e < E; ++e) v[e] = src[e * E + 4 * (cq ^ (e & SWC))];
     }
-    if (store_mode < 2) reg_fwht64_packed(v);  // position bits 6..11
-    if (row2 < m) {
-      // incremental addressing keeps 64 hoisted 64-bit offsets out of registers
-      float* ptr = cols + (s * D + q2) * ldc + row2;
-      const int64_t step = int64_t(E) * ldc;
-      if (store_mode == 0) {
+    reg_fwht_f32_packed<C::HALF>(v);  // position bits HALF .. KB-1
+    if constexpr (RETAIN) {
+      __syncthreads();
 #pragma unroll
-        for (int e = 0; e < E; ++e) {
-          ptr[0] = v[e];  // default policy: L2 merges the 4 CTAs' 32-byte sectors of a line
-          ptr += step;
-          asm volatile("" : "+l"(ptr));
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) {
-          __stcs(ptr, v[e]);  // streaming store (evict-first)
-          ptr += step;
-          asm volatile("" : "+l"(ptr));
-        }
-      }
-    }
-  }
-
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_base_slot) : "memory");
-}
-
-// ---------------------------------------------------------------------------
-// k = 12 fp32, row-pair variant: 256 threads, 8 rows per CTA; thread (rp, p)
-// owns rows (2rp, 2rp+1) x positions p*64 .. p*64+63 as 64 float2 pairs, so
-// every butterfly stage is one FADD2 (x+y) + one FFMA2(y, -1, x) per pair
-// butterfly on natural register pairs, the Kerdock sign mask is shared by the
-// two rows, and the write-back is STG.64 (two consecutive rows of a column).
-// smem tile: row-pair block rp at rp * RSP floats, pair of position pos at
-// 2*pos, 16-byte chunk c of thread p stored at chunk c ^ (p & 7);
-// RSP = 8192 + 8 makes both the STS.128 and the LDS.64 patterns conflict-free.
-// TMEM: warp w owns lanes 32*(w%4) .. +31, columns 128*(w/4) .. +127.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 1) fwht12_pairs_kernel(const float* __restrict__ a, int64_t lda, int64_t m,
-                                                              int64_t n, const uint32_t* __restrict__ qplain,
-                                                              int64_t basis_begin, int64_t basis_end,
-                                                              int bases_per_cta, float* __restrict__ cols,
-                                                              int64_t ldc) {
-  constexpr int E = 64, D = 4096, WPB = 128, RSP = 8192 + 8;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float* tile = reinterpret_cast<float*>(smem_raw);
-  __shared__ uint32_t tmem_base_slot;
-
-  const int tid = threadIdx.x, warp = tid / 32;
-  const int64_t i0 = int64_t(blockIdx.x) * 8;
-  const int64_t s_first = basis_begin + int64_t(blockIdx.y) * bases_per_cta;
-  const int64_t s_last = min(basis_end, s_first + bases_per_cta);
-
-  const int rp = tid / E, p1 = tid % E;    // phase 1: row pair, position group
-  const int rp2 = tid % 4, q2 = tid / 4;   // phase 2: row pair, position residue
-  const int64_t row_a = i0 + 2 * rp, row2 = i0 + 2 * rp2;
-
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base_slot))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t taddr = tmem_base_slot + (static_cast<uint32_t>(32 * (warp % 4)) << 16) +
-                         static_cast<uint32_t>(128 * (warp / 4));
-  {
-    // park the two rows' 64 values as interleaved pairs (v[2e], v[2e+1]) = (row_a, row_a+1)
-    float v[2 * E];
-    const int64_t pos0 = int64_t(p1) * E;
-#pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int64_t row = row_a + r;
-      if (row < m && pos0 + E <= n) {
-        const float* arow = a + row * lda + pos0;
-#pragma unroll
-        for (int e = 0; e < E; e += 4) {
-          const float4 f = __ldg(reinterpret_cast<const float4*>(arow + e));
-          v[2 * e + r] = f.x;
-          v[2 * (e + 1) + r] = f.y;
-          v[2 * (e + 2) + r] = f.z;
-          v[2 * (e + 3) + r] = f.w;
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) v[2 * e + r] = (row < m && pos0 + e < n) ? a[row * lda + pos0 + e] : 0.f;
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) tmem_st_x32(taddr + 32 * c, v + 32 * c);
-    tmem_wait_st();
-  }
-
-  uint32_t q0n = 0, q1n = 0;
-  if (s_first < s_last) {
-    q0n = __ldg(qplain + s_first * WPB + 2 * p1);
-    q1n = __ldg(qplain + s_first * WPB + 2 * p1 + 1);
-  }
-  for (int64_t s = s_first; s < s_last; ++s) {
-    float2 V[E];
-    {
-      float* vf = reinterpret_cast<float*>(V);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld_x32(taddr + 32 * c, vf + 32 * c);
-    }
-    const uint32_t q0 = q0n, q1 = q1n;
-    if (s + 1 < s_last) {
-      q0n = __ldg(qplain + (s + 1) * WPB + 2 * p1);
-      q1n = __ldg(qplain + (s + 1) * WPB + 2 * p1 + 1);
-    }
-    tmem_wait_ld();
-    // Kerdock sign mask (sketch.hpp:185), shared by both rows of the pair
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const uint32_t msk = ((e < 32 ? q0 : q1) << (31 - (e & 31))) & 0x80000000u;
-      V[e].x = __uint_as_float(__float_as_uint(V[e].x) ^ msk);
-      V[e].y = __uint_as_float(__float_as_uint(V[e].y) ^ msk);
-    }
-    // position bits 0..5 (h = 1 .. 32), reference stage order
-#pragma unroll
-    for (int hb = 0; hb < 6; ++hb) {
-      const int h = 1 << hb;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        if ((e & h) == 0) {
-          const float2 x = V[e], y = V[e + h];
-          V[e] = __fadd2_rn(x, y);
-          V[e + h] = __ffma2_rn(y, make_float2(-1.f, -1.f), x);
-        }
-      }
-    }
-    __syncthreads();  // previous basis' phase-2 reads done
-    {
-      float* dst = tile + rp * RSP + p1 * (2 * E);
-#pragma unroll
-      for (int c = 0; c < 32; ++c)
-        *reinterpret_cast<float4*>(dst + 4 * (c ^ (p1 & 7))) = make_float4(V[2 * c].x, V[2 * c].y, V[2 * c + 1].x,
-                                                                          V[2 * c + 1].y);
-    }
-    __syncthreads();
-    {
-      const float* src = tile + rp2 * RSP + 2 * (q2 & 1);
-      const int cq = q2 >> 1;
-#pragma unroll
-      for (int e = 0; e < E; ++e) V[e] = *reinterpret_cast<const float2*>(src + e * (2 * E) + 4 * (cq ^ (e & 7)));
-    }
-    // position bits 6..11 (h = 64 .. 2048)
-#pragma unroll
-    for (int hb = 0; hb < 6; ++hb) {
-      const int h = 1 << hb;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        if ((e & h) == 0) {
-          const float2 x = V[e], y = V[e + h];
-          V[e] = __fadd2_rn(x, y);
-          V[e + h] = __ffma2_rn(y, make_float2(-1.f, -1.f), x);
-        }
-      }
-    }
-    // transposed write-back (sketch.hpp:191-196): column s*d + e*64 + q2, rows row2, row2+1
-    if (row2 + 1 < m) {
-      float* ptr = cols + (s * D + q2) * ldc + row2;
-      const int64_t step = int64_t(E) * ldc;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        __stcs(reinterpret_cast<float2*>(ptr), V[e]);
-        ptr += step;
-        asm volatile("" : "+l"(ptr));
+      for (int e = 0; e < E; ++e) tile[(int64_t(e) * E + q2) * R + r2] = v[e];
+      __syncthreads();
+      const int64_t r_lo = req_start[s], r_hi = req_start[s + 1];
+      for (int64_t it = tid; it < (r_hi - r_lo) * R; it += NT) {
+        const int64_t r = r_lo + it / R;
+        const int rr = static_cast<int>(it % R);
+        const int64_t w = req_ell[r] - s * D;
+        if (i0 + rr < m) cols[req_pos[r] * ldc + i0 + rr] = tile[w * R + rr];
       }
     } else if (row2 < m) {
+      // transposed write-back (sketch.hpp:191-196): column s*d + e*E + q2, row row2
       float* ptr = cols + (s * D + q2) * ldc + row2;
       const int64_t step = int64_t(E) * ldc;
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        __stcs(ptr, V[e].x);
+        ptr[0] = v[e];
         ptr += step;
         asm volatile("" : "+l"(ptr));
       }
     }
+    s = s_next;
   }
 
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -654,13 +525,16 @@ cudaError_t launch_qtables(const uint32_t* revtab, int k, int64_t nbases, uint32
   return cudaGetLastError();
 }
 
-template <typename T, int KB>
+template <typename T, int KB, bool RETAIN = false>
 static cudaError_t launch_fwht_k(const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
-                                 int64_t b0, int64_t b1, T* cols, int64_t ldc, cudaStream_t st) {
+                                 int64_t b0, int64_t b1, T* cols, int64_t ldc, cudaStream_t st,
+                                 const int64_t* req_start = nullptr, const int64_t* req_ell = nullptr,
+                                 const int64_t* req_pos = nullptr) {
   constexpr int NT = (sizeof(T) == 8 && KB >= 12) ? 256 : ((KB >= 14) ? 256 : 512);
   using C = FwhtCfg<T, KB, NT>;
   static_assert(C::R >= 1, "rows per CTA");
-  auto kern = fwht_sketch_kernel<T, KB, NT>;
+  static_assert(!RETAIN || size_t(C::D) * C::R <= size_t(C::R) * C::RS, "retain staging fits the tile");
+  auto kern = fwht_sketch_kernel<T, KB, NT, RETAIN>;
   if (C::SMEM > 227 * 1024) return cudaErrorNotSupported;
   if (C::SMEM > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
@@ -675,44 +549,60 @@ static cudaError_t launch_fwht_k(const T* a, int64_t lda, int64_t m, int64_t n, 
   const int64_t gy = (nb + bpc - 1) / bpc;
   if (row_tiles > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
   dim3 grid(static_cast<unsigned>(row_tiles), static_cast<unsigned>(gy));
-  kern<<<grid, NT, C::SMEM, st>>>(a, lda, m, n, qplain, b0, b1, bpc, cols, ldc);
+  kern<<<grid, NT, C::SMEM, st>>>(a, lda, m, n, qplain, b0, b1, bpc, cols, ldc, req_start, req_ell, req_pos);
   return cudaGetLastError();
 }
 
-static cudaError_t launch_fwht12_tmem(const float* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
-                                      int64_t b0, int64_t b1, float* cols, int64_t ldc, cudaStream_t st) {
-  constexpr size_t smem = size_t(8) * (4096 + 4) * sizeof(float);
-  cudaError_t e = cudaFuncSetAttribute(fwht12_tmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  if (e != cudaSuccess) return e;
-  const int64_t nb = b1 - b0;
-  if (nb <= 0) return cudaSuccess;
-  const int64_t row_tiles = (m + 7) / 8;
-  int bpc = 32;
-  if (const char* b = std::getenv("FSTG_FWHT_BPC")) bpc = std::max(1, std::atoi(b));  // A/B experiments only
-  while (bpc > 1 && row_tiles * ((nb + bpc - 1) / bpc) < 148 * 8) bpc /= 2;
-  const int64_t gy = (nb + bpc - 1) / bpc;
-  if (row_tiles > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
-  const char* sm = std::getenv("FSTG_FWHT_STORE");  // A/B experiments only
-  const int store_mode = (sm && std::string(sm) == "cs") ? 1 : (sm && std::string(sm) == "nofwht") ? 2 : 0;
-  fwht12_tmem_kernel<<<dim3(static_cast<unsigned>(row_tiles), static_cast<unsigned>(gy)), 512, smem, st>>>(
-      a, lda, m, n, qplain, b0, b1, bpc, cols, ldc, store_mode);
-  return cudaGetLastError();
-}
+template <int KB, bool RETAIN>
+static cudaError_t launch_fwht_tmem(const float* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
+                                    int64_t b0, int64_t b1, float* cols, int64_t ldc, cudaStream_t st,
+                                    const int64_t* req_start, const int64_t* req_ell, const int64_t* req_pos);
 
-static cudaError_t launch_fwht12_pairs(const float* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
-                                       int64_t b0, int64_t b1, float* cols, int64_t ldc, cudaStream_t st) {
-  constexpr size_t smem = size_t(4) * (8192 + 8) * sizeof(float);
-  cudaError_t e = cudaFuncSetAttribute(fwht12_pairs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+template <typename T>
+cudaError_t launch_fwht_retain(int k, const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
+                               int64_t nbases, T* out, int64_t ldc, const int64_t* req_start, const int64_t* req_ell,
+                               const int64_t* req_pos, cudaStream_t st) {
+  if constexpr (sizeof(T) == 4) {
+    if (k == 12 && (lda % 4) == 0)
+      return launch_fwht_tmem<12, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
+    if (k == 14 && (lda % 4) == 0)
+      return launch_fwht_tmem<14, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
+  }
+  switch (k) {
+    case 2: return launch_fwht_k<T, 2, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
+    case 4: return launch_fwht_k<T, 4, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
+    case 6: return launch_fwht_k<T, 6, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
+    case 8: return launch_fwht_k<T, 8, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
+    case 10: return launch_fwht_k<T, 10, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
+    case 12: return launch_fwht_k<T, 12, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
+    case 14: return launch_fwht_k<T, 14, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
+    default: return cudaErrorNotSupported;
+  }
+}
+template cudaError_t launch_fwht_retain<float>(int, const float*, int64_t, int64_t, int64_t, const uint32_t*, int64_t,
+                                               float*, int64_t, const int64_t*, const int64_t*, const int64_t*,
+                                               cudaStream_t);
+template cudaError_t launch_fwht_retain<double>(int, const double*, int64_t, int64_t, int64_t, const uint32_t*, int64_t,
+                                                double*, int64_t, const int64_t*, const int64_t*, const int64_t*,
+                                                cudaStream_t);
+
+template <int KB, bool RETAIN>
+static cudaError_t launch_fwht_tmem(const float* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
+                                    int64_t b0, int64_t b1, float* cols, int64_t ldc, cudaStream_t st,
+                                    const int64_t* req_start, const int64_t* req_ell, const int64_t* req_pos) {
+  using C = TmemCfg<KB>;
+  auto kern = fwht_tmem_kernel<KB, RETAIN>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
   if (e != cudaSuccess) return e;
   const int64_t nb = b1 - b0;
   if (nb <= 0) return cudaSuccess;
-  const int64_t row_tiles = (m + 7) / 8;
-  int bpc = 32;
+  const int64_t row_tiles = (m + C::R - 1) / C::R;
+  int bpc = RETAIN ? 256 : 32;  // the A tile is reused across bpc bases (TMEM)
   while (bpc > 1 && row_tiles * ((nb + bpc - 1) / bpc) < 148 * 8) bpc /= 2;
   const int64_t gy = (nb + bpc - 1) / bpc;
   if (row_tiles > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
-  fwht12_pairs_kernel<<<dim3(static_cast<unsigned>(row_tiles), static_cast<unsigned>(gy)), 256, smem, st>>>(
-      a, lda, m, n, qplain, b0, b1, bpc, cols, ldc);
+  kern<<<dim3(static_cast<unsigned>(row_tiles), static_cast<unsigned>(gy)), C::NT, C::SMEM, st>>>(
+      a, lda, m, n, qplain, b0, b1, bpc, cols, ldc, req_start, req_ell, req_pos);
   return cudaGetLastError();
 }
 
@@ -720,11 +610,10 @@ template <typename T>
 cudaError_t launch_fwht_sketch(int k, const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
                                int64_t b0, int64_t b1, T* cols, int64_t ldc, cudaStream_t st) {
   if constexpr (sizeof(T) == 4) {
-    if (k == 12 && (lda % 4) == 0) {
-      const char* var = std::getenv("FSTG_FWHT_VARIANT");  // A/B experiments only
-      if (var && std::string(var) == "pairs") return launch_fwht12_pairs(a, lda, m, n, qplain, b0, b1, cols, ldc, st);
-      return launch_fwht12_tmem(a, lda, m, n, qplain, b0, b1, cols, ldc, st);
-    }
+    if (k == 12 && (lda % 4) == 0)
+      return launch_fwht_tmem<12, false>(a, lda, m, n, qplain, b0, b1, cols, ldc, st, nullptr, nullptr, nullptr);
+    if (k == 14 && (lda % 4) == 0)
+      return launch_fwht_tmem<14, false>(a, lda, m, n, qplain, b0, b1, cols, ldc, st, nullptr, nullptr, nullptr);
   }
   switch (k) {
     case 2: return launch_fwht_k<T, 2>(a, lda, m, n, qplain, b0, b1, cols, ldc, st);

@@ -92,7 +92,7 @@ struct SmemLayout {
 
 template <typename T>
 __host__ __device__ inline SmemLayout smem_layout(int64_t d, int stages, int stage_stride, int64_t want,
-                                                  int rstride) {
+                                                  int rstride, int xbufs) {
   SmemLayout L{};
   size_t off = 0;
   auto take = [&off](size_t bytes, size_t align) {
@@ -102,7 +102,7 @@ __host__ __device__ inline SmemLayout smem_layout(int64_t d, int stages, int sta
     return at;
   };
   L.ring = take(size_t(stages) * stage_stride, 1024);
-  L.x = take(kXBuf * size_t(d < 4 ? 4 : d) * sizeof(T), 16);
+  L.x = take(size_t(xbufs) * size_t(d < 4 ? 4 : d) * sizeof(T), 16);
   L.tbuf = take(kTRing * sizeof(T), 16);
   L.bars = take((2 * kMaxStages + 2 * kTRing + 2 * kXBuf + 4 + 2 * kRStages) * sizeof(uint64_t), 8);
   L.hist = take(256 * sizeof(uint32_t), 16);
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
   constexpr int CPT = CPS / kNC;                                  // chunks per consumer thread per segment
 
   extern __shared__ __align__(1024) unsigned char smem[];
-  const SmemLayout Ls = smem_layout<T>(A.d, A.stages, A.stage_stride, A.want, A.rstride);
+  const SmemLayout Ls = smem_layout<T>(A.d, A.stages, A.stage_stride, A.want, A.rstride, A.xbufs);
   unsigned char* ring = smem + Ls.ring;
   T* xbuf = reinterpret_cast<T*>(smem + Ls.x);
   T* tring = reinterpret_cast<T*>(smem + Ls.tbuf);
@@ -415,7 +415,8 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
       for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x) {
         const uint32_t* vidx = A.idx + v * A.N;
         for (int64_t j = 0; j < A.N; ++j) {
-          const T* col = A.cols + static_cast<int64_t>(__ldg(vidx + j)) * A.ldc;
+          const T* col = A.gathered ? A.gathered + (v * A.N + j) * A.ldc
+                                    : A.cols + static_cast<int64_t>(__ldg(vidx + j)) * A.ldc;
           for (int sg = 0; sg < A.nseg; ++sg) {
             if (used) mbar_wait(&empty[stage], phase ^ 1u);
             const uint32_t bytes = (sg == A.nseg - 1) ? stage_bytes_last : stage_bytes_full;
@@ -439,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     const int ctid = tid - kWarpCoef * 32;  // 0 .. kCW*32-1
     uint32_t lv = 0;
     for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
-      const uint32_t xb = lv % kXBuf, xu = lv / kXBuf;
+      const uint32_t xb = lv % static_cast<uint32_t>(A.xbufs), xu = lv / static_cast<uint32_t>(A.xbufs);
       if (xu > 0) mbar_wait(&x_empty[xb], (xu - 1) & 1u);
       T* xs = xbuf + xb * dx;
       const T* xv = A.X + v * A.ldx;
@@ -522,7 +523,8 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     uint32_t rg = 0;  // running index of refinement rows through the ring (all tail threads agree)
     uint32_t lv = 0;
     for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
-      const uint32_t slot = lv & 1u, su = lv >> 1, xb = lv % kXBuf, xu = lv / kXBuf;
+      const uint32_t slot = lv & 1u, su = lv >> 1, xb = lv % static_cast<uint32_t>(A.xbufs),
+                     xu = lv / static_cast<uint32_t>(A.xbufs);
       T* means = scratch + slot * slot_elems;
       T* mus = means + A.K * A.m_pad;
       mbar_wait(&m_full[slot], su & 1u);
@@ -899,20 +901,24 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
 // ------------------------------------------------------------- launching --
 template <typename T>
 int stream_grid_size(const StreamArgs<T>& args, bool strict, int64_t B, size_t* smem_bytes, int* stages,
-                     int* stage_stride, int* rstride_out) {
+                     int* stage_stride, int* rstride_out, int* xbufs_out) {
   const int64_t stage_bytes = (args.m_pad * int64_t(sizeof(T)) < kSegBytes) ? args.m_pad * int64_t(sizeof(T)) : kSegBytes;
   const int stride = static_cast<int>((stage_bytes + 127) / 128 * 128);
   const int64_t row_bytes = args.lda * int64_t(sizeof(T));
   const int rstride = row_bytes <= kSegBytes ? static_cast<int>((row_bytes + 127) / 128 * 128) : 0;
   *rstride_out = rstride;
-  const SmemLayout L0 = smem_layout<T>(args.d, 0, stride, args.want, rstride);
+  // three x buffers when they fit next to a minimal ring, else two (d = 16384)
+  int xbufs = kXBuf;
+  if (smem_layout<T>(args.d, 2, stride, args.want, rstride, xbufs).total > static_cast<size_t>(kSmemBudget)) xbufs = 2;
+  *xbufs_out = xbufs;
+  const SmemLayout L0 = smem_layout<T>(args.d, 0, stride, args.want, rstride, xbufs);
   int S = static_cast<int>((kSmemBudget - static_cast<int64_t>(L0.total) - 1024) / stride);
   // ~64 KiB in flight per SM is enough (profiles/r01_stream_stages.txt: 3-5 x 16 KiB stages beat 10)
   S = std::min(S, std::max(4, static_cast<int>(kInflightBytes / stride)));
   if (const char* e = std::getenv("FSTG_STREAM_STAGES")) S = std::min(S, std::max(2, std::atoi(e)));  // experiments
   if (S > kMaxStages) S = kMaxStages;
   if (S < 2) S = 2;
-  const SmemLayout L = smem_layout<T>(args.d, S, stride, args.want, rstride);
+  const SmemLayout L = smem_layout<T>(args.d, S, stride, args.want, rstride, xbufs);
   *smem_bytes = L.total;
   *stages = S;
   *stage_stride = stride;
@@ -941,7 +947,7 @@ static cudaError_t launch_one(const StreamArgs<T>& args, int grid, size_t smem, 
 
 template <typename T>
 cudaError_t launch_stream(const StreamArgs<T>& args, bool strict, int grid, cudaStream_t st) {
-  const SmemLayout L = smem_layout<T>(args.d, args.stages, args.stage_stride, args.want, args.rstride);
+  const SmemLayout L = smem_layout<T>(args.d, args.stages, args.stage_stride, args.want, args.rstride, args.xbufs);
   if (L.total > static_cast<size_t>(kSmemBudget)) return cudaErrorInvalidConfiguration;
   if (args.nseg <= 1) {
     return strict ? launch_one<T, true, 1>(args, grid, L.total, st) : launch_one<T, false, 1>(args, grid, L.total, st);
@@ -954,8 +960,8 @@ cudaError_t launch_stream(const StreamArgs<T>& args, bool strict, int grid, cuda
 
 template cudaError_t launch_stream<float>(const StreamArgs<float>&, bool, int, cudaStream_t);
 template cudaError_t launch_stream<double>(const StreamArgs<double>&, bool, int, cudaStream_t);
-template int stream_grid_size<float>(const StreamArgs<float>&, bool, int64_t, size_t*, int*, int*, int*);
-template int stream_grid_size<double>(const StreamArgs<double>&, bool, int64_t, size_t*, int*, int*, int*);
+template int stream_grid_size<float>(const StreamArgs<float>&, bool, int64_t, size_t*, int*, int*, int*, int*);
+template int stream_grid_size<double>(const StreamArgs<double>&, bool, int64_t, size_t*, int*, int*, int*, int*);
 template int64_t stream_scratch_elems<float>(const StreamArgs<float>&, int);
 template int64_t stream_scratch_elems<double>(const StreamArgs<double>&, int);
 

@@ -91,6 +91,7 @@ EXPORTED = [
     "fstg_draw_samples", "fstg_transform_batch", "fstg_transform_with_samples_batch", "fstg_profile_enable",
     "fstg_profile_reset", "fstg_profile_read", "fstg_launch_count", "fstg_gen_gaussian",
     "fstg_gen_sparse_targets", "fstg_save", "fstg_load", "fstg_gen_mixture_targets",
+    "fstg_preprocess_design", "fstg_sample_columns", "fstg_transform_gathered_batch",
 ]
 
 
@@ -324,6 +325,45 @@ def preprocess(a, device: int = 0, stream: Optional[int] = None) -> Sketch:
     _check(lib().fstg_preprocess(_ptr(a), C.c_int(_dtype_code(dt)), C.c_int64(m), C.c_int64(n), C.c_int(device),
                                  C.c_void_p(stream), C.byref(h)))
     return Sketch(h.value)
+
+
+def preprocess_design(a, device: int = 0, stream: Optional[int] = None) -> Sketch:
+    """Design-only sketch (embedded A + Kerdock tables, no columns) for n whose sketch cannot exist."""
+    a = a.contiguous() if _is_torch(a) else np.ascontiguousarray(a)
+    m, n = tuple(a.shape)
+    h = C.c_void_p()
+    _check(lib().fstg_preprocess_design(_ptr(a), C.c_int(_dtype_code(a.dtype)), C.c_int64(m), C.c_int64(n),
+                                        C.c_int(device), C.c_void_p(stream), C.byref(h)))
+    return Sketch(h.value)
+
+
+def sample_columns(sk: Sketch, indices, out=None, stream: Optional[int] = None):
+    """Retain-sampled preprocessing: columns A s_ell for the given indices, (count, column_stride)."""
+    if not _is_torch(indices):
+        indices = np.ascontiguousarray(indices, dtype=np.int64).ravel()
+    count = int(indices.numel() if _is_torch(indices) else indices.size)
+    if out is None:
+        out = np.zeros((count, sk.column_stride), dtype=sk.dtype)
+    _check(lib().fstg_sample_columns(sk.handle, _ptr(indices), C.c_int64(count), _ptr(out), C.c_void_p(stream)))
+    return out
+
+
+def transform_gathered_batch(sk: Sketch, X, p: StreamParams, indices, gathered, *, candidates: bool = False,
+                             mu: bool = False, out: Optional[BatchResult] = None,
+                             stream: Optional[int] = None) -> BatchResult:
+    """transform_with_samples with drawn.use_gathered (stream.hpp:235-236): columns from `gathered`
+    (device tensor, B*J*K x column_stride), indices (B x J*K) for the coefficients."""
+    X = _prep_x(sk, X)
+    B = X.shape[0]
+    p.validate()
+    want = candidate_count(p.s, p.widen, sk.m)
+    if out is None:
+        out = _alloc_outputs(_is_torch(X) and X.is_cuda, B, want, sk.m, sk.dtype, candidates, mu, sk.device)
+    pc = p._c()
+    _check(lib().fstg_transform_gathered_batch(sk.handle, _ptr(X), C.c_int64(B), C.byref(pc), _ptr(indices),
+                                               _ptr(gathered), _ptr(out.counts), _ptr(out.support), _ptr(out.values),
+                                               _ptr(out.candidates), _ptr(out.mu), C.c_void_p(stream)))
+    return out
 
 
 def preprocess_shard(a, basis_begin: int, basis_end: int, include_identity: bool, device: int = 0,

@@ -1,0 +1,123 @@
+"""Retain-sampled preprocessing (design-only sketches, fstg_sample_columns) and
+the gathered-column transform (stream.hpp:184-191, 235-236) — the path that
+makes config 4 (n = 16384, 8.8 TB sketch) computable. GPU."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fst():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2105_05879_b200 import fst
+    return fst
+
+
+def _idx(L, count, seed, extra=()):
+    rng = np.random.default_rng(seed)
+    idx = rng.integers(0, L, size=count)
+    return np.concatenate([idx, np.array(extra, dtype=np.int64), idx[:5]]).astype(np.int64)  # + duplicates
+
+
+@pytest.mark.parametrize("m,n,dtype", [(40, 256, np.float64), (33, 1000, np.float32), (7, 4096, np.float32),
+                                       (256, 256, np.float64), (5, 60, np.float32)])
+def test_sample_columns_equal_sketch_columns(fst, m, n, dtype):
+    a = np.random.default_rng(m + n).standard_normal((m, n)).astype(dtype)
+    sk = fst.preprocess(a)
+    idx = _idx(sk.L, 300, 1, extra=[0, sk.L - 1, sk.L - sk.d, sk.L - sk.d + n - 1])
+    got = fst.sample_columns(sk, idx)
+    for j, ell in enumerate(idx):
+        assert got[j, :m].tobytes() == sk.column(int(ell)).tobytes(), (j, ell)
+    des = fst.preprocess_design(a)
+    got2 = fst.sample_columns(des, idx)
+    assert got2[:, :m].tobytes() == got[:, :m].tobytes()
+    with pytest.raises(ValueError):
+        des.column(0)
+    with pytest.raises(ValueError):
+        fst.transform_batch(des, np.zeros((1, n), dtype=dtype), fst.StreamParams(epsilon=0.1, s=1, J=2, K=2))
+    with pytest.raises(IndexError):
+        fst.sample_columns(des, np.array([sk.L], dtype=np.int64))
+
+
+def test_gathered_transform_matches_sketch_and_oracle(fst, orc):
+    import torch
+    a = orc.gen_orthogonal(256, 31)
+    sk, des, ref = fst.preprocess(a), fst.preprocess_design(a), orc.preprocess(a)
+    B, J, K = 8, 60, 3
+    X = np.stack([orc.gen_exact_sparse(a, 8, orc.gen_seed(v))[0] for v in range(B)])
+    seeds = np.array([orc.stream_seed(v) for v in range(B)], dtype=np.uint64)
+    p = fst.StreamParams(epsilon=0.1, s=8, J=J, K=K)
+    idx = fst.draw_samples(sk, p, seeds=seeds)                        # (B, N)
+    cols = torch.from_numpy(fst.sample_columns(des, idx.ravel())).cuda()
+    g = fst.transform_gathered_batch(des, X, p, idx, cols, candidates=True, mu=True)
+    d = fst.transform_batch(sk, X, p, seeds=seeds, candidates=True, mu=True)
+    for v in range(B):
+        rg, rd = g.result(v), d.result(v)
+        r = orc.transform(ref, X[v], orc.StreamParams(epsilon=0.1, s=8, J=J, K=K, seed=int(seeds[v])))
+        for res in (rg, rd):
+            assert np.array_equal(res.mu, r.mu)
+            assert res.candidate_set.tolist() == r.candidate_set.tolist()
+            assert res.support.tolist() == r.support.tolist()
+            np.testing.assert_allclose(res.values, r.values, rtol=1e-12)
+
+
+@pytest.mark.parametrize("m,n", [(2048, 4096), (600, 4000), (64, 16384)])
+def test_sample_columns_many_rows_sparse_bases(fst, orc, m, n):
+    """Many row tiles -> many bases per CTA (bpc up to 256) with most bases
+    holding no request: the visited-basis walk and its sign-word prefetch."""
+    import torch
+    a = torch.randn(m, n, dtype=torch.float64, device="cuda:0", generator=torch.Generator("cuda:0").manual_seed(m))
+    a32 = a.float().contiguous()
+    des = fst.preprocess_design(a32)
+    idx = _idx(des.L, 40, m, extra=[0, 1, des.d, des.L - des.d - 1, des.L - des.d, des.L - 1])
+    got = fst.sample_columns(des, idx)[:, :m].astype(np.float64)
+    S = torch.from_numpy(orc.design_columns(des.k, n, idx)).cuda()
+    expect = (S @ a32.double().T).cpu().numpy()
+    err = np.abs(got - expect).max(axis=1)
+    scale = np.abs(expect).max(axis=1)
+    assert np.all(err <= 2e-5 * np.maximum(scale, 1.0)), (err.max(), np.argmax(err))
+
+
+def test_config4_shape_spot_check(fst, orc):
+    """n = 16384 (k = 14, the 8.8 TB design): sampled columns of a design-only
+    sketch vs A s_ell in fp64, and three vectors through the gathered transform
+    vs the oracle's draw_and_gather path on the same columns."""
+    import torch
+    from paper_2105_05879_b200 import generators
+    n = 16384
+    A64 = generators.iid_gaussian(n, 1024, "cuda:0")
+    A32 = A64.float().contiguous()
+    des = fst.preprocess_design(A32)
+    assert des.L == 134234112 and des.k == 14
+    idx = _idx(des.L, 64, 7, extra=[des.L - 1, des.L - des.d])
+    got = fst.sample_columns(des, idx)
+    S = torch.from_numpy(orc.design_columns(14, n, idx)).cuda()     # (count, n) design vectors s_ell
+    expect = (S @ A32.double().T).cpu().numpy()                       # column ell = A s_ell
+    err = np.abs(got.astype(np.float64) - expect).max(axis=1)
+    scale = np.abs(expect).max(axis=1) + 1e-30
+    assert np.all(err <= 2e-5 * np.maximum(scale, 1.0)), err.max()
+    # three vectors, J = 100, K = 2, s = 64, eps = 0.05 (config 4 parameters, shorter N)
+    prob = generators.config2_problem  # noqa: F841 (config 4 uses the same A^-1 y generator at n = 16384)
+    B = 3
+    g_seeds, st_seeds = generators.trial_seeds(11, 0, B)
+    Y = generators.sparse_targets(g_seeds, n, 64, value_kind=1)
+    lu = torch.linalg.lu_factor(A64)
+    X64 = torch.linalg.lu_solve(*lu, torch.from_numpy(Y).cuda().T).T
+    X64 = X64 / torch.linalg.vector_norm(X64, dim=1, keepdim=True)
+    X = X64.float().contiguous()
+    p = fst.StreamParams(epsilon=0.05, s=64, J=100, K=2)
+    ind = fst.draw_samples(des, p, seeds=st_seeds)
+    cols = torch.from_numpy(fst.sample_columns(des, ind.ravel())).cuda()
+    out = fst.transform_gathered_batch(des, X, p, ind, cols, candidates=True, mu=True)
+    a_host = A32.double().cpu().numpy()
+    for v in range(B):
+        gathered = cols[v * 200:(v + 1) * 200, :n].double().cpu().numpy()
+        x = X[v].double().cpu().numpy()
+        r = orc.transform_gathered(a_host, x, orc.StreamParams(epsilon=0.05, s=64, J=100, K=2), ind[v], gathered)
+        g = out.result(v)
+        np.testing.assert_allclose(g.mu, r.mu, rtol=1e-4, atol=1e-5)
+        assert g.support.tolist() == r.support.tolist()
+        np.testing.assert_allclose(g.values, r.values, rtol=1e-5)
