@@ -212,6 +212,46 @@ int fstg_transform_gathered_batch(const fstg_sketch* sk, const void* X, int64_t 
                                   const int64_t* indices, const void* gathered, int32_t* counts, int32_t* support,
                                   void* values, int32_t* candidates, void* mu, void* stream);
 
+/* ------------------------------------------------------ design verifiers --- */
+/* kerdock.hpp:198-317, cli.hpp:45-82, on the GPU (sign tables of the design
+ * expanded on `device`). All reported quantities are exact: every inner
+ * product of unit design vectors is F/d with F an integer (one integer FWHT
+ * per basis pair yields a whole cross Gram). Policies: */
+#define FSTG_VERIFY_REFERENCE 0  /* the reference's: exhaustive for k <= 6, sampled above (same seeds/draws) */
+#define FSTG_VERIFY_EXHAUSTIVE 1 /* every basis pair / every column pair for any k <= cap (k <= 14) */
+
+/* kerdock.hpp:199-208 MubReport */
+typedef struct fstg_mub_report {
+  double max_within_gram_dev; /* max |B^T B - I| over every basis */
+  double min_cross_sq;        /* extremes of squared cross-basis inner products */
+  double max_cross_sq;
+  double max_cross_dev;       /* max |<x,y>^2 - 1/d| */
+  int32_t exhaustive;         /* 0 when basis pairs were sampled */
+  int32_t reserved;
+  int64_t basis_pairs;        /* cross-basis pairs checked */
+} fstg_mub_report;
+
+/* kerdock.hpp:261-266 MomentReport */
+typedef struct fstg_moment_report {
+  double m1;
+  double m2;
+  int32_t exact;              /* 0 for the sampled estimate */
+  int32_t reserved;
+  int64_t pairs;              /* ordered column pairs summed */
+} fstg_moment_report;
+
+/* kerdock.hpp:213-256 verify_mub. k > cap -> FSTG_ERR_INVALID_ARGUMENT
+ * (the reference's invalid_argument); k > 14 -> FSTG_ERR_NOT_SUPPORTED. */
+int fstg_verify_mub(int k, int cap, int policy, int device, fstg_mub_report* out);
+/* kerdock.hpp:301-315 verify_design_moments (same errors). */
+int fstg_verify_design_moments(int k, int cap, int policy, int device, fstg_moment_report* out);
+/* kerdock.hpp:267-276 design_moment_target c_{d,k}. */
+double fstg_design_moment_target(int64_t d, int k);
+/* cli.hpp:45-60: every Kerdock matrix zero-diagonal and symmetric
+ * (*skew_symmetric = 1), and the number of basis pairs a < b whose sum is
+ * rank-deficient (must be 0). Ranks on the GPU. */
+int fstg_verify_kerdock_set(int k, int device, int* skew_symmetric, int64_t* bad_pairs);
+
 /* ------------------------------------------------------------ profiling ---- */
 /* When enabled, the library brackets each launch of its kernels with CUDA
  * events on the launching stream; fstg_profile_read returns the accumulated

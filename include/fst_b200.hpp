@@ -211,4 +211,23 @@ inline void transform_batch(const Sketch& sk, const void* X, std::int64_t B, con
   check(fstg_transform_batch(sk.handle(), X, B, &c, seeds, counts, support, values, nullptr, nullptr, stream));
 }
 
+// kerdock.hpp:198-317 design verifiers (GPU; policy FSTG_VERIFY_REFERENCE
+// reproduces the reference's reports, FSTG_VERIFY_EXHAUSTIVE checks every pair).
+using MubReport = fstg_mub_report;
+using MomentReport = fstg_moment_report;
+
+inline MubReport verify_mub(int k, int cap = 8, int policy = FSTG_VERIFY_REFERENCE, int device = 0) {
+  MubReport r{};
+  check(fstg_verify_mub(k, cap, policy, device, &r));
+  return r;
+}
+
+inline MomentReport verify_design_moments(int k, int cap = 8, int policy = FSTG_VERIFY_REFERENCE, int device = 0) {
+  MomentReport r{};
+  check(fstg_verify_design_moments(k, cap, policy, device, &r));
+  return r;
+}
+
+inline double design_moment_target(std::int64_t d, int k) { return fstg_design_moment_target(d, k); }
+
 }  // namespace fst_b200

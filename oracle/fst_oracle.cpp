@@ -9,6 +9,7 @@
 #include <cstring>
 #include <limits>
 #include <numeric>
+#include <random>
 #include <thread>
 
 namespace fst_oracle {
@@ -650,6 +651,159 @@ std::vector<double> gen_exact_sparse(const double* a, std::int64_t m, std::int64
     x_out[j] = acc;
   }
   return truth;
+}
+
+// ----------------------------------------------- kerdock.hpp:198-317 verifiers --
+
+std::vector<double> materialize_design(const DesignParams& p) {  // kerdock.hpp:160-188
+  const std::int64_t d = p.d, nk = p.kerdock_bases();
+  std::vector<double> u(static_cast<std::size_t>(d * p.L), 0.0);
+  const double scale = 1.0 / std::sqrt(static_cast<double>(d));
+  std::vector<double> sign(static_cast<std::size_t>(d));
+  for (std::int64_t s = 0; s < nk; ++s) {
+    const auto m = kerdock_matrix(p, static_cast<std::uint64_t>(s));
+    for (std::int64_t j = 0; j < d; ++j)
+      sign[j] = quadratic_form(m.data(), p.k, coords_of_position(static_cast<std::uint64_t>(j), p.k)) ? -scale : scale;
+    for (std::int64_t w = 0; w < d; ++w) {
+      double* col = u.data() + (s * d + w) * d;
+      for (std::int64_t j = 0; j < d; ++j) col[j] = (std::popcount(static_cast<std::uint64_t>(w & j)) & 1) ? -sign[j] : sign[j];
+    }
+  }
+  for (std::int64_t w = 0; w < d; ++w) u[static_cast<std::size_t>((nk * d + w) * d + w)] = 1.0;  // identity block last
+  return u;
+}
+
+namespace {
+
+// G = B1^T B2 for two d-column blocks of a column-major d x L matrix.
+void block_gram(const double* b1, const double* b2, std::int64_t d, std::vector<double>& g) {
+  g.assign(static_cast<std::size_t>(d * d), 0.0);
+  for (std::int64_t i = 0; i < d; ++i)
+    for (std::int64_t j = 0; j < d; ++j) {
+      const double* x = b1 + i * d;
+      const double* y = b2 + j * d;
+      double acc = 0;
+      for (std::int64_t t = 0; t < d; ++t) acc += x[t] * y[t];
+      g[static_cast<std::size_t>(i * d + j)] = acc;
+    }
+}
+
+}  // namespace
+
+MubReport verify_mub(const DesignParams& p, int cap) {  // kerdock.hpp:213-256
+  if (p.k > cap) throw std::invalid_argument("verify_mub: k exceeds the verification cap");
+  const std::int64_t d = p.d, nb = p.kerdock_bases() + 1;
+  const std::vector<double> u = materialize_design(p);
+  MubReport rep;
+  rep.min_cross_sq = std::numeric_limits<double>::infinity();
+  rep.max_cross_sq = -std::numeric_limits<double>::infinity();
+  std::vector<double> g;
+  for (std::int64_t b = 0; b < nb; ++b) {
+    const double* blk = u.data() + b * d * d;
+    block_gram(blk, blk, d, g);
+    for (std::int64_t i = 0; i < d; ++i)
+      for (std::int64_t j = 0; j < d; ++j)
+        rep.max_within_gram_dev =
+            std::max(rep.max_within_gram_dev, std::abs(g[static_cast<std::size_t>(i * d + j)] - (i == j ? 1.0 : 0.0)));
+  }
+  auto check_cross = [&](std::int64_t b, std::int64_t b2) {
+    block_gram(u.data() + b * d * d, u.data() + b2 * d * d, d, g);
+    for (const double c : g) {
+      const double sq = c * c;
+      rep.min_cross_sq = std::min(rep.min_cross_sq, sq);
+      rep.max_cross_sq = std::max(rep.max_cross_sq, sq);
+      rep.max_cross_dev = std::max(rep.max_cross_dev, std::abs(sq - 1.0 / static_cast<double>(d)));
+    }
+  };
+  if (p.k <= 6) {
+    for (std::int64_t b = 0; b < nb; ++b)
+      for (std::int64_t b2 = b + 1; b2 < nb; ++b2) check_cross(b, b2);
+  } else {
+    rep.exhaustive = false;
+    std::mt19937_64 rng(0x6d7562u);  // the reference's fixed seed
+    for (int i = 0; i < 256; ++i) {
+      const auto b = static_cast<std::int64_t>(rng() % static_cast<std::uint64_t>(nb));
+      auto b2 = static_cast<std::int64_t>(rng() % static_cast<std::uint64_t>(nb - 1));
+      if (b2 >= b) ++b2;
+      check_cross(b, b2);
+    }
+  }
+  if (!std::isfinite(rep.min_cross_sq)) rep.min_cross_sq = rep.max_cross_sq = 0;
+  return rep;
+}
+
+double design_moment_target(std::int64_t d, int k) {  // kerdock.hpp:267-276
+  double num = 1, den = 1;
+  for (int i = 0; i < k; ++i) {
+    num *= static_cast<double>(2 * i + 1);
+    den *= static_cast<double>(d + 2 * i);
+  }
+  return num / den;
+}
+
+MomentReport design_moments_of(const double* u, std::int64_t d, std::int64_t L) {  // kerdock.hpp:280-297
+  MomentReport rep;
+  double sum2 = 0, sum4 = 0;
+  for (std::int64_t a = 0; a < L; ++a)
+    for (std::int64_t b = 0; b < L; ++b) {
+      const double* x = u + a * d;
+      const double* y = u + b * d;
+      double ip = 0;
+      for (std::int64_t t = 0; t < d; ++t) ip += x[t] * y[t];
+      const double sq = ip * ip;
+      sum2 += sq;
+      sum4 += sq * sq;
+    }
+  const double pairs = static_cast<double>(L) * static_cast<double>(L);
+  rep.m1 = sum2 / pairs;
+  rep.m2 = sum4 / pairs;
+  return rep;
+}
+
+MomentReport verify_design_moments(const DesignParams& p, int cap) {  // kerdock.hpp:301-315
+  if (p.k > cap) throw std::invalid_argument("verify_design_moments: k exceeds the verification cap");
+  const std::vector<double> u = materialize_design(p);
+  if (p.k <= 6) return design_moments_of(u.data(), p.d, p.L);
+  MomentReport rep;
+  rep.exact = false;
+  std::mt19937_64 rng(0x6d6f6du);
+  const int samples = 4'000'000;
+  double sum2 = 0, sum4 = 0;
+  for (int i = 0; i < samples; ++i) {
+    const auto a = static_cast<std::int64_t>(rng() % static_cast<std::uint64_t>(p.L));
+    const auto b = static_cast<std::int64_t>(rng() % static_cast<std::uint64_t>(p.L));
+    const double* x = u.data() + a * p.d;
+    const double* y = u.data() + b * p.d;
+    double ip = 0;
+    for (std::int64_t t = 0; t < p.d; ++t) ip += x[t] * y[t];
+    const double sq = ip * ip;
+    sum2 += sq;
+    sum4 += sq * sq;
+  }
+  rep.m1 = sum2 / samples;
+  rep.m2 = sum4 / samples;
+  return rep;
+}
+
+void verify_kerdock_set(const DesignParams& p, bool* skew, std::int64_t* bad_pairs) {  // cli.hpp:45-60
+  const std::int64_t nk = p.kerdock_bases();
+  std::vector<std::vector<std::uint64_t>> mats(static_cast<std::size_t>(nk));
+  bool ok = true;
+  for (std::int64_t s = 0; s < nk; ++s) {
+    mats[s] = kerdock_matrix(p, static_cast<std::uint64_t>(s));
+    for (int i = 0; i < p.k && ok; ++i) ok = ((mats[s][i] >> i) & 1) == 0;
+    for (int i = 0; i < p.k && ok; ++i)
+      for (int j = 0; j < p.k && ok; ++j) ok = ((mats[s][i] >> j) & 1) == ((mats[s][j] >> i) & 1);
+  }
+  std::int64_t bad = 0;
+  std::vector<std::uint64_t> sum(static_cast<std::size_t>(p.k));
+  for (std::int64_t a = 0; a < nk; ++a)
+    for (std::int64_t b = a + 1; b < nk; ++b) {
+      for (int i = 0; i < p.k; ++i) sum[i] = mats[a][i] ^ mats[b][i];
+      if (gf2_rank(sum.data(), p.k) != p.k) ++bad;
+    }
+  *skew = ok;
+  *bad_pairs = bad;
 }
 
 }  // namespace fst_oracle

@@ -176,6 +176,39 @@ TransformResult<double> transform_gathered(const double* a, std::int64_t m, std:
                                            const StreamParams& p, const std::vector<std::int64_t>& indices,
                                            const double* gathered);
 
+// ----------------------------------------------- kerdock.hpp:198-317 verifiers --
+
+/// kerdock.hpp:160-188 (detail::materialize_design): all L unit design vectors
+/// as a column-major d x L matrix (column c at c*d), Kerdock blocks first.
+std::vector<double> materialize_design(const DesignParams& p);
+
+/// kerdock.hpp:199-208
+struct MubReport {
+  double max_within_gram_dev = 0;
+  double min_cross_sq = 0;
+  double max_cross_sq = 0;
+  double max_cross_dev = 0;
+  bool exhaustive = true;
+  bool pass(double tol) const { return max_within_gram_dev <= tol && max_cross_dev <= tol; }
+};
+/// kerdock.hpp:213-256 (exhaustive for k <= 6, 256 sampled basis pairs above).
+MubReport verify_mub(const DesignParams& p, int cap = 8);
+
+/// kerdock.hpp:261-278
+struct MomentReport {
+  double m1 = 0;
+  double m2 = 0;
+  bool exact = true;
+};
+double design_moment_target(std::int64_t d, int k);
+/// kerdock.hpp:280-297 — u column-major d x L.
+MomentReport design_moments_of(const double* u, std::int64_t d, std::int64_t L);
+/// kerdock.hpp:301-315 (exact for k <= 6, 4M sampled pairs above).
+MomentReport verify_design_moments(const DesignParams& p, int cap = 8);
+/// cli.hpp:45-60: zero-diagonal symmetric matrices, number of basis pairs whose
+/// sum is rank-deficient (must be 0 for a Kerdock set).
+void verify_kerdock_set(const DesignParams& p, bool* skew, std::int64_t* bad_pairs);
+
 // --------------------------------------------------------- generators.hpp --
 
 /// generators.hpp:20-33 — Haar orthogonal: Householder QR of a SeededRng

@@ -12,6 +12,8 @@ import os
 import subprocess
 from dataclasses import dataclass, field
 
+from typing import NamedTuple
+
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -68,6 +70,8 @@ def lib():
         _lib.orc_sketch_columns.restype = C.c_void_p
         _lib.orc_sketch_columns.argtypes = [C.c_void_p]
         _lib.orc_sketch_free.argtypes = [C.c_void_p]
+        _lib.orc_design_moment_target.restype = C.c_double
+        _lib.orc_design_moment_target.argtypes = [C.c_int64, C.c_int]
     return _lib
 
 
@@ -471,3 +475,64 @@ def gen_exact_sparse(a: np.ndarray, s: int, seed: int):
     _check(lib().orc_gen_exact_sparse(_ptr(a), C.c_int64(m), C.c_int64(n), C.c_int64(s), C.c_uint64(seed),
                                       _ptr(x), _ptr(truth)))
     return x, truth
+
+
+# ---- design verifiers (kerdock.hpp:198-317, cli.hpp:45-60) ----
+class MubReport(NamedTuple):
+    max_within_gram_dev: float
+    min_cross_sq: float
+    max_cross_sq: float
+    max_cross_dev: float
+    exhaustive: bool
+
+    def passed(self, tol: float) -> bool:
+        return self.max_within_gram_dev <= tol and self.max_cross_dev <= tol
+
+
+class MomentReport(NamedTuple):
+    m1: float
+    m2: float
+    exact: bool
+
+
+def materialize_design(k: int) -> np.ndarray:
+    """(L, d): row c = unit design vector u_c (the reference's d x L columns)."""
+    d = 1 << k
+    L = d * (d // 2 + 1)
+    out = np.zeros((L, d), dtype=np.float64)
+    _check(lib().orc_materialize_design(C.c_int(k), _ptr(out)))
+    return out
+
+
+def verify_mub(k: int, cap: int = 8) -> MubReport:
+    out = np.zeros(4)
+    ex = C.c_int()
+    _check(lib().orc_verify_mub(C.c_int(k), C.c_int(cap), _ptr(out), C.byref(ex)))
+    return MubReport(*[float(v) for v in out], bool(ex.value))
+
+
+def verify_design_moments(k: int, cap: int = 8) -> MomentReport:
+    out = np.zeros(2)
+    ex = C.c_int()
+    _check(lib().orc_verify_design_moments(C.c_int(k), C.c_int(cap), _ptr(out), C.byref(ex)))
+    return MomentReport(float(out[0]), float(out[1]), bool(ex.value))
+
+
+def design_moments_of(u) -> MomentReport:
+    """u: (L, d) rows = columns of the reference's d x L matrix."""
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.zeros(2)
+    _check(lib().orc_design_moments_of(_ptr(u), C.c_int64(u.shape[1]), C.c_int64(u.shape[0]), _ptr(out)))
+    return MomentReport(float(out[0]), float(out[1]), True)
+
+
+def design_moment_target(d: int, k: int) -> float:
+    return float(lib().orc_design_moment_target(C.c_int64(d), C.c_int(k)))
+
+
+def verify_kerdock_set(k: int):
+    """(skew-symmetric with zero diagonal, rank-deficient pair count)."""
+    skew = C.c_int()
+    bad = C.c_int64()
+    _check(lib().orc_verify_kerdock_set(C.c_int(k), C.byref(skew), C.byref(bad)))
+    return bool(skew.value), int(bad.value)

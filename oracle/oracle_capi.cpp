@@ -510,4 +510,45 @@ int orc_gen_exact_sparse(const double* a, std::int64_t m, std::int64_t n, std::i
   });
 }
 
+// ---- design verifiers (kerdock.hpp:198-317, cli.hpp:45-60) ----
+int orc_materialize_design(int k, double* out) {
+  return guarded([&] {
+    const auto u = materialize_design(DesignParams::make(k));
+    std::memcpy(out, u.data(), sizeof(double) * u.size());
+  });
+}
+int orc_verify_mub(int k, int cap, double* out4, int* exhaustive) {
+  return guarded([&] {
+    const MubReport r = verify_mub(DesignParams::make(k), cap);
+    out4[0] = r.max_within_gram_dev;
+    out4[1] = r.min_cross_sq;
+    out4[2] = r.max_cross_sq;
+    out4[3] = r.max_cross_dev;
+    *exhaustive = r.exhaustive ? 1 : 0;
+  });
+}
+int orc_verify_design_moments(int k, int cap, double* out2, int* exact) {
+  return guarded([&] {
+    const MomentReport r = verify_design_moments(DesignParams::make(k), cap);
+    out2[0] = r.m1;
+    out2[1] = r.m2;
+    *exact = r.exact ? 1 : 0;
+  });
+}
+int orc_design_moments_of(const double* u, std::int64_t d, std::int64_t L, double* out2) {
+  return guarded([&] {
+    const MomentReport r = design_moments_of(u, d, L);
+    out2[0] = r.m1;
+    out2[1] = r.m2;
+  });
+}
+double orc_design_moment_target(std::int64_t d, int k) { return design_moment_target(d, k); }
+int orc_verify_kerdock_set(int k, int* skew, std::int64_t* bad_pairs) {
+  return guarded([&] {
+    bool ok = false;
+    verify_kerdock_set(DesignParams::make(k), &ok, bad_pairs);
+    *skew = ok ? 1 : 0;
+  });
+}
+
 }  // extern "C"

@@ -9,8 +9,10 @@
 #include <cstdlib>
 #include <cstring>
 #include <filesystem>
+#include <limits>
 #include <map>
 #include <mutex>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -949,6 +951,223 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   }
 }
 
+// ----------------------------------------------------- design verifiers ----
+// kerdock.hpp:198-317 / cli.hpp:45-60 on the GPU (verify.cu). Inner products
+// are F/d with integer F, so every report field is assembled exactly from the
+// integer statistics the kernels return.
+using u128 = unsigned __int128;
+
+u128 get_u128(const unsigned long long* v) { return (static_cast<u128>(v[1]) << 64) | v[0]; }
+
+// num / den for a power-of-two den, exact whenever the quotient and the
+// remainder fit a double's mantissa (always, for a valid design).
+double exact_ratio(u128 num, u128 den) {
+  const u128 q = num / den, r = num % den;
+  return static_cast<double>(q) + static_cast<double>(r) / static_cast<double>(den);
+}
+
+struct VerifyTables {
+  Design D;
+  DevBuf revtab, qplain;
+};
+
+void verify_prologue(int k, int cap, int policy, int device, const char* who, VerifyTables& t, cudaStream_t st) {
+  t.D = Design::make(k);
+  if (k > cap) throw InvalidArgument(std::string(who) + ": k exceeds the verification cap");
+  if (policy != FSTG_VERIFY_REFERENCE && policy != FSTG_VERIFY_EXHAUSTIVE)
+    throw InvalidArgument(std::string(who) + ": unknown policy");
+  if (k > 14) throw NotSupported(std::string(who) + ": k > 14 is not supported on the GPU path");
+  require_device(device);
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  const std::vector<uint32_t> rev = reversed_row_table(t.D);
+  const int64_t nk = t.D.kerdock_bases(), wpb = t.D.d >= 32 ? t.D.d / 32 : 1;
+  t.revtab = DevBuf(rev.size() * 4, st);
+  t.qplain = DevBuf(size_t(nk) * wpb * 4, st);
+  cuda_check(cudaMemcpyAsync(t.revtab.p, rev.data(), rev.size() * 4, cudaMemcpyHostToDevice, st), "upload tables");
+  ProfScope ps("qtables", st);
+  cuda_check(launch_qtables(t.revtab.as<uint32_t>(), k, nk, t.qplain.as<uint32_t>(), nullptr, st), "qtable kernel");
+}
+
+struct PairStats {
+  u128 x2w = 0, x4w = 0, x2c = 0, x4c = 0;
+  int bad = 0, f2min = INT32_MAX, f2max = 0;
+};
+
+// Basis pairs through the integer FWHT kernel; pairs == empty -> the whole upper triangle.
+PairStats run_pairs(const VerifyTables& t, const std::vector<int32_t>& pb, const std::vector<int32_t>& pb2,
+                    cudaStream_t st) {
+  const int64_t nk = t.D.kerdock_bases();
+  const bool all = pb.empty();
+  const int64_t npairs = all ? nk * (nk + 1) / 2 : static_cast<int64_t>(pb.size());
+  DevBuf acc(8 * 8, st), stats(3 * 4, st), dpb, dpb2;
+  const int init[3] = {0, INT32_MAX, 0};
+  cuda_check(cudaMemsetAsync(acc.p, 0, 64, st), "memset");
+  cuda_check(cudaMemcpyAsync(stats.p, init, sizeof(init), cudaMemcpyHostToDevice, st), "H2D");
+  if (!all) {
+    dpb = DevBuf(pb.size() * 4, st);
+    dpb2 = DevBuf(pb.size() * 4, st);
+    cuda_check(cudaMemcpyAsync(dpb.p, pb.data(), pb.size() * 4, cudaMemcpyHostToDevice, st), "H2D pairs");
+    cuda_check(cudaMemcpyAsync(dpb2.p, pb2.data(), pb.size() * 4, cudaMemcpyHostToDevice, st), "H2D pairs");
+  }
+  {
+    ProfScope ps("verify_pairs", st);
+    cuda_check(launch_verify_pairs(t.D.k, t.qplain.as<uint32_t>(), nk, npairs, dpb.as<int32_t>(), dpb2.as<int32_t>(),
+                                   acc.as<unsigned long long>(), stats.as<int>(), st),
+               "verify pairs kernel");
+  }
+  unsigned long long h[8];
+  int hs[3];
+  cuda_check(cudaMemcpyAsync(h, acc.p, 64, cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaMemcpyAsync(hs, stats.p, 12, cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+  PairStats r;
+  r.x2w = get_u128(h);
+  r.x4w = get_u128(h + 2);
+  r.x2c = get_u128(h + 4);
+  r.x4c = get_u128(h + 6);
+  r.bad = hs[0];
+  r.f2min = hs[1];
+  r.f2max = hs[2];
+  return r;
+}
+
+void verify_mub_impl(int k, int cap, int policy, int device, fstg_mub_report* out) {
+  if (!out) throw InvalidArgument("verify_mub: null report");
+  cudaStream_t st = nullptr;
+  VerifyTables t;
+  verify_prologue(k, cap, policy, device, "verify_mub", t, st);
+  const int64_t d = t.D.d, nk = t.D.kerdock_bases(), nb = nk + 1;
+  const bool exhaustive = policy == FSTG_VERIFY_EXHAUSTIVE || k <= 6;
+  std::vector<int32_t> pb, pb2;
+  int64_t identity_pairs = 0, cross_pairs = 0;
+  if (exhaustive) {
+    identity_pairs = nk;  // (b, identity) for every Kerdock b
+    cross_pairs = nb * (nb - 1) / 2;
+  } else {
+    for (int64_t b = 0; b < nk; ++b) {  // within-basis Gram of every basis (kerdock.hpp:223-227)
+      pb.push_back(static_cast<int32_t>(b));
+      pb2.push_back(static_cast<int32_t>(b));
+    }
+    std::mt19937_64 rng(0x6d7562u);  // kerdock.hpp:245: fixed-seed basis-pair sample
+    for (int i = 0; i < 256; ++i) {
+      const auto b = static_cast<int64_t>(rng() % static_cast<uint64_t>(nb));
+      auto b2 = static_cast<int64_t>(rng() % static_cast<uint64_t>(nb - 1));
+      if (b2 >= b) ++b2;
+      ++cross_pairs;
+      if (b == nk || b2 == nk) {
+        ++identity_pairs;
+      } else {
+        pb.push_back(static_cast<int32_t>(std::min(b, b2)));  // F is symmetric in the pair
+        pb2.push_back(static_cast<int32_t>(std::max(b, b2)));
+      }
+    }
+  }
+  const PairStats ps = run_pairs(t, pb, pb2, st);
+  const double dd = static_cast<double>(d), inv_d = 1.0 / dd;
+  fstg_mub_report r{};
+  r.max_within_gram_dev = static_cast<double>(ps.bad) / dd;  // identity block: I^T I - I = 0
+  double lo = std::numeric_limits<double>::infinity(), hi = -std::numeric_limits<double>::infinity();
+  if (ps.f2max > 0 || ps.f2min != INT32_MAX) {
+    lo = static_cast<double>(ps.f2min) / (dd * dd);
+    hi = static_cast<double>(ps.f2max) / (dd * dd);
+  }
+  if (identity_pairs > 0) {  // e_pos . u_{s,w} = +-2^(-k/2): squared exactly 1/d
+    lo = std::min(lo, inv_d);
+    hi = std::max(hi, inv_d);
+  }
+  if (!std::isfinite(lo)) lo = hi = 0;
+  r.min_cross_sq = lo;
+  r.max_cross_sq = hi;
+  r.max_cross_dev = cross_pairs > 0 ? std::max(std::abs(lo - inv_d), std::abs(hi - inv_d)) : 0.0;
+  r.exhaustive = exhaustive ? 1 : 0;
+  r.basis_pairs = cross_pairs;
+  *out = r;
+}
+
+void verify_moments_impl(int k, int cap, int policy, int device, fstg_moment_report* out) {
+  if (!out) throw InvalidArgument("verify_design_moments: null report");
+  cudaStream_t st = nullptr;
+  VerifyTables t;
+  verify_prologue(k, cap, policy, device, "verify_design_moments", t, st);
+  const int64_t d = t.D.d, nk = t.D.kerdock_bases(), L = t.D.L;
+  const u128 ud = static_cast<u128>(d);
+  fstg_moment_report r{};
+  if (policy == FSTG_VERIFY_EXHAUSTIVE || k <= 6) {
+    // sum over ordered column pairs: Kerdock x Kerdock blocks from the FWHT
+    // (sum_{w,w'} (F[w^w']/d)^2 = sum_u F^2 / d, ^4: sum_u F^4 / d^3), both
+    // orders of every cross pair; identity x identity = d ones; identity x
+    // Kerdock (both orders) = 2 d^2 entries of 1/d (and 1/d^2 for ^4).
+    const PairStats ps = run_pairs(t, {}, {}, st);
+    const u128 n2 = ps.x2w + 2 * ps.x2c + (ud + 2 * static_cast<u128>(nk) * ud) * ud;
+    const u128 n4 = ps.x4w + 2 * ps.x4c + (ud + 2 * static_cast<u128>(nk)) * ud * ud * ud;
+    const double pairs = static_cast<double>(L) * static_cast<double>(L);
+    r.m1 = exact_ratio(n2, ud) / pairs;
+    r.m2 = exact_ratio(n4, ud * ud * ud) / pairs;
+    r.exact = 1;
+    r.pairs = L * L;
+  } else {
+    const int samples = 4'000'000;  // kerdock.hpp:305-313, same engine, seed and draw order
+    std::vector<int64_t> ia(samples), ib(samples);
+    std::mt19937_64 rng(0x6d6f6du);
+    for (int i = 0; i < samples; ++i) {
+      ia[i] = static_cast<int64_t>(rng() % static_cast<uint64_t>(L));
+      ib[i] = static_cast<int64_t>(rng() % static_cast<uint64_t>(L));
+    }
+    DevBuf da(size_t(samples) * 8, st), db(size_t(samples) * 8, st), acc(4 * 8, st);
+    cuda_check(cudaMemcpyAsync(da.p, ia.data(), size_t(samples) * 8, cudaMemcpyHostToDevice, st), "H2D samples");
+    cuda_check(cudaMemcpyAsync(db.p, ib.data(), size_t(samples) * 8, cudaMemcpyHostToDevice, st), "H2D samples");
+    cuda_check(cudaMemsetAsync(acc.p, 0, 32, st), "memset");
+    {
+      ProfScope ps("verify_samples", st);
+      cuda_check(launch_verify_samples(k, t.qplain.as<uint32_t>(), da.as<int64_t>(), db.as<int64_t>(), samples,
+                                       acc.as<unsigned long long>(), st),
+                 "verify samples kernel");
+    }
+    unsigned long long h[4];
+    cuda_check(cudaMemcpyAsync(h, acc.p, 32, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "sync");
+    // sum2 = sum F^2 / d^2, sum4 = sum F^4 / d^4 (each sampled term exact)
+    r.m1 = exact_ratio(get_u128(h), ud * ud) / samples;
+    r.m2 = exact_ratio(get_u128(h + 2), ud * ud * ud * ud) / samples;
+    r.exact = 0;
+    r.pairs = samples;
+  }
+  *out = r;
+}
+
+void verify_kerdock_set_impl(int k, int device, int* skew, int64_t* bad_pairs) {
+  if (!skew || !bad_pairs) throw InvalidArgument("verify_kerdock_set: null output");
+  const Design D = Design::make(k);
+  if (k > 14) throw NotSupported("verify_kerdock_set: k > 14 is not supported on the GPU path");
+  require_device(device);
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cudaStream_t st = nullptr;
+  const Field f(D.k - 1, D.modulus);
+  const int64_t nk = D.kerdock_bases();
+  std::vector<uint32_t> rows(size_t(nk) * k);
+  bool ok = true;
+  for (int64_t s = 0; s < nk; ++s) {
+    const auto m = kerdock_matrix(D, f, static_cast<uint64_t>(s));
+    for (int i = 0; i < k; ++i) {
+      rows[size_t(s) * k + i] = static_cast<uint32_t>(m[i]);
+      ok = ok && ((m[i] >> i) & 1) == 0;
+      for (int j = 0; j < k; ++j) ok = ok && ((m[i] >> j) & 1) == ((m[j] >> i) & 1);
+    }
+  }
+  DevBuf drows(rows.size() * 4, st), bad(8, st);
+  cuda_check(cudaMemcpyAsync(drows.p, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice, st), "H2D rows");
+  cuda_check(cudaMemsetAsync(bad.p, 0, 8, st), "memset");
+  {
+    ProfScope ps("verify_ranks", st);
+    cuda_check(launch_verify_ranks(k, drows.as<uint32_t>(), nk, bad.as<unsigned long long>(), st), "rank kernel");
+  }
+  unsigned long long h = 0;
+  cuda_check(cudaMemcpyAsync(&h, bad.p, 8, cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+  *skew = ok ? 1 : 0;
+  *bad_pairs = static_cast<int64_t>(h);
+}
+
 }  // namespace
 
 // ====================================================================== ABI ==
@@ -1237,6 +1456,27 @@ int fstg_profile_read(const char* name, double* ms, int64_t* launches) {
 int fstg_launch_count(int64_t* launches) {
   if (launches) *launches = g_launches.load();
   return FSTG_OK;
+}
+
+int fstg_verify_mub(int k, int cap, int policy, int device, fstg_mub_report* out) {
+  return guarded([&] { verify_mub_impl(k, cap, policy, device, out); });
+}
+
+int fstg_verify_design_moments(int k, int cap, int policy, int device, fstg_moment_report* out) {
+  return guarded([&] { verify_moments_impl(k, cap, policy, device, out); });
+}
+
+double fstg_design_moment_target(int64_t d, int k) {  // kerdock.hpp:267-276
+  double num = 1, den = 1;
+  for (int i = 0; i < k; ++i) {
+    num *= static_cast<double>(2 * i + 1);
+    den *= static_cast<double>(d + 2 * i);
+  }
+  return num / den;
+}
+
+int fstg_verify_kerdock_set(int k, int device, int* skew_symmetric, int64_t* bad_pairs) {
+  return guarded([&] { verify_kerdock_set_impl(k, device, skew_symmetric, bad_pairs); });
 }
 
 }  // extern "C"

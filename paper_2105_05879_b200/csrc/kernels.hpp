@@ -1,4 +1,4 @@
-// Launch wrappers of the sm_100a kernels (preprocess.cu, draw.cu, stream.cu).
+// Launch wrappers of the sm_100a kernels (preprocess.cu, draw.cu, stream.cu, verify.cu).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -24,6 +24,19 @@ cudaError_t launch_identity(const T* a, int64_t lda, int64_t m, int64_t n, int64
                             int64_t ldc, cudaStream_t st);
 template <typename T>
 cudaError_t launch_row_norms(const T* a, int64_t lda, int64_t m, int64_t n, double* out, cudaStream_t st);
+
+// ---- design verifiers (verify.cu) ----
+// Per basis pair (explicit list, or pb == nullptr: the upper triangle incl.
+// the diagonal) the d-point integer FWHT of (-1)^(Q_b + Q_b2): acc (8 u64 =
+// 4 u128) += {sum F^2 within, sum F^4 within, sum F^2 cross, sum F^4 cross};
+// stats = {max |F - d delta| within, min F^2 cross, max F^2 cross}.
+cudaError_t launch_verify_pairs(int k, const uint32_t* qplain, int64_t nk, int64_t npairs, const int32_t* pb,
+                                const int32_t* pb2, unsigned long long* acc, int* stats, cudaStream_t st);
+// Sampled column pairs (ia[i], ib[i]): acc (4 u64) += {sum F^2, sum F^4}, F = d <u_a, u_b>.
+cudaError_t launch_verify_samples(int k, const uint32_t* qplain, const int64_t* ia, const int64_t* ib, int64_t count,
+                                  unsigned long long* acc, cudaStream_t st);
+// Pairs a < b of Kerdock matrices (nk x k row words) whose sum has rank < k.
+cudaError_t launch_verify_ranks(int k, const uint32_t* rows, int64_t nk, unsigned long long* bad, cudaStream_t st);
 
 // ---- draws (draw.cu) ----
 template <typename IdxT>

@@ -92,6 +92,7 @@ EXPORTED = [
     "fstg_profile_reset", "fstg_profile_read", "fstg_launch_count", "fstg_gen_gaussian",
     "fstg_gen_sparse_targets", "fstg_save", "fstg_load", "fstg_gen_mixture_targets",
     "fstg_preprocess_design", "fstg_sample_columns", "fstg_transform_gathered_batch",
+    "fstg_verify_mub", "fstg_verify_design_moments", "fstg_design_moment_target", "fstg_verify_kerdock_set",
 ]
 
 
@@ -109,6 +110,8 @@ def lib():
         L.fstg_candidate_count.argtypes = [C.c_int64, C.c_int64, C.c_int64]
         L.fstg_destroy.argtypes = [C.c_void_p]
         L.fstg_destroy.restype = None
+        L.fstg_design_moment_target.restype = C.c_double
+        L.fstg_design_moment_target.argtypes = [C.c_int64, C.c_int]
         _lib = L
     return _lib
 
@@ -500,6 +503,73 @@ def transform_with_samples(sk: Sketch, x, p: StreamParams, indices) -> Transform
     r = transform_with_samples_batch(sk, x.reshape(1, -1), p, np.asarray(indices, dtype=np.int64).reshape(1, -1),
                                      candidates=True, mu=True)
     return r.result(0, p.J * p.K)
+
+
+# ------------------------------------------------------- design verifiers ----
+VERIFY_REFERENCE = 0   # the reference's policy: exhaustive for k <= 6, sampled above (same seeds)
+VERIFY_EXHAUSTIVE = 1  # every basis pair / every column pair, any k <= cap
+
+
+class _MubReport(C.Structure):
+    _fields_ = [("max_within_gram_dev", C.c_double), ("min_cross_sq", C.c_double), ("max_cross_sq", C.c_double),
+                ("max_cross_dev", C.c_double), ("exhaustive", C.c_int32), ("reserved", C.c_int32),
+                ("basis_pairs", C.c_int64)]
+
+
+class _MomentReport(C.Structure):
+    _fields_ = [("m1", C.c_double), ("m2", C.c_double), ("exact", C.c_int32), ("reserved", C.c_int32),
+                ("pairs", C.c_int64)]
+
+
+@dataclass
+class MubReport:
+    """kerdock.hpp:199-208"""
+    max_within_gram_dev: float
+    min_cross_sq: float
+    max_cross_sq: float
+    max_cross_dev: float
+    exhaustive: bool
+    basis_pairs: int
+
+    def passed(self, tol: float) -> bool:
+        return self.max_within_gram_dev <= tol and self.max_cross_dev <= tol
+
+
+@dataclass
+class MomentReport:
+    """kerdock.hpp:261-266"""
+    m1: float
+    m2: float
+    exact: bool
+    pairs: int
+
+
+def verify_mub(k: int, cap: int = 8, policy: int = VERIFY_REFERENCE, device: int = 0) -> MubReport:
+    """kerdock.hpp:213-256 on the GPU (k > cap raises ValueError like the reference's invalid_argument)."""
+    r = _MubReport()
+    _check(lib().fstg_verify_mub(C.c_int(k), C.c_int(cap), C.c_int(policy), C.c_int(device), C.byref(r)))
+    return MubReport(r.max_within_gram_dev, r.min_cross_sq, r.max_cross_sq, r.max_cross_dev, bool(r.exhaustive),
+                     int(r.basis_pairs))
+
+
+def verify_design_moments(k: int, cap: int = 8, policy: int = VERIFY_REFERENCE, device: int = 0) -> MomentReport:
+    """kerdock.hpp:301-315 on the GPU."""
+    r = _MomentReport()
+    _check(lib().fstg_verify_design_moments(C.c_int(k), C.c_int(cap), C.c_int(policy), C.c_int(device),
+                                            C.byref(r)))
+    return MomentReport(r.m1, r.m2, bool(r.exact), int(r.pairs))
+
+
+def design_moment_target(d: int, k: int) -> float:
+    """kerdock.hpp:267-276: c_{d,k} = 1*3*...*(2k-1) / (d (d+2) ... (d+2(k-1)))."""
+    return float(lib().fstg_design_moment_target(C.c_int64(d), C.c_int(k)))
+
+
+def verify_kerdock_set(k: int, device: int = 0):
+    """cli.hpp:45-60: (all matrices symmetric with zero diagonal, rank-deficient pair-sum count)."""
+    skew, bad = C.c_int(), C.c_int64()
+    _check(lib().fstg_verify_kerdock_set(C.c_int(k), C.c_int(device), C.byref(skew), C.byref(bad)))
+    return bool(skew.value), int(bad.value)
 
 
 # -------------------------------------------------------------- profiling ----

@@ -183,6 +183,21 @@ int main() {
     check_throws<std::invalid_argument>([&] { preprocess(bad.data(), 2, 2); }, "nan");
     check_throws<std::invalid_argument>([&] { preprocess(bad.data(), 0, 2); }, "empty");
   }
+  // kerdock.hpp:198-317 verifiers (test_kerdock.cpp:200-216, 231-247)
+  {
+    const MubReport mub = verify_mub(4);
+    if (!mub.exhaustive || mub.max_within_gram_dev != 0.0 || mub.min_cross_sq != 1.0 / 16 || mub.max_cross_dev != 0.0) {
+      std::printf("FAIL verify_mub(4)\n");
+      ++failures;
+    }
+    const MomentReport mom = verify_design_moments(4);
+    if (std::abs(mom.m1 - 1.0 / 16) > 1e-12 || std::abs(mom.m2 - 1.0 / 96) > 1e-12 ||
+        design_moment_target(16, 2) != mom.m2) {
+      std::printf("FAIL verify_design_moments(4)\n");
+      ++failures;
+    }
+    check_throws<std::invalid_argument>([&] { verify_mub(6, 4); }, "cap");
+  }
   std::printf("cpp api: %s (%d failures)\n", failures ? "FAIL" : "ok", failures);
   return failures ? 1 : 0;
 }
