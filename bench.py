@@ -443,17 +443,28 @@ def run_sweep(args):
 
 # ------------------------------------------- config 4: retain-sampled ----
 def run_config4(args):
-    """Config 4: n = 16384 fp32, A iid N(0,1/n), 8192 vectors per step, s = 64, eps = 0.05.
+    """Config 4: n = 16384 fp32, A iid N(0,1/n), 8192 vectors per step per GPU, s = 64, eps = 0.05.
     The 8.8 TB sketch cannot exist: per chunk of vectors the indices are drawn,
     every Kerdock basis is FWHT-transformed keeping only the sampled columns
     (fstg_sample_columns — the full O(n^3 log n) Kerdock computation once per
-    chunk), and the stream reads the retained columns (fstg_transform_gathered_batch)."""
+    chunk), and the stream reads the retained columns (fstg_transform_gathered_batch).
+    N > 1 GPUs: a chunk spans every rank's vectors,
+    rank r computes only the columns of its Kerdock-basis shard and one NCCL
+    all-to-all routes each column to its vector's owner (parallel.route_retained_columns)."""
     import torch
-    from paper_2105_05879_b200 import fst, generators
-    dev = "cuda:0"
-    torch.cuda.set_device(0)
+    import torch.distributed as dist
+    from paper_2105_05879_b200 import fst, generators, parallel
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = f"cuda:{local}"
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(dev))
     n, B, s_val, eps_val = 16384, 8192, 64, 0.05
-    A64 = generators.iid_gaussian(n, 16384, dev)
+    A64 = generators.iid_gaussian(n, 16384, dev) if rank == 0 else torch.empty((n, n), dtype=torch.float64, device=dev)
+    if world > 1:
+        parallel.broadcast_matrix(A64, src=0)
     A32 = A64.float().contiguous()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -461,72 +472,108 @@ def run_config4(args):
     e1.record()
     torch.cuda.synchronize()
     design_ms = e0.elapsed_time(e1)
-    g_seeds, st_seeds = generators.trial_seeds(X_SEED, 0, B)
-    Y = torch.from_numpy(generators.sparse_targets(g_seeds, n, s_val, value_kind=1)).to(dev)
+    # every rank knows every vector's seed (draws of the whole chunk decide the routing)
+    g_all, st_all = generators.trial_seeds(X_SEED, 0, B * world)
+    first = rank * B
+    Y = torch.from_numpy(generators.sparse_targets(g_all[first:first + B], n, s_val, value_kind=1)).to(dev)
     lu = torch.linalg.lu_factor(A64)
     X = torch.linalg.lu_solve(*lu, Y.T).T
     X = (X / torch.linalg.vector_norm(X, dim=1, keepdim=True)).float().contiguous()
-    del Y, lu
-    seeds_dev = torch.from_numpy(st_seeds.view(np.int64)).to(dev)
+    del Y, lu, A64
+    seeds_all = torch.from_numpy(st_all.view(np.int64)).to(dev)
     p = fst.StreamParams(epsilon=eps_val, s=s_val, J=args.J, K=args.K, widen=WIDEN)
     N = args.J * args.K
     want = fst.candidate_count(s_val, WIDEN, n)
-    chunk = 2048
+    chunk = 2048 if world == 1 else 1024            # vectors per rank per chunk (~100 GB of columns in flight)
     ldc = des.column_stride
-    idx = torch.empty((chunk, N), dtype=torch.int64, device=dev)
-    cols = torch.empty((chunk * N, ldc), dtype=torch.float32, device=dev)  # 100 GB retained columns
+    nk = des.d // 2
+    shards = parallel.basis_shards(nk, world)
+    idx = torch.empty((chunk * world, N), dtype=torch.int64, device=dev)
+    cols = torch.empty((chunk * N, ldc), dtype=torch.float32, device=dev) if world == 1 else None
     out = fst.BatchResult(torch.zeros(B, dtype=torch.int32, device=dev),
                           torch.zeros((B, want), dtype=torch.int32, device=dev),
                           torch.zeros((B, want), dtype=torch.float32, device=dev))
     stream = torch.cuda.current_stream()
 
+    def sample_fn(ells):
+        buf = torch.empty((len(ells), ldc), dtype=torch.float32, device=dev)
+        fst.sample_columns(des, ells, out=buf, stream=stream.cuda_stream)
+        return buf
+
     def step(timing):
         for c0 in range(0, B, chunk):
             cb = min(chunk, B - c0)
-            fst._check(fst.lib().fstg_draw_samples(des.handle, fst.C.byref(p._c()), fst._ptr(seeds_dev[c0:c0 + cb]),
-                                                   fst.C.c_int64(cb), fst._ptr(idx), fst.C.c_void_p(stream.cuda_stream)))
             a0 = torch.cuda.Event(enable_timing=True)
             a1 = torch.cuda.Event(enable_timing=True)
-            a0.record(stream)
-            fst.sample_columns(des, idx[:cb].reshape(-1), out=cols, stream=stream.cuda_stream)
-            a1.record(stream)
+            if world == 1:
+                fst._check(fst.lib().fstg_draw_samples(des.handle, fst.C.byref(p._c()),
+                                                       fst._ptr(seeds_all[c0:c0 + cb]), fst.C.c_int64(cb),
+                                                       fst._ptr(idx), fst.C.c_void_p(stream.cuda_stream)))
+                a0.record(stream)
+                fst.sample_columns(des, idx[:cb].reshape(-1), out=cols, stream=stream.cuda_stream)
+                a1.record(stream)
+                gathered, ind = cols, idx[:cb]
+            else:
+                # chunk = vectors [q*B + c0, q*B + c0 + cb) of every rank q
+                rows = torch.cat([seeds_all[q * B + c0:q * B + c0 + cb] for q in range(world)])
+                fst._check(fst.lib().fstg_draw_samples(des.handle, fst.C.byref(p._c()), fst._ptr(rows),
+                                                       fst.C.c_int64(cb * world), fst._ptr(idx),
+                                                       fst.C.c_void_p(stream.cuda_stream)))
+                idx_host = idx[:cb * world].cpu().numpy()
+                plan = parallel.RoutingPlan(idx_host, [(q * cb, cb) for q in range(world)], shards, des.d, nk, rank)
+                a0.record(stream)
+                gathered = parallel.route_retained_columns(plan, sample_fn, ldc, torch.float32, dev)
+                a1.record(stream)
+                ind = idx[rank * cb:(rank + 1) * cb]
             sub = fst.BatchResult(out.counts[c0:c0 + cb], out.support[c0:c0 + cb], out.values[c0:c0 + cb])
-            fst.transform_gathered_batch(des, X[c0:c0 + cb], p, idx[:cb], cols, out=sub, stream=stream.cuda_stream)
+            fst.transform_gathered_batch(des, X[c0:c0 + cb], p, ind, gathered, out=sub, stream=stream.cuda_stream)
             timing.append((a0, a1))
+            del gathered
 
     warm = []
     for _ in range(max(1, args.warmup)):
         step(warm)
     torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     timing = []
-    with ClockSampler(0) as clk:
+    with ClockSampler(local) as clk:
         t0.record(stream)
         for _ in range(args.steps):
             step(timing)
         t1.record(stream)
         torch.cuda.synchronize()
-    ms = t0.elapsed_time(t1)
+    if world > 1:
+        dist.barrier()
+    ms = parallel.max_over_ranks(t0.elapsed_time(t1), device=dev)
     retain_ms = sum(a.elapsed_time(b) for a, b in timing)
     passes = len(timing)
-    adds_per_pass = (des.d // 2) * n * des.d * 14  # (d/2) m d log2 d
+    adds_per_pass = (des.d // 2) * n * des.d * 14 / world  # (d/2) m d log2 d, this rank's basis shard
     fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12     # nominal FP32 TFLOP/s (no measured CUDA-core peak)
     achieved = adds_per_pass * passes / (retain_ms / 1e3) / 1e12
-    line = {"metric": "thresholded-Ax vectors/sec (config4, n=16384, retain-sampled)", "value": B * args.steps / (ms / 1e3),
-            "unit": "vectors/s", "n_gpus": 1, "steps": args.steps, "warmup": max(1, args.warmup),
+    mean_support = float(out.counts.float().mean())
+    if world > 1:
+        mean_support = parallel.max_over_ranks(mean_support, device=dev)
+    line = {"metric": "thresholded-Ax vectors/sec (config4, n=16384, retain-sampled)",
+            "value": B * world * args.steps / (ms / 1e3),
+            "unit": "vectors/s", "n_gpus": world, "steps": args.steps, "warmup": max(1, args.warmup),
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "fp32", "data": "synthetic (A iid N(0,1/n), y 64-sparse N(0,1), x = A^-1 y / |.|)",
-            "config": {"workload": f"config4: n=m=16384 fp32, s=64, eps=0.05, 8192 vectors/step in chunks of {chunk}, "
-                                   f"J={args.J}, K={args.K} (full sketch 8.8 TB: sampled columns retained, "
-                                   f"{chunk * N * ldc * 4 / 1e9:.0f} GB per chunk)",
-                       "mean_support": float(out.counts.float().mean())},
+            "config": {"workload": f"config4: n=m=16384 fp32, s=64, eps=0.05, 8192 vectors/step/GPU in chunks of "
+                                   f"{chunk}/GPU, J={args.J}, K={args.K} (full sketch 8.8 TB: sampled columns "
+                                   f"retained{'' if world == 1 else ', basis-sharded + NCCL all-to-all'})",
+                       "mean_support": mean_support},
             "preprocess": {"design_ms": design_ms, "kerdock_pass_ms": retain_ms / passes,
                            "kerdock_passes_per_step": passes // args.steps,
                            "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "Tadd/s",
                                         "frac": achieved / fp32_peak, "peak_source": "nominal 148 SM x 128 lanes x "
                                         "2 (FADD2) x 1.965 GHz"}},
             "clocks": clk.summary()}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 # ------------------------------------------------------- reference arm ----

@@ -11,6 +11,13 @@ collectives are in preparation:
     column-major sketch) and an in-place all-gather over NVLink completes every
     replica (option (ii) of §8(e); option (i), local recompute after the
     broadcast, is the default because it moves 64 MB instead of ~120 GB).
+  * ``route_retained_columns`` — config 4 (n = 16384, no sketch can exist,
+    §8(e) step 3): rank r computes the sampled columns whose Kerdock basis
+    lies in its basis shard (the identity block belongs to the last rank),
+    for every vector of the chunk, and one all-to-all sends each column to
+    the rank that owns its vector, which scatters them into the
+    draw_and_gather layout (stream.hpp:184-191). The O(n^3 log n) Kerdock
+    pass splits across ranks, and a chunk can hold world x more vectors.
   * ``max_over_ranks``     — step time = max over ranks (device-timed).
 
 Everything here is host logic; it is tested on CPU with the gloo backend
@@ -80,6 +87,67 @@ def allgather_basis_shards(full, world: int, rank: int, nk: int, d: int, ldc: in
     kerdock = full[: nk * d * ldc]
     mine = kerdock[rank * per:(rank + 1) * per]
     dist.all_gather_into_tensor(kerdock, mine, group=group)
+
+
+def column_owner(ells: np.ndarray, shards: List[Tuple[int, int]], d: int, nk: int) -> np.ndarray:
+    """Rank that computes column ell: the owner of its Kerdock basis, the last rank for the identity block."""
+    ells = np.asarray(ells, dtype=np.int64)
+    starts = np.array([first for first, _ in shards], dtype=np.int64)
+    basis = ells // d
+    owner = np.searchsorted(starts, basis, side="right") - 1
+    # empty shards share a start with their successor: searchsorted picks the last of them, which is non-empty
+    owner = np.where(basis >= nk, len(shards) - 1, owner)
+    return owner.astype(np.int64)
+
+
+class RoutingPlan:
+    """Who computes and who receives every (vector, sample) column of a chunk.
+
+    idx_all (B, N): the draws of every vector of the chunk (identical on every
+    rank, fstg_draw_samples); vec_ranges[q] = (first, count) rows owned by rank
+    q (contiguous, increasing). Columns travel grouped by destination rank and,
+    within a destination, in (vector, sample) order."""
+
+    def __init__(self, idx_all: np.ndarray, vec_ranges: List[Tuple[int, int]], shards: List[Tuple[int, int]], d: int,
+                 nk: int, rank: int):
+        idx_all = np.asarray(idx_all, dtype=np.int64)
+        B, N = idx_all.shape
+        world = len(vec_ranges)
+        if len(shards) != world or not (0 <= rank < world):
+            raise ValueError("RoutingPlan: ranks / shards mismatch")
+        if sum(c for _, c in vec_ranges) != B or any(vec_ranges[q][0] != sum(c for _, c in vec_ranges[:q])
+                                                     for q in range(world)):
+            raise ValueError("RoutingPlan: vector ranges must tile [0, B) in rank order")
+        src = column_owner(idx_all.ravel(), shards, d, nk)
+        flat = idx_all.ravel()
+        # send side: my columns in flat (vector, sample) order == grouped by destination
+        mine = np.nonzero(src == rank)[0]
+        self.send_ells = flat[mine]
+        row_dst = np.repeat(np.arange(world), [c * N for _, c in vec_ranges])
+        self.send_counts = np.bincount(row_dst[mine], minlength=world).astype(np.int64)
+        # receive side: rows of my vectors, grouped by source rank, flat order inside a source
+        first, count = vec_ranges[rank]
+        lo, hi = first * N, (first + count) * N
+        src_mine = src[lo:hi]
+        order = np.argsort(src_mine, kind="stable")
+        self.recv_positions = order.astype(np.int64)          # local row (v_local * N + j) of each received column
+        self.recv_counts = np.bincount(src_mine, minlength=world).astype(np.int64)
+        self.local_rows = count * N
+
+
+def route_retained_columns(plan: RoutingPlan, sample_fn, ldc: int, dtype, device, group=None):
+    """Computes this rank's columns (sample_fn(ells) -> (len, ldc) tensor), exchanges them with one
+    all_to_all_single, and returns the (local_rows, ldc) gathered buffer of this rank's vectors."""
+    import torch
+    import torch.distributed as dist
+    send = sample_fn(plan.send_ells) if len(plan.send_ells) else torch.empty((0, ldc), dtype=dtype, device=device)
+    recv = torch.empty((int(plan.recv_counts.sum()), ldc), dtype=dtype, device=device)
+    dist.all_to_all_single(recv, send, output_split_sizes=plan.recv_counts.tolist(),
+                           input_split_sizes=plan.send_counts.tolist(), group=group)
+    del send
+    gathered = torch.empty((plan.local_rows, ldc), dtype=dtype, device=device)
+    gathered.index_copy_(0, torch.from_numpy(plan.recv_positions).to(device), recv)
+    return gathered
 
 
 def broadcast_matrix(a, src: int = 0, group=None):

@@ -121,3 +121,37 @@ def test_config4_shape_spot_check(fst, orc):
         np.testing.assert_allclose(g.mu, r.mu, rtol=1e-4, atol=1e-5)
         assert g.support.tolist() == r.support.tolist()
         np.testing.assert_allclose(g.values, r.values, rtol=1e-5)
+
+
+def test_route_retained_columns_nccl_single_rank(fst, orc):
+    """The config-4 multi-GPU routing (RoutingPlan + NCCL all_to_all_single +
+    scatter) on a one-rank NCCL group with the real fstg_sample_columns: the
+    routed buffer equals the direct draw_and_gather columns."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2105_05879_b200 import parallel
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda:0"))
+    try:
+        a = torch.randn(300, 1000, device="cuda:0", dtype=torch.float32)
+        des = fst.preprocess_design(a)
+        idx_all = np.random.default_rng(2).integers(0, des.L, size=(6, 50))
+        nk = des.d // 2
+        plan = parallel.RoutingPlan(idx_all, [(0, 6)], parallel.basis_shards(nk, 1), des.d, nk, 0)
+
+        def sample_fn(ells):
+            buf = torch.empty((len(ells), des.column_stride), dtype=torch.float32, device="cuda:0")
+            fst.sample_columns(des, ells, out=buf)
+            return buf
+
+        got = parallel.route_retained_columns(plan, sample_fn, des.column_stride, torch.float32, "cuda:0")
+        want = fst.sample_columns(des, idx_all.ravel())
+        assert np.array_equal(got.cpu().numpy(), want)
+    finally:
+        dist.destroy_process_group()

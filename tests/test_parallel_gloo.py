@@ -85,3 +85,69 @@ def test_shard_plans():
     with pytest.raises(ValueError):
         parallel.vector_shard(8, 8, 1)
     assert parallel.shard_element_range((256, 256), 4096, 4096) == (256 * 4096 * 4096, 512 * 4096 * 4096)
+
+
+def _route_worker(rank, world, port, tmpdir):
+    """Config-4 routing (parallel.RoutingPlan / route_retained_columns) on gloo:
+    each rank computes only the columns of its basis shard (oracle columns
+    A s_ell), the all-to-all delivers them, and every rank's gathered buffer
+    must equal the direct draw_and_gather of its own vectors."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as orc
+        k, n, m = 4, 13, 11
+        d, nk = 1 << k, (1 << k) // 2
+        L = d * (nk + 1)
+        a = np.random.default_rng(3).standard_normal((m, n))
+        ok = []
+        for B, N in [(5, 7), (1, 3), (9, 40)]:
+            idx_all = np.random.default_rng(B * 100 + N).integers(0, L, size=(B, N))
+            idx_all[0, 0] = L - 1                                   # identity block -> last rank
+            vec_ranges = [parallel.strong_shard(q, world, B) for q in range(world)]
+            shards = parallel.basis_shards(nk, world)
+            plan = parallel.RoutingPlan(idx_all, vec_ranges, shards, d, nk, rank)
+            computed = []
+
+            def sample_fn(ells):
+                owners = parallel.column_owner(ells, shards, d, nk)
+                assert np.all(owners == rank)                       # only my basis shard is computed here
+                computed.append(len(ells))
+                return torch.from_numpy(orc.design_columns(k, n, ells) @ a.T)
+
+            got = parallel.route_retained_columns(plan, sample_fn, m, torch.float64, "cpu")
+            first, count = vec_ranges[rank]
+            want = orc.design_columns(k, n, idx_all[first:first + count].ravel()) @ a.T if count else np.zeros((0, m))
+            ok.append(bool(got.shape == (count * N, m) and np.array_equal(got.numpy(), want)))
+        np.save(os.path.join(tmpdir, f"route{rank}.npy"), {"ok": ok}, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_config4_routing(tmp_path):
+    world, port = 2, _free_port()
+    mp.spawn(_route_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert all(np.load(tmp_path / f"route{r}.npy", allow_pickle=True).item()["ok"])
+
+
+def test_routing_plan_single_process():
+    """Plan bookkeeping for 3 ranks without a process group: every (vector, sample)
+    is sent exactly once, by the owner of its basis, to the owner of its vector."""
+    d, nk, L = 16, 8, 16 * 9
+    rng = np.random.default_rng(5)
+    idx_all = rng.integers(0, L, size=(10, 6))
+    vec_ranges = [parallel.strong_shard(q, 3, 10) for q in range(3)]
+    shards = parallel.basis_shards(nk, 3)
+    plans = [parallel.RoutingPlan(idx_all, vec_ranges, shards, d, nk, r) for r in range(3)]
+    N = idx_all.shape[1]
+    for q in range(3):                                   # what q receives from r == what r sends to q
+        for r in range(3):
+            assert plans[q].recv_counts[r] == plans[r].send_counts[q]
+        assert plans[q].recv_counts.sum() == vec_ranges[q][1] * N
+        assert sorted(plans[q].recv_positions.tolist()) == list(range(vec_ranges[q][1] * N))
+    assert sum(len(p.send_ells) for p in plans) == idx_all.size
+    assert parallel.column_owner(np.array([L - 1]), shards, d, nk)[0] == 2
+    assert parallel.column_owner(np.array([0]), parallel.basis_shards(1, 4), d, 1)[0] == 0
+    with pytest.raises(ValueError):
+        parallel.RoutingPlan(idx_all, vec_ranges[:2], shards, d, nk, 0)
