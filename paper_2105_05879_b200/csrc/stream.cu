@@ -42,11 +42,17 @@ constexpr int kTRing = 64;                  // slots of the coefficient ring
 constexpr int kNS = 4;                      // samples per coefficient-warp group
 constexpr int kSegBytes = 16384;            // one ring stage at most
 constexpr int kMaxStages = 64;
-constexpr int kXBuf = 3;                    // x buffers: coefficients on v+2 while the tail refines v
+// x buffers: coefficients on v+1 while the tail refines v. A third buffer (coefficients two
+// vectors ahead) measured 5% slower at config 3 (profiles/r01_stream_pipeline.txt).
+constexpr int kXBuf = 2;
 constexpr int kSmemBudget = 227 * 1024;
-constexpr int kInflightBytes = 5 * 16384;    // column bytes in flight per SM
+constexpr int kInflightBytes = 8 * 16384;    // cap on column bytes in flight per SM (shared memory decides)
 constexpr int kBarCoef = 2, kBarTail = 3;   // named barrier ids
-constexpr int kRStages = kTLW - 1;          // refinement ring: tail warp 0 issues, warps 1..6 consume
+#ifndef FSTG_RSTAGES
+#define FSTG_RSTAGES 6
+#endif
+constexpr int kRStages = FSTG_RSTAGES;       // refinement ring: tail warp 0 issues, warps 1..kRStages consume
+static_assert(kRStages >= 1 && kRStages <= kTLW - 1, "refinement stages are owned by tail warps 1..kTLW-1");
 
 template <typename T>
 struct KeyOf;
@@ -408,26 +414,52 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
 
   if (warp == kWarpProd) {
     // ======================= producer warp =======================
-    if (lane == 0 && !(A.debug & 2)) {
+    // P lanes issue the bulk copies in lockstep (one lane's back-to-back copies
+    // serialise at ~4 TB/s chip-wide, profiles/r01_tma_issue.txt); lane l owns the
+    // ring stages s = l (mod P), P | S, so every stage is refilled in order by one
+    // thread and its empty-barrier parity never runs two phases ahead. Each lane
+    // loads the sample index of its next copy while issuing the current one.
+    int P = 1;
+    for (int c = S < 32 ? S : 32; c > 1; --c)
+      if (S % c == 0) {
+        P = c;
+        break;
+      }
+    if (lane < P && !(A.debug & 2)) {
       const uint64_t pol = policy_evict_first();
-      int stage = 0;
-      uint32_t phase = 0, used = 0;
-      for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x) {
-        const uint32_t* vidx = A.idx + v * A.N;
-        for (int64_t j = 0; j < A.N; ++j) {
-          const T* col = A.gathered ? A.gathered + (v * A.N + j) * A.ldc
-                                    : A.cols + static_cast<int64_t>(__ldg(vidx + j)) * A.ldc;
-          for (int sg = 0; sg < A.nseg; ++sg) {
-            if (used) mbar_wait(&empty[stage], phase ^ 1u);
-            const uint32_t bytes = (sg == A.nseg - 1) ? stage_bytes_last : stage_bytes_full;
-            mbar_arrive_expect_tx(&full[stage], bytes);
-            bulk_g2s(ring + size_t(stage) * A.stage_stride, col + int64_t(sg) * SEG, bytes, &full[stage], pol);
-            if (++stage == S) {
-              stage = 0;
-              phase ^= 1u;
-              used = 1;
-            }
+      const int nseg = A.nseg;
+      int64_t v = blockIdx.x, j = 0;
+      int sg = 0;
+      auto advance = [&](int by) {
+        sg += by;
+        while (sg >= nseg) {
+          sg -= nseg;
+          if (++j == A.N) {
+            j = 0;
+            v += gridDim.x;
           }
+        }
+      };
+      advance(lane);
+      uint32_t ell_next = (v < A.B && !A.gathered) ? __ldg(A.idx + v * A.N + j) : 0u;
+      int stage = lane;
+      uint32_t phase = 0, used = 0;
+      while (v < A.B) {
+        const int64_t vc = v, jc = j;
+        const int sgc = sg;
+        const uint32_t ell = ell_next;
+        advance(P);
+        if (v < A.B && !A.gathered) ell_next = __ldg(A.idx + v * A.N + j);
+        const T* col = A.gathered ? A.gathered + (vc * A.N + jc) * A.ldc : A.cols + static_cast<int64_t>(ell) * A.ldc;
+        if (used) mbar_wait(&empty[stage], phase ^ 1u);
+        const uint32_t bytes = (sgc == nseg - 1) ? stage_bytes_last : stage_bytes_full;
+        mbar_arrive_expect_tx(&full[stage], bytes);
+        bulk_g2s(ring + size_t(stage) * A.stage_stride, col + int64_t(sgc) * SEG, bytes, &full[stage], pol);
+        stage += P;
+        if (stage >= S) {
+          stage -= S;
+          phase ^= 1u;
+          used = 1;
         }
       }
     }
@@ -663,7 +695,10 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
       // ---- refinement: v_i = a_i . x, fp64 accumulation (stream.hpp:259-266) ----
       mbar_wait(&x_full[xb], xu & 1u);
       const T* xs = xbuf + xb * dx;
-      if (A.rstride > 0) {
+      if (A.debug & 4) {
+        // experiment: no refinement (no A-row traffic)
+        for (int64_t ci = tw * 32 + lane; ci < A.want; ci += kTLW * 32) cflag[ci] = 0;
+      } else if (A.rstride > 0) {
         // Gather-GEMV staged through TMA: tail warp 0 bulk-copies the candidate
         // rows of A (L2-resident, evict-last) into a kRStages-deep ring; warp
         // 1 + st owns stage st and takes the rows whose running index g
@@ -671,17 +706,20 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
         // one warp (mbarrier parity never aliases).
         const uint32_t rbytes = static_cast<uint32_t>(A.lda * sizeof(T));
         if (tw == 0) {
-          if (lane == 0) {
-            for (int64_t ci = 0; ci < A.want; ++ci) {
+          // lane st issues the rows of stage st (one issuing thread per stage, like its consumer)
+          if (lane < kRStages) {
+            const uint32_t st = static_cast<uint32_t>(lane);
+            const uint32_t first = (st + kRStages - rg % kRStages) % kRStages;
+            for (int64_t ci = first; ci < A.want; ci += kRStages) {
               const uint32_t g = rg + static_cast<uint32_t>(ci);
-              const uint32_t st = g % kRStages, u = g / kRStages;
+              const uint32_t u = g / kRStages;
               if (u > 0) mbar_wait(&r_empty[st], (u - 1) & 1u);
               mbar_arrive_expect_tx(&r_full[st], rbytes);
               bulk_g2s(rring + size_t(st) * A.rstride, A.a + int64_t(cand[ci]) * A.lda, rbytes, &r_full[st], pol_keep);
             }
           }
           __syncwarp();
-        } else {
+        } else if (tw - 1 < kRStages) {
           const uint32_t st = static_cast<uint32_t>(tw - 1);
           const uint32_t first = (st + kRStages - rg % kRStages) % kRStages;  // first ci with (rg + ci) % kRS == st
           for (int64_t ci = first; ci < A.want; ci += kRStages) {
@@ -907,9 +945,7 @@ int stream_grid_size(const StreamArgs<T>& args, bool strict, int64_t B, size_t* 
   const int64_t row_bytes = args.lda * int64_t(sizeof(T));
   const int rstride = row_bytes <= kSegBytes ? static_cast<int>((row_bytes + 127) / 128 * 128) : 0;
   *rstride_out = rstride;
-  // three x buffers when they fit next to a minimal ring, else two (d = 16384)
-  int xbufs = kXBuf;
-  if (smem_layout<T>(args.d, 2, stride, args.want, rstride, xbufs).total > static_cast<size_t>(kSmemBudget)) xbufs = 2;
+  const int xbufs = kXBuf;
   *xbufs_out = xbufs;
   const SmemLayout L0 = smem_layout<T>(args.d, 0, stride, args.want, rstride, xbufs);
   int S = static_cast<int>((kSmemBudget - static_cast<int64_t>(L0.total) - 1024) / stride);
