@@ -914,6 +914,17 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
       ProfScope ps("stream", st);
       cuda_check(launch_stream<T>(args, strict, grid, st), "stream kernel");
     }
+    if (args.debug & 8) {  // experiment: where each warp role waits (stream.cu WaitSite)
+      cuda_check(cudaStreamSynchronize(st), "sync");
+      unsigned long long w[14] = {};
+      stream_wait_profile(w, 14);
+      auto pct = [&](int site, int total) { return w[total] ? 100.0 * double(w[site]) / double(w[total]) : 0.0; };
+      std::fprintf(stderr,
+                   "stream waits (%% of role time): producer empty %.1f | coef x_empty %.1f t_empty %.1f | tail m_full "
+                   "%.1f x_full %.1f r_empty %.1f r_full %.1f | consumer t_full %.1f column %.1f m_empty %.1f\n",
+                   pct(0, 10), pct(1, 11), pct(2, 11), pct(3, 12), pct(4, 12), pct(5, 12), pct(6, 12), pct(7, 13),
+                   pct(8, 13), pct(9, 13));
+    }
     // ---- outputs ----
     if (!all_dev) {
       cuda_check(cudaEventRecord(ev_done[b], st), "event");

@@ -25,6 +25,10 @@ cudaError_t launch_identity(const T* a, int64_t lda, int64_t m, int64_t n, int64
 template <typename T>
 cudaError_t launch_row_norms(const T* a, int64_t lda, int64_t m, int64_t n, double* out, cudaStream_t st);
 
+// Experiment readout of the stream kernel's per-role mbarrier wait cycles
+// (FSTG_STREAM_DEBUG bit 8; 14 counters, see stream.cu WaitSite); resets them.
+void stream_wait_profile(unsigned long long* out, int count);
+
 // ---- design verifiers (verify.cu) ----
 // Per basis pair (explicit list, or pb == nullptr: the upper triangle incl.
 // the diagonal) the d-point integer FWHT of (-1)^(Q_b + Q_b2): acc (8 u64 =

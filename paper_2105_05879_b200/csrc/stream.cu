@@ -31,12 +31,15 @@
 
 namespace fstg {
 
-constexpr int kNCW = 8;                     // consumer warps
+#ifndef FSTG_NCW
+#define FSTG_NCW 8
+#endif
+constexpr int kNCW = FSTG_NCW;              // consumer warps
 constexpr int kNC = kNCW * 32;              // consumer threads
 constexpr int kCW = 8;                      // coefficient warps
 constexpr int kTLW = 7;                     // tail warps (median / select / refine / compact); 24 warps total
 constexpr int kTL = kTLW * 32;              // tail threads
-constexpr int kThreads = kNC + kCW * 32 + kTL + 32;  // + producer warp = 768 (80 regs/thread)
+constexpr int kThreads = kNC + kCW * 32 + kTL + 32;  // + producer warp (768 threads with 8 consumer warps: 80 regs)
 constexpr int kWarpCoef = kNCW, kWarpTail = kNCW + kCW, kWarpProd = kNCW + kCW + kTLW;
 constexpr int kTRing = 64;                  // slots of the coefficient ring
 constexpr int kNS = 4;                      // samples per coefficient-warp group
@@ -53,6 +56,37 @@ constexpr int kBarCoef = 2, kBarTail = 3;   // named barrier ids
 #endif
 constexpr int kRStages = FSTG_RSTAGES;       // refinement ring: tail warp 0 issues, warps 1..kRStages consume
 static_assert(kRStages >= 1 && kRStages <= kTLW - 1, "refinement stages are owned by tail warps 1..kTLW-1");
+
+// Experiment instrumentation (FSTG_STREAM_DEBUG bit 8): cycles each warp role
+// spends in each mbarrier wait, summed over warps (lane 0) into g_wait_cycles.
+enum WaitSite {
+  kWProdEmpty, kWCoefXEmpty, kWCoefTEmpty, kWTailMFull, kWTailXFull, kWTailREmpty, kWTailRFull,
+  kWConsT, kWConsCol, kWConsMEmpty, kWTotProd, kWTotCoef, kWTotTail, kWTotCons, kWSites
+};
+__device__ unsigned long long g_wait_cycles[kWSites];
+
+struct WaitProf {
+  bool on;
+  unsigned long long* acc;  // kWSites shared-memory counters, acc[kWSites] = warps finished
+  __device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity, int site) {
+    if (on) {
+      const long long t0 = clock64();
+      mbar_wait(bar, parity);
+      if ((threadIdx.x & 31) == 0) atomicAdd(&acc[site], static_cast<unsigned long long>(clock64() - t0));
+    } else {
+      mbar_wait(bar, parity);
+    }
+  }
+  // called once per warp when its role ends; the last warp publishes the CTA's totals
+  __device__ __forceinline__ void done(int site, long long t_start) {
+    if (!on || (threadIdx.x & 31) != 0) return;
+    atomicAdd(&acc[site], static_cast<unsigned long long>(clock64() - t_start));
+    __threadfence_block();
+    if (atomicAdd(&acc[kWSites], 1ull) == static_cast<unsigned long long>(blockDim.x / 32 - 1)) {
+      for (int i = 0; i < kWSites; ++i) atomicAdd(&g_wait_cycles[i], atomicAdd(&acc[i], 0ull));
+    }
+  }
+};
 
 template <typename T>
 struct KeyOf;
@@ -371,6 +405,10 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
   T* cval = reinterpret_cast<T*>(smem + Ls.cval);
   uint8_t* cflag = reinterpret_cast<uint8_t*>(smem + Ls.cflag);
   __shared__ uint32_t wbase[32];
+  __shared__ unsigned long long wait_acc[kWSites + 1];
+  const long long t_start = clock64();
+  WaitProf wp{(A.debug & 8) != 0, wait_acc};
+  if (threadIdx.x <= kWSites) wait_acc[threadIdx.x] = 0;
 
   const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
   const int S = A.stages;
@@ -451,7 +489,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
         advance(P);
         if (v < A.B && !A.gathered) ell_next = __ldg(A.idx + v * A.N + j);
         const T* col = A.gathered ? A.gathered + (vc * A.N + jc) * A.ldc : A.cols + static_cast<int64_t>(ell) * A.ldc;
-        if (used) mbar_wait(&empty[stage], phase ^ 1u);
+        if (used) wp.wait(&empty[stage], phase ^ 1u, kWProdEmpty);
         const uint32_t bytes = (sgc == nseg - 1) ? stage_bytes_last : stage_bytes_full;
         mbar_arrive_expect_tx(&full[stage], bytes);
         bulk_g2s(ring + size_t(stage) * A.stage_stride, col + int64_t(sgc) * SEG, bytes, &full[stage], pol);
@@ -463,6 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
         }
       }
     }
+    wp.done(kWTotProd, t_start);
     return;
   }
 
@@ -473,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     uint32_t lv = 0;
     for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
       const uint32_t xb = lv % static_cast<uint32_t>(A.xbufs), xu = lv / static_cast<uint32_t>(A.xbufs);
-      if (xu > 0) mbar_wait(&x_empty[xb], (xu - 1) & 1u);
+      if (xu > 0) wp.wait(&x_empty[xb], (xu - 1) & 1u, kWCoefXEmpty);
       T* xs = xbuf + xb * dx;
       const T* xv = A.X + v * A.ldx;
       for (int64_t p = ctid; p < A.d; p += kCW * 32) xs[p] = (p < A.n) ? xv[p] : T(0);
@@ -492,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
           const uint64_t g = g0 + uint64_t(j);
           const uint32_t slot = static_cast<uint32_t>(g % kTRing), u = static_cast<uint32_t>(g / kTRing);
           const T t = coeff_strict<T>(A, xs, __ldg(vidx + j));
-          if (u > 0) mbar_wait(&t_empty[slot], (u - 1) & 1u);
+          if (u > 0) wp.wait(&t_empty[slot], (u - 1) & 1u, kWCoefTEmpty);
           tring[slot] = t;
           mbar_arrive(&t_full[slot]);
         }
@@ -520,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
             if (j < A.N) {
               const uint64_t g = g0 + uint64_t(j);
               const uint32_t slot = static_cast<uint32_t>(g % kTRing), u = static_cast<uint32_t>(g / kTRing);
-              if (u > 0) mbar_wait(&t_empty[slot], (u - 1) & 1u);
+              if (u > 0) wp.wait(&t_empty[slot], (u - 1) & 1u, kWCoefTEmpty);
               if (lane == 0) {
                 tring[slot] = t[k];
                 mbar_arrive(&t_full[slot]);
@@ -534,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
           const uint64_t g = g0 + uint64_t(j);
           const uint32_t slot = static_cast<uint32_t>(g % kTRing), u = static_cast<uint32_t>(g / kTRing);
           const T t = coeff_generic<T>(A, xs, __ldg(vidx + j), lane);
-          if (u > 0) mbar_wait(&t_empty[slot], (u - 1) & 1u);
+          if (u > 0) wp.wait(&t_empty[slot], (u - 1) & 1u, kWCoefTEmpty);
           if (lane == 0) {
             tring[slot] = t;
             mbar_arrive(&t_full[slot]);
@@ -544,6 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
       }
       named_bar_sync(kBarCoef, kCW * 32);
     }
+    wp.done(kWTotCoef, t_start);
     return;
   }
 
@@ -559,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
                      xu = lv / static_cast<uint32_t>(A.xbufs);
       T* means = scratch + slot * slot_elems;
       T* mus = means + A.K * A.m_pad;
-      mbar_wait(&m_full[slot], su & 1u);
+      wp.wait(&m_full[slot], su & 1u, kWTailMFull);
 
       // ---- median of the K batch means (stream.hpp:126-143) ----
       for (int64_t c = ttid; int64_t(c) * VEC < A.m_pad; c += kTL) {
@@ -693,7 +733,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
       named_bar_sync(kBarTail, kTL);
 
       // ---- refinement: v_i = a_i . x, fp64 accumulation (stream.hpp:259-266) ----
-      mbar_wait(&x_full[xb], xu & 1u);
+      wp.wait(&x_full[xb], xu & 1u, kWTailXFull);
       const T* xs = xbuf + xb * dx;
       if (A.debug & 4) {
         // experiment: no refinement (no A-row traffic)
@@ -713,7 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
             for (int64_t ci = first; ci < A.want; ci += kRStages) {
               const uint32_t g = rg + static_cast<uint32_t>(ci);
               const uint32_t u = g / kRStages;
-              if (u > 0) mbar_wait(&r_empty[st], (u - 1) & 1u);
+              if (u > 0) wp.wait(&r_empty[st], (u - 1) & 1u, kWTailREmpty);
               mbar_arrive_expect_tx(&r_full[st], rbytes);
               bulk_g2s(rring + size_t(st) * A.rstride, A.a + int64_t(cand[ci]) * A.lda, rbytes, &r_full[st], pol_keep);
             }
@@ -724,7 +764,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
           const uint32_t first = (st + kRStages - rg % kRStages) % kRStages;  // first ci with (rg + ci) % kRS == st
           for (int64_t ci = first; ci < A.want; ci += kRStages) {
             const uint32_t g = rg + static_cast<uint32_t>(ci);
-            mbar_wait(&r_full[st], (g / kRStages) & 1u);
+            wp.wait(&r_full[st], (g / kRStages) & 1u, kWTailRFull);
             double dot = 0.0, dot2 = 0.0;
             if constexpr (sizeof(T) == 4) {
               const int64_t nv = (A.n + 3) / 4;
@@ -843,6 +883,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
       if (ttid == 0) A.counts[v] = static_cast<int32_t>(out_base);
       named_bar_sync(kBarTail, kTL);  // cand/cval/cflag reuse by the next vector
     }
+    wp.done(kWTotTail, t_start);
     return;
   }
 
@@ -868,13 +909,13 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     for (int64_t j = 0; j < A.N; ++j) {
       T t = T(1);
       if (!(A.debug & 1)) {
-        mbar_wait(&t_full[tslot], tphase);
+        wp.wait(&t_full[tslot], tphase, kWConsT);
         t = tring[tslot];
       }
 #pragma unroll
       for (int sg = 0; sg < NSEG; ++sg) {
         if (sg < A.nseg && !(A.debug & 2)) {
-          mbar_wait(&full[stage], phase);
+          wp.wait(&full[stage], phase, kWConsCol);
           const typename Vec<T>::V* src = reinterpret_cast<const typename Vec<T>::V*>(ring + size_t(stage) * A.stage_stride);
           const int64_t rows_here = (sg == A.nseg - 1) ? seg_last_rows : SEG;
 #pragma unroll
@@ -911,7 +952,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
       }
       if (++jb == A.J) {
         // batch b complete: mean = sum / J (IEEE division, stream.hpp:237)
-        if (b == 0 && su > 0) mbar_wait(&m_empty[slot], (su - 1) & 1u);
+        if (b == 0 && su > 0) wp.wait(&m_empty[slot], (su - 1) & 1u, kWConsMEmpty);
         T* mb = means + b * A.m_pad;
         const T Jt = static_cast<T>(A.J);
 #pragma unroll
@@ -934,6 +975,16 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     __syncwarp();
     if (lane == 0) mbar_arrive(&m_full[slot]);
   }
+  wp.done(kWTotCons, t_start);
+}
+
+// Experiment readout for FSTG_STREAM_DEBUG bit 8 (reset after reading).
+void stream_wait_profile(unsigned long long* out, int count) {
+  unsigned long long h[kWSites] = {};
+  cudaMemcpyFromSymbol(h, g_wait_cycles, sizeof(h));
+  const unsigned long long z[kWSites] = {};
+  cudaMemcpyToSymbol(g_wait_cycles, z, sizeof(z));
+  for (int i = 0; i < count && i < kWSites; ++i) out[i] = h[i];
 }
 
 // ------------------------------------------------------------- launching --

@@ -1,4 +1,8 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-ARGS2="--steps 1 --warmup 1 --no-e2e --no-cpu --batch 4096"
-timeout 600 python bench.py $ARGS2 > gpurun_out/plain2.log 2>&1 && \
-timeout 1500 ncu --set full --clock-control none --import-source on -k regex:stream_kernel -s 1 -c 1 -o gpurun_out/prof_stream3 python bench.py $ARGS2 > gpurun_out/ncu_stream.log 2>&1; echo "stream full rc=$?"
+CMD="python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e"
+timeout 300 $CMD > gpurun_out/ncu_pre.json 2> gpurun_out/ncu_pre.err; rc=$?; echo "plain rc=$rc"
+if [ $rc -eq 0 ]; then
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_kernel --launch-skip 3 --launch-count 1 \
+    -o gpurun_out/stream_full -f $CMD > gpurun_out/ncu_run.log 2>&1; echo "ncu rc=$?"; tail -3 gpurun_out/ncu_run.log
+fi
+ls -la gpurun_out/stream_full.ncu-rep
