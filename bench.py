@@ -323,6 +323,23 @@ def run_b200(args):
                           f"{r['seconds']:.1f} s: reference transform() restated in C++ (oracle/), fp64, "
                           f"columns A*s_ell pre-materialised in host DRAM because the 275 GB fp64 sketch "
                           f"exceeds host RAM")}
+        # single-core transform, and the reference preprocessing on the
+        # host (all threads / 1 thread) on a bounded sample of bases, extrapolated to all 2048
+        r1 = cpu_sample(a64, X64, prob.seeds[:P], args.J, args.K, 1, min(3.0, args.cpu_seconds / 3))
+        cpu["single_core"] = {"value": r1["value"], "unit": "vectors/s", "cores": 1,
+                              "sample": f"{r1['vectors']} vectors, {r1['seconds']:.1f} s"}
+        from oracle import oracle as orc
+        nk = 2048
+        pre_all = orc.bench_preprocess(a64, threads, threads)
+        pre_one = orc.bench_preprocess(a64, 1, 1)
+        cpu["preprocess"] = {
+            "unit": "s", "dtype": "f64",
+            "all_threads": {"cores": threads, "sample_bases": threads, "sample_s": pre_all,
+                            "extrapolated_s": pre_all * nk / threads},
+            "one_thread": {"cores": 1, "sample_bases": 1, "sample_s": pre_one, "extrapolated_s": pre_one * nk},
+            "note": ("reference per-basis preprocessing (kerdock_matrix + masked FWHT + transposed stores, "
+                     "sketch.hpp:171-196) timed on the first bases and scaled to 2048 Kerdock bases; the full "
+                     "275 GB fp64 sketch does not fit host RAM")}
 
     line = {
         "metric": METRIC if args.config == "3" else f"thresholded-Ax vectors/sec ({cfg['desc'].split(':')[0]})",

@@ -224,6 +224,37 @@ const T* Sketch<T>::column(std::int64_t ell) const {  // sketch.hpp:114-117
   return columns.data() + ell * m;
 }
 
+// sketch.hpp:171-196 for one Kerdock basis: signs Q_s(pos) (176-179), rows in
+// 32-row tiles masked + zero padded (182-186), unnormalised FWHT (187),
+// transposed write into the basis' d columns of m values (191-196).
+template <typename T>
+void kerdock_block(const T* a, std::int64_t m, std::int64_t n, const DesignParams& design, const std::uint64_t* mat,
+                   T* block, std::vector<T>& sign, std::vector<T>& tile) {
+  constexpr std::int64_t kRowTile = 32;
+  const std::int64_t d = design.d;
+  sign.resize(static_cast<std::size_t>(d));
+  tile.resize(static_cast<std::size_t>(kRowTile * d));
+  for (std::int64_t j = 0; j < d; ++j)
+    sign[j] = quadratic_form(mat, design.k, coords_of_position(static_cast<std::uint64_t>(j), design.k)) ? T(-1) : T(1);
+  for (std::int64_t i0 = 0; i0 < m; i0 += kRowTile) {
+    const std::int64_t rows = std::min(kRowTile, m - i0);
+    for (std::int64_t r = 0; r < rows; ++r) {
+      T* buf = tile.data() + r * d;
+      const T* arow = a + (i0 + r) * n;
+      for (std::int64_t j = 0; j < n; ++j) buf[j] = sign[j] * arow[j];
+      std::fill(buf + n, buf + d, T(0));
+      fwht_unnormalized(buf, static_cast<std::size_t>(d));
+    }
+    for (std::int64_t w = 0; w < d; ++w) {
+      T* dst = block + w * m + i0;
+      const T* src = tile.data() + w;
+      for (std::int64_t r = 0; r < rows; ++r) dst[r] = src[r * d];
+    }
+  }
+}
+template void kerdock_block<double>(const double*, std::int64_t, std::int64_t, const DesignParams&,
+                                    const std::uint64_t*, double*, std::vector<double>&, std::vector<double>&);
+
 template <typename T>
 Sketch<T> preprocess(const T* a, std::int64_t m, std::int64_t n, int threads) {
   // sketch.hpp:149-211. Per Kerdock basis s: sign table (176-179), 32-row tiles
@@ -250,32 +281,9 @@ Sketch<T> preprocess(const T* a, std::int64_t m, std::int64_t n, int threads) {
 
   T* cols = sk.columns.data();
   auto work = [&](std::int64_t s_first, std::int64_t s_last) {
-    constexpr std::int64_t kRowTile = 32;
-    std::vector<T> sign(static_cast<std::size_t>(d));
-    std::vector<T> tile(static_cast<std::size_t>(kRowTile * d));
-    for (std::int64_t s = s_first; s < s_last; ++s) {
-      const auto& mat = sk.kerdock[s];
-      for (std::int64_t j = 0; j < d; ++j)
-        sign[j] = quadratic_form(mat.data(), sk.design.k,
-                                 coords_of_position(static_cast<std::uint64_t>(j), sk.design.k))
-                      ? T(-1)
-                      : T(1);
-      for (std::int64_t i0 = 0; i0 < m; i0 += kRowTile) {
-        const std::int64_t rows = std::min(kRowTile, m - i0);
-        for (std::int64_t r = 0; r < rows; ++r) {
-          T* buf = tile.data() + r * d;
-          const T* arow = a + (i0 + r) * n;
-          for (std::int64_t j = 0; j < n; ++j) buf[j] = sign[j] * arow[j];
-          std::fill(buf + n, buf + d, T(0));
-          fwht_unnormalized(buf, static_cast<std::size_t>(d));
-        }
-        for (std::int64_t w = 0; w < d; ++w) {
-          T* dst = cols + (s * d + w) * m + i0;
-          const T* src = tile.data() + w;
-          for (std::int64_t r = 0; r < rows; ++r) dst[r] = src[r * d];
-        }
-      }
-    }
+    std::vector<T> sign, tile;
+    for (std::int64_t s = s_first; s < s_last; ++s)
+      kerdock_block(a, m, n, sk.design, sk.kerdock[s].data(), cols + s * d * m, sign, tile);
   };
   // sketch.hpp:37-53: fork-join over disjoint basis ranges (schedule-invariant).
   threads = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(threads, nk)));

@@ -99,6 +99,10 @@ struct Sketch {
 };
 template <typename T>
 Sketch<T> preprocess(const T* a, std::int64_t m, std::int64_t n, int threads = 1);
+/// sketch.hpp:171-196 for one basis: block = its d columns of m values.
+template <typename T>
+void kerdock_block(const T* a, std::int64_t m, std::int64_t n, const DesignParams& design, const std::uint64_t* mat,
+                   T* block, std::vector<T>& sign, std::vector<T>& tile);
 
 // ---------------------------------------------------------------- rng.hpp --
 

@@ -536,3 +536,12 @@ def verify_kerdock_set(k: int):
     bad = C.c_int64()
     _check(lib().orc_verify_kerdock_set(C.c_int(k), C.byref(skew), C.byref(bad)))
     return bool(skew.value), int(bad.value)
+
+
+def bench_preprocess(a, bases: int, threads: int) -> float:
+    """Wall seconds of the reference per-basis preprocessing for the first `bases` Kerdock bases."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    secs = C.c_double()
+    _check(lib().orc_bench_preprocess(_ptr(a), C.c_int64(a.shape[0]), C.c_int64(a.shape[1]), C.c_int64(bases),
+                                      C.c_int(threads), C.byref(secs)))
+    return secs.value

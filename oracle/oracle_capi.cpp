@@ -551,4 +551,32 @@ int orc_verify_kerdock_set(int k, int* skew, std::int64_t* bad_pairs) {
   });
 }
 
+// Reference preprocessing timed on a bounded sample (bench.py's CPU leg): the
+// first `bases` Kerdock bases of A's sketch (kerdock_matrix + kerdock_block,
+// the reference's per-basis work) spread over `threads` threads, each writing
+// into its own basis-sized scratch block. Wall seconds.
+int orc_bench_preprocess(const double* a, std::int64_t m, std::int64_t n, std::int64_t bases, int threads,
+                         double* seconds) {
+  return guarded([&] {
+    const DesignParams p = DesignParams::make(even_log2_ceil(n));
+    bases = std::min<std::int64_t>(bases, p.kerdock_bases());
+    threads = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(threads, bases)));
+    std::vector<std::vector<double>> blocks(static_cast<std::size_t>(threads));
+    for (auto& b : blocks) b.assign(static_cast<std::size_t>(p.d * m), 0.0);  // touched before timing
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) {
+      pool.emplace_back([&, t] {
+        std::vector<double> sign, tile;
+        for (std::int64_t s = t; s < bases; s += threads) {
+          const auto mat = kerdock_matrix(p, static_cast<std::uint64_t>(s));
+          kerdock_block(a, m, n, p, mat.data(), blocks[t].data(), sign, tile);
+        }
+      });
+    }
+    for (auto& th : pool) th.join();
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
 }  // extern "C"
