@@ -792,8 +792,13 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   const bool all_dev = x_dev && o_dev && (seeds == nullptr || seeds_dev) && (indices == nullptr || idx_dev);
 
   // Chunking bounds scratch (indices: chunk x N x 4 bytes) and pipelines host copies.
-  int64_t chunk = all_dev ? B : std::min<int64_t>(B, 4096);
+  // Host buffers: chunks grow geometrically from kFirstChunk to kMaxChunk vectors, so
+  // the one copy that cannot overlap (the first chunk's H2D) is short while later
+  // launches are long (each launch pays a pipeline fill and an unoverlapped tail).
+  constexpr int64_t kFirstChunk = 2048, kMaxChunk = 16384;
+  int64_t chunk = all_dev ? B : std::min<int64_t>(B, kMaxChunk);
   chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, (int64_t(1) << 29) / std::max<int64_t>(N, 1)));
+  int64_t next_chunk = all_dev ? chunk : std::min<int64_t>(chunk, kFirstChunk);
 
   StreamArgs<T> args{};
   args.cols = static_cast<const T*>(sk->cols);
@@ -832,9 +837,15 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
     args.debug = dbg ? std::atoi(dbg) : 0;
   }
 
+  // Host buffers: H2D of chunk i+1 and D2H of chunk i-1 run on their own streams while
+  // chunk i computes (one shared copy stream would queue the next H2D behind the
+  // previous chunk's D2H, which waits for that chunk's kernel).
   const int nbuf = all_dev ? 1 : 2;
-  cudaStream_t copy_st = nullptr;
-  if (!all_dev) cuda_check(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking), "stream");
+  cudaStream_t copy_st = nullptr, out_st = nullptr;
+  if (!all_dev) {
+    cuda_check(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking), "stream");
+    cuda_check(cudaStreamCreateWithFlags(&out_st, cudaStreamNonBlocking), "stream");
+  }
   struct Bufs {
     DevBuf X, idx, counts, support, values, cands, mu, seeds, idx64;
   };
@@ -863,8 +874,9 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   if (!all_dev) cuda_check(cudaStreamSynchronize(st), "sync allocations");
 
   int it = 0;
-  for (int64_t v0 = 0; v0 < B; v0 += chunk, ++it) {
-    const int64_t cb = std::min(chunk, B - v0);
+  for (int64_t v0 = 0, cb = 0; v0 < B; v0 += cb, ++it) {
+    cb = std::min(next_chunk, B - v0);
+    next_chunk = std::min(chunk, next_chunk * 2);
     const int b = it % nbuf;
     Bufs& bf = bufs[b];
     // ---- inputs ----
@@ -929,16 +941,16 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
     if (!all_dev) {
       cuda_check(cudaEventRecord(ev_done[b], st), "event");
       if (!o_dev) {
-        cuda_check(cudaStreamWaitEvent(copy_st, ev_done[b], 0), "wait");
+        cuda_check(cudaStreamWaitEvent(out_st, ev_done[b], 0), "wait");
         auto d2h = [&](void* dst, const void* src, size_t bytes) {
-          cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, copy_st), "D2H");
+          cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, out_st), "D2H");
         };
         d2h(out.counts + v0, bf.counts.p, size_t(cb) * sizeof(int32_t));
         d2h(out.support + v0 * want, bf.support.p, size_t(cb) * want * sizeof(int32_t));
         d2h(static_cast<T*>(out.values) + v0 * want, bf.values.p, size_t(cb) * want * sizeof(T));
         if (out.cands) d2h(out.cands + v0 * want, bf.cands.p, size_t(cb) * want * sizeof(int32_t));
         if (out.mu) d2h(static_cast<T*>(out.mu) + v0 * m, bf.mu.p, size_t(cb) * m * sizeof(T));
-        cuda_check(cudaEventRecord(ev_out[b], copy_st), "event");
+        cuda_check(cudaEventRecord(ev_out[b], out_st), "event");
       } else {
         cuda_check(cudaEventRecord(ev_out[b], st), "event");
       }
@@ -952,8 +964,10 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   }
   if (!all_dev) {
     cuda_check(cudaStreamSynchronize(copy_st), "sync copies");
+    cuda_check(cudaStreamSynchronize(out_st), "sync copies");
     cuda_check(cudaStreamSynchronize(st), "sync compute");
     cudaStreamDestroy(copy_st);
+    cudaStreamDestroy(out_st);
   }
   for (int b = 0; b < nbuf; ++b) {
     cudaEventDestroy(ev_in[b]);

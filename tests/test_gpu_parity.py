@@ -344,3 +344,28 @@ def test_preprocess_shards_assemble_full_sketch(fst, orc):
     assert torch.equal(t0, t_full)
     with pytest.raises(IndexError):
         fst.preprocess_shard(a, 0, nk + 1, True)
+
+
+def test_host_buffers_chunked_equal_device_path(fst):
+    """Host-buffer batches run in growing chunks (2048, 4096, ... vectors) with
+    copies overlapped on a second stream; every output must equal the
+    device-resident path bit for bit (B = 7000: chunks 2048 + 4096 + 856)."""
+    import torch
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((200, 256)).astype(np.float32)
+    sk = fst.preprocess(a)
+    B = 7000
+    X = rng.standard_normal((B, 256)).astype(np.float32)
+    seeds = rng.integers(0, 2**63, size=B, dtype=np.int64)
+    p = fst.StreamParams(epsilon=0.5, s=4, J=20, K=3)
+    dev = fst.transform_batch(sk, torch.from_numpy(X).cuda(), p, seeds=torch.from_numpy(seeds).cuda(),
+                              candidates=True, mu=True)
+    host = fst.transform_batch(sk, X, p, seeds=seeds.view(np.uint64), candidates=True, mu=True)
+    counts = dev.counts.cpu().numpy()
+    assert np.array_equal(counts, host.counts)
+    valid = np.arange(dev.support.shape[1])[None, :] < counts[:, None]   # entries past counts[v] are unspecified
+    assert np.array_equal(dev.support.cpu().numpy()[valid], host.support[valid])
+    assert np.array_equal(dev.values.cpu().numpy()[valid], host.values[valid])
+    assert np.array_equal(dev.candidates.cpu().numpy(), host.candidates)
+    assert np.array_equal(dev.mu.cpu().numpy(), host.mu)
+    sk.close()
