@@ -212,6 +212,17 @@ int fstg_transform_gathered_batch(const fstg_sketch* sk, const void* X, int64_t 
                                   const int64_t* indices, const void* gathered, int32_t* counts, int32_t* support,
                                   void* values, int32_t* candidates, void* mu, void* stream);
 
+/* transform (stream.hpp:272-275) for a batch on a sketch whose columns need not
+ * exist (fstg_preprocess_design; n = 16384): the draws, then per block of
+ * row_block rows (0 = as many as ~70% of free device memory holds) the
+ * retain-sampled FWHT of those rows of every sampled column and the estimator's
+ * batch sums for those rows, then median / top-want / refinement. One Kerdock
+ * pass per call; batch means bit-identical to fstg_transform_batch on the full
+ * sketch. X, seeds and outputs in device memory. */
+int fstg_transform_design_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p,
+                                const uint64_t* seeds, int64_t row_block, int32_t* counts, int32_t* support,
+                                void* values, int32_t* candidates, void* mu, void* stream);
+
 /* ------------------------------------------------------ design verifiers --- */
 /* kerdock.hpp:198-317, cli.hpp:45-82, on the GPU (sign tables of the design
  * expanded on `device`). All reported quantities are exact: every inner

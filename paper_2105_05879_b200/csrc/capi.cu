@@ -393,13 +393,14 @@ __global__ void basis_ranges_kernel(const uint64_t* __restrict__ sorted, int64_t
 }
 
 template <typename T>
-__global__ void identity_requests_kernel(const T* __restrict__ a, int64_t lda, int64_t m, int64_t n, int64_t kb, T sqrt_d,
-                                         const uint64_t* __restrict__ ell, const int64_t* __restrict__ pos,
-                                         int64_t first, int64_t count, T* __restrict__ out, int64_t ldc) {
+__global__ void identity_requests_kernel(const T* __restrict__ a, int64_t lda, int64_t row0, int64_t row1, int64_t n,
+                                         int64_t kb, T sqrt_d, const uint64_t* __restrict__ ell,
+                                         const int64_t* __restrict__ pos, int64_t first, int64_t count,
+                                         T* __restrict__ out, int64_t ldc) {
   for (int64_t r = first + blockIdx.x; r < count; r += gridDim.x) {
     const int64_t w = static_cast<int64_t>(ell[r]) - kb;
-    T* dst = out + pos[r] * ldc;
-    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) dst[i] = (w < n) ? sqrt_d * a[i * lda + w] : T(0);
+    T* dst = out + pos[r] * ldc - row0;
+    for (int64_t i = row0 + threadIdx.x; i < row1; i += blockDim.x) dst[i] = (w < n) ? sqrt_d * a[i * lda + w] : T(0);
   }
 }
 
@@ -420,7 +421,14 @@ __global__ void check_range_kernel(const int64_t* in, int64_t count, int64_t L, 
 }
 
 template <typename T>
-void sample_columns_impl(const fstg_sketch* sk, const int64_t* indices, int64_t count, void* out, cudaStream_t st) {
+// Columns A s_ell (rows [row0, row1), column j at out + j * ldc_out) for the requested
+// indices: the retain-sampled FWHT plus the identity-block gather.
+void sample_columns_impl(const fstg_sketch* sk, const int64_t* indices, int64_t count, void* out, cudaStream_t st,
+                         int64_t row0 = 0, int64_t row1 = -1, int64_t ldc_out = 0) {
+  if (row1 < 0) row1 = sk->m;
+  if (ldc_out <= 0) ldc_out = row0 == 0 && row1 == sk->m ? sk->ldc : row1 - row0;
+  if (row0 < 0 || row1 > sk->m || row0 >= row1 || ldc_out < row1 - row0)
+    throw InvalidArgument("sample_columns: bad row range / column stride");
   if (!sk) throw InvalidArgument("sample_columns: null sketch");
   if (count < 0 || (count > 0 && (!indices || !out))) throw InvalidArgument("sample_columns: bad arguments");
   if (count == 0) return;
@@ -440,7 +448,7 @@ void sample_columns_impl(const fstg_sketch* sk, const int64_t* indices, int64_t 
   T* dst = static_cast<T*>(out);
   const bool out_is_dev = is_device_ptr(out);
   if (!out_is_dev) {
-    out_buf = DevBuf(size_t(count) * sk->ldc * sizeof(T), st);
+    out_buf = DevBuf(size_t(count) * ldc_out * sizeof(T), st);
     dst = out_buf.as<T>();
   }
   cuda_check(cudaMemsetAsync(bad.p, 0, sizeof(int), st), "memset");
@@ -461,10 +469,10 @@ void sample_columns_impl(const fstg_sketch* sk, const int64_t* indices, int64_t 
   cuda_check(cudaGetLastError(), "basis ranges");
   {
     ProfScope ps("sample_columns_fwht", st);
-    const cudaError_t e = launch_fwht_retain<T>(D.k, static_cast<const T*>(sk->a), sk->lda, sk->m, sk->n, sk->qplain,
-                                                nk, dst, sk->ldc, start.as<int64_t>(),
+    const cudaError_t e = launch_fwht_retain<T>(D.k, static_cast<const T*>(sk->a), sk->lda, row1, sk->n, sk->qplain,
+                                                nk, dst, ldc_out, start.as<int64_t>(),
                                                 reinterpret_cast<const int64_t*>(keys_sorted.p), pos_sorted.as<int64_t>(),
-                                                st);
+                                                st, row0);
     if (e == cudaErrorNotSupported) {
       cudaGetLastError();
       throw NotSupported("sample_columns: this (k, dtype) needs more than 227 KiB of shared memory per CTA");
@@ -479,16 +487,16 @@ void sample_columns_impl(const fstg_sketch* sk, const int64_t* indices, int64_t 
     if (first < count) {
       ProfScope ps("sample_columns_identity", st);
       identity_requests_kernel<T><<<static_cast<unsigned>(std::min<int64_t>(count - first, 148 * 16)), 256, 0, st>>>(
-          static_cast<const T*>(sk->a), sk->lda, sk->m, sk->n, nk * D.d,
+          static_cast<const T*>(sk->a), sk->lda, row0, row1, sk->n, nk * D.d,
           static_cast<T>(std::sqrt(static_cast<double>(D.d))), keys_sorted.as<uint64_t>(), pos_sorted.as<int64_t>(),
-          first, count, dst, sk->ldc);
+          first, count, dst, ldc_out);
       cuda_check(cudaGetLastError(), "identity requests");
     }
   }
   int h = 0;
   cuda_check(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st), "flag");
   if (!out_is_dev)
-    cuda_check(cudaMemcpyAsync(out, dst, size_t(count) * sk->ldc * sizeof(T), cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaMemcpyAsync(out, dst, size_t(count) * ldc_out * sizeof(T), cudaMemcpyDeviceToHost, st), "D2H");
   cuda_check(cudaStreamSynchronize(st), "sync");
   if (h) throw OutOfRange("Sketch::column: index out of range");
 }
@@ -974,6 +982,136 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
     cudaEventDestroy(ev_done[b]);
     cudaEventDestroy(ev_out[b]);
   }
+}
+
+// ------------------------------------------- row-blocked design transform ----
+// transform (stream.hpp:272-275) on a design-only sketch whose columns cannot
+// exist (n = 16384: 8.8 TB). Rows of the estimator are independent — row i's
+// batch sum is sum_j t_j C[i, ell_j] in j order — so the columns are produced
+// and consumed one row block at a time: per block, the retain-sampled FWHT
+// computes rows [r0, r1) of every sampled column of every vector (one pass over
+// all Kerdock bases for those rows only), and the stream kernel in PARTIAL mode
+// writes those rows of each vector's K batch means to means_io. Then TAIL mode
+// runs median / select / refinement from means_io. Per call the Kerdock work is
+// ONE full pass whatever the batch size (vector chunks would each need a full
+// pass), and the batch means are bit-identical to the full-column path.
+template <typename T>
+void transform_design_impl(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p,
+                           const uint64_t* seeds, int64_t row_block, const Outputs& out, cudaStream_t st) {
+  validate(p);
+  if (B < 0) throw InvalidArgument("transform_design: negative batch size");
+  if (B == 0) return;
+  if (X == nullptr || out.counts == nullptr || out.support == nullptr || out.values == nullptr)
+    throw InvalidArgument("transform_design: X and counts/support/values must be non-null");
+  if (!sk->has_a) throw CodedError(FSTG_ERR_NO_MATRIX, "Sketch: no embedded matrix");
+  if (!is_device_ptr(X) || !is_device_ptr(out.counts) || !is_device_ptr(out.support) || !is_device_ptr(out.values) ||
+      (out.cands && !is_device_ptr(out.cands)) || (out.mu && !is_device_ptr(out.mu)) ||
+      (seeds && !is_device_ptr(seeds)))
+    throw InvalidArgument("transform_design: X, seeds and outputs must be device memory");
+  if (p->mode < 0 || p->mode > 2) throw InvalidArgument("StreamParams: unknown mode");
+  const bool strict = p->mode == FSTG_MODE_STRICT || (p->mode == FSTG_MODE_DEFAULT && sk->dtype == FSTG_F64);
+  const Design& D = sk->design;
+  const int64_t N = p->J * p->K, m = sk->m, n = sk->n;
+  if (N > (int64_t(1) << 40)) throw NotSupported("transform: J*K too large for this build");
+  const int64_t want = candidate_count(p->s, p->widen, m);
+  cuda_check(cudaSetDevice(sk->device), "cudaSetDevice");
+  keep_pool_warm(sk->device);
+
+  // indices: int64 for the retain FWHT, uint32 for the stream kernel (same draws)
+  DevBuf idx64(size_t(B) * N * 8, st), idx32(size_t(B) * N * 4, st);
+  {
+    ProfScope ps("draw", st);
+    cuda_check(launch_draw<int64_t>(seeds, p->seed, B, N, static_cast<uint64_t>(D.L), idx64.as<int64_t>(), st), "draw");
+  }
+  {
+    ProfScope ps("draw", st);
+    cuda_check(launch_draw<uint32_t>(seeds, p->seed, B, N, static_cast<uint64_t>(D.L), idx32.as<uint32_t>(), st),
+               "draw");
+  }
+  const int64_t m_io = sk->ldc;
+  DevBuf means_io(size_t(B) * (p->K + 1) * m_io * sizeof(T), st);
+
+  StreamArgs<T> args{};
+  args.a = static_cast<const T*>(sk->a);
+  args.lda = sk->lda;
+  args.qplain = sk->qplain;
+  args.qtrans = sk->qtrans;
+  args.revtab = sk->revtab;
+  args.k = D.k;
+  args.d = D.d;
+  args.L = D.L;
+  args.n = n;
+  args.kb = D.kerdock_bases() * D.d;
+  args.J = p->J;
+  args.K = p->K;
+  args.N = N;
+  args.want = want;
+  args.epsilon = p->epsilon;
+  args.X = static_cast<const T*>(X);
+  args.ldx = n;
+  args.idx = idx32.as<uint32_t>();
+  args.B = B;
+  args.counts = out.counts;
+  args.support = out.support;
+  args.values = static_cast<T*>(out.values);
+  args.cands = out.cands;
+  args.mu = static_cast<T*>(out.mu);
+  args.means_io = means_io.as<T>();
+  args.m_io = m_io;
+  {
+    const char* dbg = std::getenv("FSTG_STREAM_DEBUG");
+    args.debug = dbg ? std::atoi(dbg) : 0;
+  }
+  constexpr int64_t SEG = 16384 / sizeof(T), ALIGN = 16 / sizeof(T);
+  auto launch = [&](const char* name) {
+    if (args.nseg > 4) throw NotSupported("transform: m too large for this GPU build (m <= 4 * 16 KiB / sizeof(T))");
+    size_t smem = 0;
+    int stages = 0, stage_stride = 0, rstride = 0, xbufs = 0;
+    const int grid = stream_grid_size<T>(args, strict, B, &smem, &stages, &stage_stride, &rstride, &xbufs);
+    if (smem > 227 * 1024) throw NotSupported("transform: shared-memory plan exceeds 227 KiB (d or want too large)");
+    args.stages = stages;
+    args.stage_stride = stage_stride;
+    args.rstride = rstride;
+    args.xbufs = xbufs;
+    DevBuf scratch(size_t(stream_scratch_elems<T>(args, grid)) * sizeof(T), st);
+    args.means = scratch.as<T>();
+    ProfScope ps(name, st);
+    cuda_check(launch_stream<T>(args, strict, grid, st), "stream kernel");
+  };
+
+  // row blocks: as many rows as ~70% of free device memory holds (or the caller's row_block)
+  const int64_t per_row = B * N * int64_t(sizeof(T));
+  if (row_block <= 0) {
+    size_t free_b = 0, total_b = 0;
+    cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+    row_block = std::max<int64_t>(ALIGN, int64_t(double(free_b) * 0.7) / std::max<int64_t>(per_row, 1));
+  }
+  row_block = std::max<int64_t>(ALIGN, row_block / ALIGN * ALIGN);
+  for (int64_t r0 = 0; r0 < m; r0 += row_block) {
+    const int64_t r1 = std::min(m, r0 + row_block);
+    const int64_t ldh = (r1 - r0 + ALIGN - 1) / ALIGN * ALIGN;
+    DevBuf cols(size_t(B) * N * ldh * sizeof(T), st);
+    sample_columns_impl<T>(sk, idx64.as<int64_t>(), B * N, cols.p, st, r0, r1, ldh);
+    args.means_mode = kMeansPartial;
+    args.cols = nullptr;
+    args.gathered = cols.as<T>();
+    args.ldc = ldh;
+    args.m = r1 - r0;
+    args.m_pad = ldh;
+    args.row0 = r0;
+    args.nseg = static_cast<int>((ldh + SEG - 1) / SEG);
+    launch("stream_partial");
+  }
+  args.means_mode = kMeansTail;
+  args.gathered = nullptr;
+  args.cols = nullptr;
+  args.ldc = m_io;
+  args.m = m;
+  args.m_pad = m_io;
+  args.row0 = 0;
+  args.nseg = static_cast<int>((m_io + SEG - 1) / SEG);
+  launch("stream_tail");
+  cuda_check(cudaStreamSynchronize(st), "sync");
 }
 
 // ----------------------------------------------------- design verifiers ----
@@ -1502,6 +1640,19 @@ double fstg_design_moment_target(int64_t d, int k) {  // kerdock.hpp:267-276
 
 int fstg_verify_kerdock_set(int k, int device, int* skew_symmetric, int64_t* bad_pairs) {
   return guarded([&] { verify_kerdock_set_impl(k, device, skew_symmetric, bad_pairs); });
+}
+
+int fstg_transform_design_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p,
+                                const uint64_t* seeds, int64_t row_block, int32_t* counts, int32_t* support,
+                                void* values, int32_t* candidates, void* mu, void* stream) {
+  return guarded([&] {
+    if (!sk) throw InvalidArgument("null sketch");
+    const Outputs o{counts, support, values, candidates, mu};
+    if (sk->dtype == FSTG_F32)
+      transform_design_impl<float>(sk, X, B, p, seeds, row_block, o, static_cast<cudaStream_t>(stream));
+    else
+      transform_design_impl<double>(sk, X, B, p, seeds, row_block, o, static_cast<cudaStream_t>(stream));
+  });
 }
 
 }  // extern "C"

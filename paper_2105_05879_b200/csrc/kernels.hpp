@@ -14,11 +14,12 @@ template <typename T>
 cudaError_t launch_fwht_sketch(int k, const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
                                int64_t basis_begin, int64_t basis_end, T* cols, int64_t ldc, cudaStream_t st);
 // Retain-sampled FWHT: only requested columns (sorted by ell; basis s owns
-// [req_start[s], req_start[s+1])) are written, to out[req_pos[r] * ldc].
+// [req_start[s], req_start[s+1])) are written, to out[req_pos[r] * ldc], for
+// rows [row0, m) (row i lands at out[... + i - row0]).
 template <typename T>
 cudaError_t launch_fwht_retain(int k, const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
                                int64_t nbases, T* out, int64_t ldc, const int64_t* req_start, const int64_t* req_ell,
-                               const int64_t* req_pos, cudaStream_t st);
+                               const int64_t* req_pos, cudaStream_t st, int64_t row0 = 0);
 template <typename T>
 cudaError_t launch_identity(const T* a, int64_t lda, int64_t m, int64_t n, int64_t d, int64_t nk, T* cols,
                             int64_t ldc, cudaStream_t st);
@@ -85,14 +86,25 @@ struct StreamArgs {
   int stages;
   int stage_stride;  // bytes between ring stages (>= one segment, 128-byte multiple)
   int rstride;       // bytes per refinement-ring stage (one row of A); 0 = direct loads
-  int xbufs;         // x buffers in shared memory (3, or 2 when d is large)
+  int xbufs;         // x buffers in shared memory
   int nseg;
   int chunk;
+  // Row-blocked design-only transform (fstg_transform_design_batch):
+  //   kMeansFull    the whole pipeline (default)
+  //   kMeansPartial columns hold rows [row0, row0 + m) only (m_pad = their padded height);
+  //                 the batch means of those rows go to means_io, no tail
+  //   kMeansTail    no columns: median / select / refinement from means_io (m_pad = m_io)
+  // means_io: B x (K + 1) x m_io (K batch means, then mu written by the tail).
+  int means_mode;
+  T* means_io;
+  int64_t m_io, row0;
   // experiment switches (env FSTG_STREAM_DEBUG; 0 in production):
   // bit 0: column pipeline only (coefficient warps idle, t = 1)
   // bit 1: coefficient pipeline only (no column loads, consumers skip the ring)
+  // bit 2: no refinement; bit 3: per-role mbarrier wait profile
   int debug;
 };
+enum MeansMode { kMeansFull = 0, kMeansPartial = 1, kMeansTail = 2 };
 
 template <typename T>
 cudaError_t launch_stream(const StreamArgs<T>& args, bool strict, int grid, cudaStream_t st);

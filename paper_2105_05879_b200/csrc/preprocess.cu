@@ -170,14 +170,14 @@ __global__ void __launch_bounds__(NT) fwht_sketch_kernel(const T* __restrict__ a
                                                          int64_t basis_end, int bases_per_cta, T* __restrict__ cols,
                                                          int64_t ldc, const int64_t* __restrict__ req_start,
                                                          const int64_t* __restrict__ req_ell,
-                                                         const int64_t* __restrict__ req_pos) {
+                                                         const int64_t* __restrict__ req_pos, int64_t row0) {
   using C = FwhtCfg<T, KB, NT>;
   constexpr int E = C::E, R = C::R, RS = C::RS, D = C::D, SW = C::SW;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* tile = reinterpret_cast<T*>(smem_raw);
 
   const int tid = threadIdx.x;
-  const int64_t i0 = int64_t(blockIdx.x) * R;
+  const int64_t i0 = row0 + int64_t(blockIdx.x) * R;  // rows [row0, m): retain-sampled row blocks
   const int64_t s_first = basis_begin + int64_t(blockIdx.y) * bases_per_cta;
   const int64_t s_last = min(basis_end, s_first + bases_per_cta);
   const uint64_t pol_keep = policy_evict_last();
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(NT) fwht_sketch_kernel(const T* __restrict__ a
         const int64_t r = r_lo + it / R;
         const int rr = static_cast<int>(it % R);
         const int64_t w = req_ell[r] - s * D;
-        if (i0 + rr < m) cols[req_pos[r] * ldc + i0 + rr] = tile[w * R + rr];
+        if (i0 + rr < m) cols[req_pos[r] * ldc + (i0 - row0) + rr] = tile[w * R + rr];
       }
       continue;  // the next basis' first __syncthreads orders the tile reuse
     }
@@ -333,8 +333,15 @@ struct TmemCfg {
   static constexpr int HALF = KB / 2;
   static constexpr int E = 1 << HALF;
   static constexpr int D = 1 << KB;
-  static constexpr int NT = (KB == 12) ? 512 : 256;
+  // k = 14: one row per CTA (128 threads, 65 KiB tile) so two CTAs share an SM and
+  // overlap each other's transpose barriers (register-limited to 2 x 128 x 256).
+#ifndef FSTG_K14_NT
+#define FSTG_K14_NT 128
+#endif
+  static constexpr int NT = (KB == 12) ? 512 : FSTG_K14_NT;
+  static constexpr int MIN_CTAS = (KB == 12 || NT > 128) ? 1 : 2;
   static constexpr int R = NT / E;
+  static constexpr int TCOLS = E * ((NT / 32 + 3) / 4);  // TMEM columns: E per warp, 4 warps share a column range
   static constexpr int RS = D + 32 / R;          // row stride (floats): phase-2 reads conflict-free
   static constexpr int WPT = E / 32;             // sign words per thread
   static constexpr int CH = E / 4;               // 16-byte chunks per thread
@@ -343,10 +350,11 @@ struct TmemCfg {
 };
 
 template <int KB, bool RETAIN>
-__global__ void __launch_bounds__(TmemCfg<KB>::NT, 1) fwht_tmem_kernel(
+__global__ void __launch_bounds__(TmemCfg<KB>::NT, TmemCfg<KB>::MIN_CTAS) fwht_tmem_kernel(
     const float* __restrict__ a, int64_t lda, int64_t m, int64_t n, const uint32_t* __restrict__ qplain,
     int64_t basis_begin, int64_t basis_end, int bases_per_cta, float* __restrict__ cols, int64_t ldc,
-    const int64_t* __restrict__ req_start, const int64_t* __restrict__ req_ell, const int64_t* __restrict__ req_pos) {
+    const int64_t* __restrict__ req_start, const int64_t* __restrict__ req_ell, const int64_t* __restrict__ req_pos,
+    int64_t row0) {
   using C = TmemCfg<KB>;
   constexpr int E = C::E, R = C::R, RS = C::RS, D = C::D, NT = C::NT, WPT = C::WPT, CH = C::CH, SWC = C::SWC;
   constexpr int WPB = D / 32;
@@ -355,7 +363,7 @@ __global__ void __launch_bounds__(TmemCfg<KB>::NT, 1) fwht_tmem_kernel(
   __shared__ uint32_t tmem_base_slot;
 
   const int tid = threadIdx.x, warp = tid / 32;
-  const int64_t i0 = int64_t(blockIdx.x) * R;
+  const int64_t i0 = row0 + int64_t(blockIdx.x) * R;  // rows [row0, m): retain-sampled row blocks
   const int64_t s_first = basis_begin + int64_t(blockIdx.y) * bases_per_cta;
   const int64_t s_last = min(basis_end, s_first + bases_per_cta);
   const int r1 = tid / E, p1 = tid % E;
@@ -364,7 +372,8 @@ __global__ void __launch_bounds__(TmemCfg<KB>::NT, 1) fwht_tmem_kernel(
   const int64_t row2 = i0 + r2;
 
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&tmem_base_slot))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_slot)),
+                 "n"(C::TCOLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -451,7 +460,7 @@ __global__ void __launch_bounds__(TmemCfg<KB>::NT, 1) fwht_tmem_kernel(
         const int64_t r = r_lo + it / R;
         const int rr = static_cast<int>(it % R);
         const int64_t w = req_ell[r] - s * D;
-        if (i0 + rr < m) cols[req_pos[r] * ldc + i0 + rr] = tile[w * R + rr];
+        if (i0 + rr < m) cols[req_pos[r] * ldc + (i0 - row0) + rr] = tile[w * R + rr];
       }
     } else if (row2 < m) {
       // transposed write-back (sketch.hpp:191-196): column s*d + e*E + q2, row row2
@@ -469,7 +478,8 @@ __global__ void __launch_bounds__(TmemCfg<KB>::NT, 1) fwht_tmem_kernel(
 
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem_base_slot) : "memory");
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_slot), "n"(C::TCOLS) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -529,7 +539,7 @@ template <typename T, int KB, bool RETAIN = false>
 static cudaError_t launch_fwht_k(const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
                                  int64_t b0, int64_t b1, T* cols, int64_t ldc, cudaStream_t st,
                                  const int64_t* req_start = nullptr, const int64_t* req_ell = nullptr,
-                                 const int64_t* req_pos = nullptr) {
+                                 const int64_t* req_pos = nullptr, int64_t row0 = 0) {
   constexpr int NT = (sizeof(T) == 8 && KB >= 12) ? 256 : ((KB >= 14) ? 256 : 512);
   using C = FwhtCfg<T, KB, NT>;
   static_assert(C::R >= 1, "rows per CTA");
@@ -542,67 +552,69 @@ static cudaError_t launch_fwht_k(const T* a, int64_t lda, int64_t m, int64_t n, 
   }
   const int64_t nb = b1 - b0;
   if (nb <= 0) return cudaSuccess;
-  const int64_t row_tiles = (m + C::R - 1) / C::R;
+  const int64_t row_tiles = (m - row0 + C::R - 1) / C::R;
   // Bases per CTA: enough CTAs for >= 4 waves, at most 16 bases each.
   int bpc = 16;
   while (bpc > 1 && row_tiles * ((nb + bpc - 1) / bpc) < 148 * 8) bpc /= 2;
   const int64_t gy = (nb + bpc - 1) / bpc;
   if (row_tiles > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
   dim3 grid(static_cast<unsigned>(row_tiles), static_cast<unsigned>(gy));
-  kern<<<grid, NT, C::SMEM, st>>>(a, lda, m, n, qplain, b0, b1, bpc, cols, ldc, req_start, req_ell, req_pos);
+  kern<<<grid, NT, C::SMEM, st>>>(a, lda, m, n, qplain, b0, b1, bpc, cols, ldc, req_start, req_ell, req_pos, row0);
   return cudaGetLastError();
 }
 
 template <int KB, bool RETAIN>
 static cudaError_t launch_fwht_tmem(const float* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
                                     int64_t b0, int64_t b1, float* cols, int64_t ldc, cudaStream_t st,
-                                    const int64_t* req_start, const int64_t* req_ell, const int64_t* req_pos);
+                                    const int64_t* req_start, const int64_t* req_ell, const int64_t* req_pos,
+                                    int64_t row0);
 
 template <typename T>
 cudaError_t launch_fwht_retain(int k, const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
                                int64_t nbases, T* out, int64_t ldc, const int64_t* req_start, const int64_t* req_ell,
-                               const int64_t* req_pos, cudaStream_t st) {
+                               const int64_t* req_pos, cudaStream_t st, int64_t row0) {
   if constexpr (sizeof(T) == 4) {
     if (k == 12 && (lda % 4) == 0)
-      return launch_fwht_tmem<12, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
+      return launch_fwht_tmem<12, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos, row0);
     if (k == 14 && (lda % 4) == 0)
-      return launch_fwht_tmem<14, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
+      return launch_fwht_tmem<14, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos, row0);
   }
   switch (k) {
-    case 2: return launch_fwht_k<T, 2, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
-    case 4: return launch_fwht_k<T, 4, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
-    case 6: return launch_fwht_k<T, 6, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
-    case 8: return launch_fwht_k<T, 8, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
-    case 10: return launch_fwht_k<T, 10, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
-    case 12: return launch_fwht_k<T, 12, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
-    case 14: return launch_fwht_k<T, 14, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos);
+    case 2: return launch_fwht_k<T, 2, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos, row0);
+    case 4: return launch_fwht_k<T, 4, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos, row0);
+    case 6: return launch_fwht_k<T, 6, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos, row0);
+    case 8: return launch_fwht_k<T, 8, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos, row0);
+    case 10: return launch_fwht_k<T, 10, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos, row0);
+    case 12: return launch_fwht_k<T, 12, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos, row0);
+    case 14: return launch_fwht_k<T, 14, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos, row0);
     default: return cudaErrorNotSupported;
   }
 }
 template cudaError_t launch_fwht_retain<float>(int, const float*, int64_t, int64_t, int64_t, const uint32_t*, int64_t,
                                                float*, int64_t, const int64_t*, const int64_t*, const int64_t*,
-                                               cudaStream_t);
+                                               cudaStream_t, int64_t);
 template cudaError_t launch_fwht_retain<double>(int, const double*, int64_t, int64_t, int64_t, const uint32_t*, int64_t,
                                                 double*, int64_t, const int64_t*, const int64_t*, const int64_t*,
-                                                cudaStream_t);
+                                                cudaStream_t, int64_t);
 
 template <int KB, bool RETAIN>
 static cudaError_t launch_fwht_tmem(const float* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
                                     int64_t b0, int64_t b1, float* cols, int64_t ldc, cudaStream_t st,
-                                    const int64_t* req_start, const int64_t* req_ell, const int64_t* req_pos) {
+                                    const int64_t* req_start, const int64_t* req_ell, const int64_t* req_pos,
+                                    int64_t row0) {
   using C = TmemCfg<KB>;
   auto kern = fwht_tmem_kernel<KB, RETAIN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
   if (e != cudaSuccess) return e;
   const int64_t nb = b1 - b0;
   if (nb <= 0) return cudaSuccess;
-  const int64_t row_tiles = (m + C::R - 1) / C::R;
+  const int64_t row_tiles = (m - row0 + C::R - 1) / C::R;
   int bpc = RETAIN ? 256 : 32;  // the A tile is reused across bpc bases (TMEM)
   while (bpc > 1 && row_tiles * ((nb + bpc - 1) / bpc) < 148 * 8) bpc /= 2;
   const int64_t gy = (nb + bpc - 1) / bpc;
   if (row_tiles > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
   kern<<<dim3(static_cast<unsigned>(row_tiles), static_cast<unsigned>(gy)), C::NT, C::SMEM, st>>>(
-      a, lda, m, n, qplain, b0, b1, bpc, cols, ldc, req_start, req_ell, req_pos);
+      a, lda, m, n, qplain, b0, b1, bpc, cols, ldc, req_start, req_ell, req_pos, row0);
   return cudaGetLastError();
 }
 
@@ -611,9 +623,9 @@ cudaError_t launch_fwht_sketch(int k, const T* a, int64_t lda, int64_t m, int64_
                                int64_t b0, int64_t b1, T* cols, int64_t ldc, cudaStream_t st) {
   if constexpr (sizeof(T) == 4) {
     if (k == 12 && (lda % 4) == 0)
-      return launch_fwht_tmem<12, false>(a, lda, m, n, qplain, b0, b1, cols, ldc, st, nullptr, nullptr, nullptr);
+      return launch_fwht_tmem<12, false>(a, lda, m, n, qplain, b0, b1, cols, ldc, st, nullptr, nullptr, nullptr, 0);
     if (k == 14 && (lda % 4) == 0)
-      return launch_fwht_tmem<14, false>(a, lda, m, n, qplain, b0, b1, cols, ldc, st, nullptr, nullptr, nullptr);
+      return launch_fwht_tmem<14, false>(a, lda, m, n, qplain, b0, b1, cols, ldc, st, nullptr, nullptr, nullptr, 0);
   }
   switch (k) {
     case 2: return launch_fwht_k<T, 2>(a, lda, m, n, qplain, b0, b1, cols, ldc, st);

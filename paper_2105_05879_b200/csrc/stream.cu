@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
         P = c;
         break;
       }
-    if (lane < P && !(A.debug & 2)) {
+    if (lane < P && !(A.debug & 2) && A.means_mode != kMeansTail) {
       const uint64_t pol = policy_evict_first();
       const int nseg = A.nseg;
       int64_t v = blockIdx.x, j = 0;
@@ -512,7 +512,8 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     uint32_t lv = 0;
     for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
       const uint32_t xb = lv % static_cast<uint32_t>(A.xbufs), xu = lv / static_cast<uint32_t>(A.xbufs);
-      if (xu > 0) wp.wait(&x_empty[xb], (xu - 1) & 1u, kWCoefXEmpty);
+      // (PARTIAL: no tail reads x; this role's own end-of-vector barrier orders the reuse)
+      if (xu > 0 && A.means_mode != kMeansPartial) wp.wait(&x_empty[xb], (xu - 1) & 1u, kWCoefXEmpty);
       T* xs = xbuf + xb * dx;
       const T* xv = A.X + v * A.ldx;
       for (int64_t p = ctid; p < A.d; p += kCW * 32) xs[p] = (p < A.n) ? xv[p] : T(0);
@@ -520,8 +521,8 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
       if (ctid == 0) mbar_arrive(&x_full[xb]);
       const uint32_t* vidx = A.idx + v * A.N;
       const uint64_t g0 = uint64_t(lv) * uint64_t(A.N);
-      if (A.debug & 1) {
-        // column-pipeline experiment: no coefficients
+      if ((A.debug & 1) || A.means_mode == kMeansTail) {
+        // TAIL mode (no columns) or the column-pipeline experiment: no coefficients
       } else if constexpr (STRICT) {
         // One producing thread per ring slot (stride = kTRing): a slot's uses are
         // produced in order by the same thread, so a parity wait is never two
@@ -589,6 +590,10 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
 
   if (warp >= kWarpTail) {
     // ======================= tail warps =======================
+    if (A.means_mode == kMeansPartial) {
+      wp.done(kWTotTail, t_start);
+      return;
+    }
     const int ttid = tid - kWarpTail * 32, tw = warp - kWarpTail;
     const uint64_t pol_keep = policy_evict_last();
     int parity = 0;
@@ -597,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
       const uint32_t slot = lv & 1u, su = lv >> 1, xb = lv % static_cast<uint32_t>(A.xbufs),
                      xu = lv / static_cast<uint32_t>(A.xbufs);
-      T* means = scratch + slot * slot_elems;
+      T* means = A.means_mode == kMeansTail ? A.means_io + v * (A.K + 1) * A.m_pad : scratch + slot * slot_elems;
       T* mus = means + A.K * A.m_pad;
       wp.wait(&m_full[slot], su & 1u, kWTailMFull);
 
@@ -893,7 +898,17 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
   uint32_t lv = 0;
   for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
     const uint32_t slot = lv & 1u, su = lv >> 1;
-    T* means = scratch + slot * slot_elems;
+    if (A.means_mode == kMeansTail) {  // means come from means_io: only the slot handshake
+      if (su > 0) wp.wait(&m_empty[slot], (su - 1) & 1u, kWConsMEmpty);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&m_full[slot]);
+      continue;
+    }
+    const bool partial = A.means_mode == kMeansPartial;
+    // PARTIAL: rows [row0, row0 + m) of vector v's K batch means in means_io
+    T* means = partial ? A.means_io + v * (A.K + 1) * A.m_io + A.row0 : scratch + slot * slot_elems;
+    const int64_t bstride = partial ? A.m_io : A.m_pad;
+    const int64_t rows_out = partial ? A.m : A.m_pad;
     const uint64_t g0 = uint64_t(lv) * uint64_t(A.N);
 
     T acc[NSEG][CPT][VEC];
@@ -952,8 +967,8 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
       }
       if (++jb == A.J) {
         // batch b complete: mean = sum / J (IEEE division, stream.hpp:237)
-        if (b == 0 && su > 0) wp.wait(&m_empty[slot], (su - 1) & 1u, kWConsMEmpty);
-        T* mb = means + b * A.m_pad;
+        if (b == 0 && su > 0 && !partial) wp.wait(&m_empty[slot], (su - 1) & 1u, kWConsMEmpty);
+        T* mb = means + b * bstride;
         const T Jt = static_cast<T>(A.J);
 #pragma unroll
         for (int sg = 0; sg < NSEG; ++sg)
@@ -963,7 +978,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
             if (sg < A.nseg && row0 < A.m_pad) {
 #pragma unroll
               for (int e = 0; e < VEC; ++e) {
-                mb[row0 + e] = acc[sg][c][e] / Jt;
+                if (row0 + e < rows_out) mb[row0 + e] = acc[sg][c][e] / Jt;
                 acc[sg][c][e] = T(0);
               }
             }
@@ -973,7 +988,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&m_full[slot]);
+    if (lane == 0 && !partial) mbar_arrive(&m_full[slot]);
   }
   wp.done(kWTotCons, t_start);
 }

@@ -93,6 +93,7 @@ EXPORTED = [
     "fstg_gen_sparse_targets", "fstg_save", "fstg_load", "fstg_gen_mixture_targets",
     "fstg_preprocess_design", "fstg_sample_columns", "fstg_transform_gathered_batch",
     "fstg_verify_mub", "fstg_verify_design_moments", "fstg_design_moment_target", "fstg_verify_kerdock_set",
+    "fstg_transform_design_batch",
 ]
 
 
@@ -379,6 +380,31 @@ def preprocess_shard(a, basis_begin: int, basis_end: int, include_identity: bool
                                        C.c_int(device), C.c_void_p(stream), C.c_int64(basis_begin),
                                        C.c_int64(basis_end), C.c_int(1 if include_identity else 0), C.byref(h)))
     return Sketch(h.value)
+
+
+def transform_design_batch(sk: Sketch, X, p: StreamParams, seeds=None, *, row_block: int = 0,
+                           candidates: bool = False, mu: bool = False, out: Optional[BatchResult] = None,
+                           stream: Optional[int] = None) -> BatchResult:
+    """transform (stream.hpp:272-275) for a batch on a design-only sketch (no columns exist):
+    row blocks of the sampled columns are computed and consumed in turn (one Kerdock pass per call).
+    X, seeds and outputs are device tensors."""
+    import torch
+    X = _prep_x(sk, X)
+    if not (_is_torch(X) and X.is_cuda):
+        raise ValueError("transform_design_batch: X must be a CUDA tensor")
+    B = X.shape[0]
+    p.validate()
+    want = candidate_count(p.s, p.widen, sk.m)
+    if out is None:
+        out = _alloc_outputs(True, B, want, sk.m, sk.dtype, candidates, mu, sk.device)
+    if seeds is not None and not (_is_torch(seeds) and seeds.is_cuda):
+        seeds = torch.from_numpy(np.ascontiguousarray(seeds, dtype=np.uint64).view(np.int64)).to(X.device)
+    pc = p._c()
+    _check(lib().fstg_transform_design_batch(sk.handle, _ptr(X), C.c_int64(B), C.byref(pc), _ptr(seeds),
+                                             C.c_int64(row_block), _ptr(out.counts), _ptr(out.support),
+                                             _ptr(out.values), _ptr(out.candidates), _ptr(out.mu),
+                                             C.c_void_p(stream)))
+    return out
 
 
 def save(sk: Sketch, path, version: int = 1) -> None:

@@ -155,3 +155,55 @@ def test_route_retained_columns_nccl_single_rank(fst, orc):
         assert np.array_equal(got.cpu().numpy(), want)
     finally:
         dist.destroy_process_group()
+
+
+def _same(a, b):
+    import torch
+    a = a.cpu().numpy() if isinstance(a, torch.Tensor) else a
+    b = b.cpu().numpy() if isinstance(b, torch.Tensor) else b
+    return a.shape == b.shape and a.tobytes() == b.tobytes()
+
+
+@pytest.mark.parametrize("m,n,dtype,mode,row_block", [(200, 256, np.float32, 0, 64), (200, 256, np.float32, 0, 0),
+                                                      (130, 256, np.float64, 0, 40), (300, 1000, np.float32, 1, 96),
+                                                      (64, 4096, np.float32, 0, 16)])
+def test_transform_design_batch_equals_full_sketch(fst, m, n, dtype, mode, row_block):
+    """Row-blocked design-only transform (per row block: retain-sampled FWHT of those
+    rows + PARTIAL stream; then TAIL): every output bit-identical to the full-sketch
+    transform, because each row's batch sum runs over j in the same order."""
+    import torch
+    rng = np.random.default_rng(m + n)
+    a = rng.standard_normal((m, n)).astype(dtype)
+    sk, des = fst.preprocess(a), fst.preprocess_design(a)
+    B = 37
+    X = torch.from_numpy(rng.standard_normal((B, n)).astype(dtype)).cuda()
+    seeds = torch.from_numpy(rng.integers(0, 2**63, size=B, dtype=np.int64)).cuda()
+    p = fst.StreamParams(epsilon=0.5, s=3, J=23, K=3, mode=mode)
+    ref = fst.transform_batch(sk, X, p, seeds=seeds, candidates=True, mu=True)
+    got = fst.transform_design_batch(des, X, p, seeds=seeds, row_block=row_block, candidates=True, mu=True)
+    for f in ("counts", "support", "values", "candidates", "mu"):
+        assert _same(getattr(ref, f), getattr(got, f)), f
+    with pytest.raises(ValueError):
+        fst.transform_design_batch(des, X.cpu(), p, seeds=seeds)
+    sk.close()
+
+
+def test_transform_design_batch_config4_shape(fst):
+    """n = 16384 (k = 14): the row-blocked path equals the gathered-column path
+    (fstg_sample_columns of whole columns + fstg_transform_gathered_batch) bit for bit."""
+    import torch
+    from paper_2105_05879_b200 import generators
+    n, m = 16384, 256
+    A = generators.iid_gaussian(n, 1024, "cuda:0")[:m].float().contiguous()
+    des = fst.preprocess_design(A)
+    B = 3
+    X = torch.randn(B, n, device="cuda:0", generator=torch.Generator("cuda:0").manual_seed(1))
+    X = (X / torch.linalg.vector_norm(X, dim=1, keepdim=True)).contiguous()
+    seeds = torch.tensor([11, 12, 13], dtype=torch.int64, device="cuda:0")
+    p = fst.StreamParams(epsilon=0.01, s=8, J=40, K=2)
+    ind = fst.draw_samples(des, p, seeds=seeds.cpu().numpy().view(np.uint64))
+    cols = torch.from_numpy(fst.sample_columns(des, ind.ravel())).cuda()
+    ref = fst.transform_gathered_batch(des, X, p, ind, cols, candidates=True, mu=True)
+    got = fst.transform_design_batch(des, X, p, seeds=seeds, row_block=96, candidates=True, mu=True)
+    for f in ("counts", "support", "values", "candidates", "mu"):
+        assert _same(getattr(ref, f), getattr(got, f)), f
