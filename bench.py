@@ -287,6 +287,14 @@ def run_b200(args):
     achieved = bvec * vec_per_launch / (per_launch_ms / 1e3) / 1e9
     pre_achieved = sketch_bytes / (fwht_ms + ident_ms) / 1e6 if (fwht_ms + ident_ms) > 0 else None
 
+    # DRAM bytes per launch of the stream kernel from the committed ncu --set full capture
+    # (dram__bytes_read.sum + dram__bytes_write.sum = 845.77 GB + 3.19 GB for one config-3
+    # launch of 65,536 vectors), scaled to this run's vectors per launch
+    traffic, traffic_src = None, None
+    if args.config == "3":
+        traffic = (845.770680e9 + 3.188722e9) / 65536 * vec_per_launch
+        traffic_src = "profiles/r01_ncu_stream_kernel.txt (ncu --set full, 65,536-vector launch, scaled per vector)"
+
     # ---- end to end through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
@@ -367,8 +375,8 @@ def run_b200(args):
                                     "frac": (pre_achieved / peak) if pre_achieved else None,
                                     "peak_source": peak_kind}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "stream_kernel", "bytes_per_vector": bvec,
-                     "per_launch_ms": per_launch_ms, "peak_source": peak_kind},
+                     "traffic": traffic, "traffic_source": traffic_src, "kernel": "stream_kernel",
+                     "bytes_per_vector": bvec, "per_launch_ms": per_launch_ms, "peak_source": peak_kind},
         "kernels_ms": {"stream": stream_ms, "draw": draw_ms, "stream_launches": stream_launches,
                        "draw_launches": draw_launches},
         "gpu_launches": int(launches),
