@@ -42,7 +42,12 @@ constexpr int kTL = kTLW * 32;              // tail threads
 constexpr int kThreads = kNC + kCW * 32 + kTL + 32;  // + producer warp (768 threads with 8 consumer warps: 80 regs)
 constexpr int kWarpCoef = kNCW, kWarpTail = kNCW + kCW, kWarpProd = kNCW + kCW + kTLW;
 constexpr int kTRing = 64;                  // slots of the coefficient ring
-constexpr int kNS = 4;                      // samples per coefficient-warp group
+// Samples per coefficient-warp group: one x read from shared memory serves kNS
+// samples (8 vs 4: +8% at config 3, profiles/r01_stream_pipeline.txt; 16 spills).
+#ifndef FSTG_NS
+#define FSTG_NS 8
+#endif
+constexpr int kNS = FSTG_NS;
 constexpr int kSegBytes = 16384;            // one ring stage at most
 constexpr int kMaxStages = 64;
 // x buffers: coefficients on v+1 while the tail refines v. A third buffer (coefficients two
@@ -236,19 +241,23 @@ __device__ __forceinline__ T coeff_fast(const StreamArgs<T>& A, const T* xs, con
 template <typename T, int NS>
 __device__ __forceinline__ void coeff_fast_multi(const StreamArgs<T>& A, const T* xs, const uint32_t* wbase,
                                                  const uint32_t (&ells)[NS], int lane, T (&out)[NS]) {
-  constexpr int TWC = 4;  // sign-table words per sample loaded up front (d = 4096 -> all of them)
+#ifndef FSTG_TWC
+#define FSTG_TWC 1
+#endif
+  constexpr int TWC = FSTG_TWC;  // sign-table words per sample in flight (1 keeps kNS = 8 spill-free)
   const int64_t rows128 = A.d / 128;
   const int tw = static_cast<int>(A.d >= 1024 ? A.d / 1024 : 1);
-  uint32_t whi[NS], fix[NS], base[NS];
-  const uint32_t* q[NS];
+  // per sample: 32-bit word offset into qtrans, the Walsh base mask with the lane's
+  // fix folded in, and the high Walsh bits (flip of word t = parity(whi & 8t))
+  uint32_t whi[NS], base[NS], qoff[NS];
 #pragma unroll
   for (int k = 0; k < NS; ++k) {
     const uint32_t ell = static_cast<int64_t>(ells[k]) >= A.kb ? 0u : ells[k];
     const uint32_t s = ell >> A.k, w = ell & static_cast<uint32_t>(A.d - 1);
     whi[k] = w >> 7;
-    fix[k] = __popc(((w >> 2) & 31u) & static_cast<uint32_t>(lane)) & 1u;
-    base[k] = wbase[((whi[k] & 7u) << 2) | (w & 3u)];
-    q[k] = A.qtrans + (static_cast<int64_t>(s) * tw) * 32 + lane;
+    const uint32_t fix = __popc(((w >> 2) & 31u) & static_cast<uint32_t>(lane)) & 1u;
+    base[k] = wbase[((whi[k] & 7u) << 2) | (w & 3u)] ^ (fix ? 0xffffffffu : 0u);
+    qoff[k] = s * static_cast<uint32_t>(tw) * 32u + static_cast<uint32_t>(lane);
   }
   T acc[NS];
 #pragma unroll
@@ -258,7 +267,7 @@ __device__ __forceinline__ void coeff_fast_multi(const StreamArgs<T>& A, const T
 #pragma unroll
     for (int tt = 0; tt < TWC; ++tt)
 #pragma unroll
-      for (int k = 0; k < NS; ++k) raw[tt][k] = (t0 + tt < tw) ? __ldg(q[k] + (t0 + tt) * 32) : 0u;
+      for (int k = 0; k < NS; ++k) raw[tt][k] = (t0 + tt < tw) ? __ldg(A.qtrans + qoff[k] + (t0 + tt) * 32) : 0u;
 #pragma unroll
     for (int tt = 0; tt < TWC; ++tt) {
       const int t = t0 + tt;
@@ -267,7 +276,7 @@ __device__ __forceinline__ void coeff_fast_multi(const StreamArgs<T>& A, const T
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
           const uint32_t hiflip = __popc(whi[k] & (8u * t)) & 1u;
-          M[k] = raw[tt][k] ^ base[k] ^ ((hiflip ^ fix[k]) ? 0xffffffffu : 0u);
+          M[k] = raw[tt][k] ^ base[k] ^ (hiflip ? 0xffffffffu : 0u);
         }
 #pragma unroll
         for (int ip = 0; ip < 8; ++ip) {
