@@ -469,13 +469,13 @@ def run_sweep(args):
 # ------------------------------------------- config 4: retain-sampled ----
 def run_config4(args):
     """Config 4: n = 16384 fp32, A iid N(0,1/n), 8192 vectors per step per GPU, s = 64, eps = 0.05.
-    The 8.8 TB sketch cannot exist: per chunk of vectors the indices are drawn,
-    every Kerdock basis is FWHT-transformed keeping only the sampled columns
-    (fstg_sample_columns — the full O(n^3 log n) Kerdock computation once per
-    chunk), and the stream reads the retained columns (fstg_transform_gathered_batch).
-    N > 1 GPUs: a chunk spans every rank's vectors,
-    rank r computes only the columns of its Kerdock-basis shard and one NCCL
-    all-to-all routes each column to its vector's owner (parallel.route_retained_columns)."""
+    The 8.8 TB sketch cannot exist. One GPU: fstg_transform_design_batch — per row
+    block, the retain-sampled FWHT of those rows of every sampled column and the
+    stream's batch sums for those rows, then the tail (one Kerdock pass per step).
+    N > 1 GPUs: rank r computes its row shard of every
+    vector's batch means (1/N of the pass), one NCCL all-to-all of means routes
+    them to the vector owners (parallel.route_partial_means), and each rank runs
+    the tail for its own vectors."""
     import torch
     import torch.distributed as dist
     from paper_2105_05879_b200 import fst, generators, parallel
@@ -497,7 +497,7 @@ def run_config4(args):
     e1.record()
     torch.cuda.synchronize()
     design_ms = e0.elapsed_time(e1)
-    # every rank knows every vector's seed (draws of the whole chunk decide the routing)
+    # every rank knows every vector's seed (its row shard covers every vector)
     g_all, st_all = generators.trial_seeds(X_SEED, 0, B * world)
     first = rank * B
     Y = torch.from_numpy(generators.sparse_targets(g_all[first:first + B], n, s_val, value_kind=1)).to(dev)
@@ -509,11 +509,6 @@ def run_config4(args):
     p = fst.StreamParams(epsilon=eps_val, s=s_val, J=args.J, K=args.K, widen=WIDEN)
     N = args.J * args.K
     want = fst.candidate_count(s_val, WIDEN, n)
-    chunk = B if world == 1 else 1024               # N > 1: vectors per rank per chunk (~100 GB of columns in flight)
-    ldc = des.column_stride
-    nk = des.d // 2
-    shards = parallel.basis_shards(nk, world)
-    idx = torch.empty((chunk * world, N), dtype=torch.int64, device=dev) if world > 1 else None
     fst.profile_enable(True)
     out = fst.BatchResult(torch.zeros(B, dtype=torch.int32, device=dev),
                           torch.zeros((B, want), dtype=torch.int32, device=dev),
@@ -525,43 +520,30 @@ def run_config4(args):
         fst.sample_columns(des, ells, out=buf, stream=stream.cuda_stream)
         return buf
 
+    if world > 1:
+        # every rank needs every vector's x for its row shard of the batch means
+        X_all = torch.empty((B * world, n), dtype=X.dtype, device=dev)
+        dist.all_gather_into_tensor(X_all, X)
+        row_ranges = [(f, f + c) for f, c in (parallel.strong_shard(r, world, n) for r in range(world))]
+        vec_ranges = [(q * B, B) for q in range(world)]
+        ld = des.column_stride
+
     def step(timing):
+        fst.profile_reset()
         if world == 1:
             # row-blocked design transform: one Kerdock pass for all B vectors (fstg_transform_design_batch)
-            fst.profile_reset()
             fst.transform_design_batch(des, X, p, seeds=seeds_all[:B], out=out, stream=stream.cuda_stream)
-            ms_fwht, launches = fst.profile_read("sample_columns_fwht")
-            timing.append((ms_fwht, launches))
-            return
-        for c0 in range(0, B, chunk):
-            cb = min(chunk, B - c0)
-            a0 = torch.cuda.Event(enable_timing=True)
-            a1 = torch.cuda.Event(enable_timing=True)
-            if world == 1:
-                fst._check(fst.lib().fstg_draw_samples(des.handle, fst.C.byref(p._c()),
-                                                       fst._ptr(seeds_all[c0:c0 + cb]), fst.C.c_int64(cb),
-                                                       fst._ptr(idx), fst.C.c_void_p(stream.cuda_stream)))
-                a0.record(stream)
-                fst.sample_columns(des, idx[:cb].reshape(-1), out=cols, stream=stream.cuda_stream)
-                a1.record(stream)
-                gathered, ind = cols, idx[:cb]
-            else:
-                # chunk = vectors [q*B + c0, q*B + c0 + cb) of every rank q
-                rows = torch.cat([seeds_all[q * B + c0:q * B + c0 + cb] for q in range(world)])
-                fst._check(fst.lib().fstg_draw_samples(des.handle, fst.C.byref(p._c()), fst._ptr(rows),
-                                                       fst.C.c_int64(cb * world), fst._ptr(idx),
-                                                       fst.C.c_void_p(stream.cuda_stream)))
-                idx_host = idx[:cb * world].cpu().numpy()
-                plan = parallel.RoutingPlan(idx_host, [(q * cb, cb) for q in range(world)], shards, des.d, nk, rank)
-                a0.record(stream)
-                gathered = parallel.route_retained_columns(plan, sample_fn, ldc, torch.float32, dev)
-                a1.record(stream)
-                ind = idx[rank * cb:(rank + 1) * cb]
-            sub = fst.BatchResult(out.counts[c0:c0 + cb], out.support[c0:c0 + cb], out.values[c0:c0 + cb])
-            fst.transform_gathered_batch(des, X[c0:c0 + cb], p, ind, gathered, out=sub, stream=stream.cuda_stream)
-            torch.cuda.synchronize()
-            timing.append((a0.elapsed_time(a1), 1))
-            del gathered
+        else:
+            # row-sharded: rank r's rows of every vector's batch means (1/W of the Kerdock pass),
+            # one NCCL all-to-all of means (K x rows per vector), then the tail for my vectors
+            r0, r1 = row_ranges[rank]
+            part = fst.design_partial_means(des, X_all, p, seeds=seeds_all, row_begin=r0, row_end=r1,
+                                            stream=stream.cuda_stream)
+            full = parallel.route_partial_means(part, vec_ranges, row_ranges, rank, ld)
+            del part
+            fst.transform_from_means(des, X, p, full, out=out, stream=stream.cuda_stream)
+        ms_fwht, launches = fst.profile_read("sample_columns_fwht")
+        timing.append((ms_fwht, launches))
 
     warm = []
     for _ in range(max(1, args.warmup)):
@@ -581,8 +563,8 @@ def run_config4(args):
         dist.barrier()
     ms = parallel.max_over_ranks(t0.elapsed_time(t1), device=dev)
     retain_ms = sum(t for t, _ in timing)
-    passes = len(timing)                             # full Kerdock passes (1 per step on one GPU)
-    adds_per_pass = (des.d // 2) * n * des.d * 14 / world  # (d/2) m d log2 d, this rank's basis shard
+    passes = len(timing)                             # steps; each is one Kerdock pass over this rank's rows
+    adds_per_pass = (des.d // 2) * n * des.d * 14 / world  # (d/2) m d log2 d over this rank's row shard
     fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12     # nominal FP32 TFLOP/s (no measured CUDA-core peak)
     achieved = adds_per_pass * passes / (retain_ms / 1e3) / 1e12
     mean_support = float(out.counts.float().mean())
@@ -596,7 +578,8 @@ def run_config4(args):
             "config": {"workload": (f"config4: n=m=16384 fp32, s=64, eps=0.05, 8192 vectors/step/GPU, J={args.J}, "
                                     f"K={args.K} (full sketch 8.8 TB: " +
                                     ("row-blocked design transform, one Kerdock pass per step)" if world == 1 else
-                                     f"chunks of {chunk}/GPU, basis-sharded retain + NCCL all-to-all)")),
+                                     "row-sharded batch means, 1/N of the Kerdock pass per rank, NCCL all-to-all "
+                                     "of means)")),
                        "mean_support": mean_support},
             "preprocess": {"design_ms": design_ms, "kerdock_pass_ms": retain_ms / passes,
                            "kerdock_passes_per_step": passes // args.steps,

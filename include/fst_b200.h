@@ -223,6 +223,19 @@ int fstg_transform_design_batch(const fstg_sketch* sk, const void* X, int64_t B,
                                 const uint64_t* seeds, int64_t row_block, int32_t* counts, int32_t* support,
                                 void* values, int32_t* candidates, void* mu, void* stream);
 
+/* The two halves of fstg_transform_design_batch, for row-sharded multi-GPU use:
+ * rows [row_begin, row_end) of every vector's K batch means (vector v, batch b,
+ * row r at means[v * vstride + b * ld + r - row_begin]; ld >= row_end - row_begin,
+ * vstride >= K * ld), then median / top-want / refinement from complete means
+ * (means[v * vstride + b * ld + row], ld >= m and a multiple of 16 bytes,
+ * vstride >= (K + 1) * ld; slot K receives mu). Device memory. */
+int fstg_design_partial_means(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p,
+                              const uint64_t* seeds, int64_t row_begin, int64_t row_end, int64_t row_block,
+                              void* means, int64_t vstride, int64_t ld, void* stream);
+int fstg_transform_from_means(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p,
+                              void* means, int64_t vstride, int64_t ld, int32_t* counts, int32_t* support, void* values,
+                              int32_t* candidates, void* mu, void* stream);
+
 /* ------------------------------------------------------ design verifiers --- */
 /* kerdock.hpp:198-317, cli.hpp:45-82, on the GPU (sign tables of the design
  * expanded on `device`). All reported quantities are exact: every inner

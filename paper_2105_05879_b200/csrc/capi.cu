@@ -996,78 +996,55 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
 // ONE full pass whatever the batch size (vector chunks would each need a full
 // pass), and the batch means are bit-identical to the full-column path.
 template <typename T>
-void transform_design_impl(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p,
-                           const uint64_t* seeds, int64_t row_block, const Outputs& out, cudaStream_t st) {
-  validate(p);
-  if (B < 0) throw InvalidArgument("transform_design: negative batch size");
-  if (B == 0) return;
-  if (X == nullptr || out.counts == nullptr || out.support == nullptr || out.values == nullptr)
-    throw InvalidArgument("transform_design: X and counts/support/values must be non-null");
-  if (!sk->has_a) throw CodedError(FSTG_ERR_NO_MATRIX, "Sketch: no embedded matrix");
-  if (!is_device_ptr(X) || !is_device_ptr(out.counts) || !is_device_ptr(out.support) || !is_device_ptr(out.values) ||
-      (out.cands && !is_device_ptr(out.cands)) || (out.mu && !is_device_ptr(out.mu)) ||
-      (seeds && !is_device_ptr(seeds)))
-    throw InvalidArgument("transform_design: X, seeds and outputs must be device memory");
-  if (p->mode < 0 || p->mode > 2) throw InvalidArgument("StreamParams: unknown mode");
-  const bool strict = p->mode == FSTG_MODE_STRICT || (p->mode == FSTG_MODE_DEFAULT && sk->dtype == FSTG_F64);
-  const Design& D = sk->design;
-  const int64_t N = p->J * p->K, m = sk->m, n = sk->n;
-  if (N > (int64_t(1) << 40)) throw NotSupported("transform: J*K too large for this build");
-  const int64_t want = candidate_count(p->s, p->widen, m);
-  cuda_check(cudaSetDevice(sk->device), "cudaSetDevice");
-  keep_pool_warm(sk->device);
-
-  // indices: int64 for the retain FWHT, uint32 for the stream kernel (same draws)
-  DevBuf idx64(size_t(B) * N * 8, st), idx32(size_t(B) * N * 4, st);
-  {
-    ProfScope ps("draw", st);
-    cuda_check(launch_draw<int64_t>(seeds, p->seed, B, N, static_cast<uint64_t>(D.L), idx64.as<int64_t>(), st), "draw");
-  }
-  {
-    ProfScope ps("draw", st);
-    cuda_check(launch_draw<uint32_t>(seeds, p->seed, B, N, static_cast<uint64_t>(D.L), idx32.as<uint32_t>(), st),
-               "draw");
-  }
-  const int64_t m_io = sk->ldc;
-  DevBuf means_io(size_t(B) * (p->K + 1) * m_io * sizeof(T), st);
-
+struct DesignRun {
+  const fstg_sketch* sk;
+  const fstg_stream_params* p;
+  bool strict;
+  int64_t N, want;
   StreamArgs<T> args{};
-  args.a = static_cast<const T*>(sk->a);
-  args.lda = sk->lda;
-  args.qplain = sk->qplain;
-  args.qtrans = sk->qtrans;
-  args.revtab = sk->revtab;
-  args.k = D.k;
-  args.d = D.d;
-  args.L = D.L;
-  args.n = n;
-  args.kb = D.kerdock_bases() * D.d;
-  args.J = p->J;
-  args.K = p->K;
-  args.N = N;
-  args.want = want;
-  args.epsilon = p->epsilon;
-  args.X = static_cast<const T*>(X);
-  args.ldx = n;
-  args.idx = idx32.as<uint32_t>();
-  args.B = B;
-  args.counts = out.counts;
-  args.support = out.support;
-  args.values = static_cast<T*>(out.values);
-  args.cands = out.cands;
-  args.mu = static_cast<T*>(out.mu);
-  args.means_io = means_io.as<T>();
-  args.m_io = m_io;
-  {
+  cudaStream_t st;
+
+  DesignRun(const fstg_sketch* sk_, const void* X, int64_t B, const fstg_stream_params* p_, cudaStream_t st_)
+      : sk(sk_), p(p_), st(st_) {
+    validate(p);
+    if (B < 0) throw InvalidArgument("transform_design: negative batch size");
+    if (!sk->has_a) throw CodedError(FSTG_ERR_NO_MATRIX, "Sketch: no embedded matrix");
+    if (B > 0 && (X == nullptr || !is_device_ptr(X))) throw InvalidArgument("transform_design: X must be device memory");
+    if (p->mode < 0 || p->mode > 2) throw InvalidArgument("StreamParams: unknown mode");
+    strict = p->mode == FSTG_MODE_STRICT || (p->mode == FSTG_MODE_DEFAULT && sk->dtype == FSTG_F64);
+    const Design& D = sk->design;
+    N = p->J * p->K;
+    if (N > (int64_t(1) << 40)) throw NotSupported("transform: J*K too large for this build");
+    want = candidate_count(p->s, p->widen, sk->m);
+    cuda_check(cudaSetDevice(sk->device), "cudaSetDevice");
+    keep_pool_warm(sk->device);
+    args.a = static_cast<const T*>(sk->a);
+    args.lda = sk->lda;
+    args.qplain = sk->qplain;
+    args.qtrans = sk->qtrans;
+    args.revtab = sk->revtab;
+    args.k = D.k;
+    args.d = D.d;
+    args.L = D.L;
+    args.n = sk->n;
+    args.kb = D.kerdock_bases() * D.d;
+    args.J = p->J;
+    args.K = p->K;
+    args.N = N;
+    args.want = want;
+    args.epsilon = p->epsilon;
+    args.X = static_cast<const T*>(X);
+    args.ldx = sk->n;
+    args.B = B;
     const char* dbg = std::getenv("FSTG_STREAM_DEBUG");
     args.debug = dbg ? std::atoi(dbg) : 0;
   }
-  constexpr int64_t SEG = 16384 / sizeof(T), ALIGN = 16 / sizeof(T);
-  auto launch = [&](const char* name) {
+
+  void launch(const char* name) {
     if (args.nseg > 4) throw NotSupported("transform: m too large for this GPU build (m <= 4 * 16 KiB / sizeof(T))");
     size_t smem = 0;
     int stages = 0, stage_stride = 0, rstride = 0, xbufs = 0;
-    const int grid = stream_grid_size<T>(args, strict, B, &smem, &stages, &stage_stride, &rstride, &xbufs);
+    const int grid = stream_grid_size<T>(args, strict, args.B, &smem, &stages, &stage_stride, &rstride, &xbufs);
     if (smem > 227 * 1024) throw NotSupported("transform: shared-memory plan exceeds 227 KiB (d or want too large)");
     args.stages = stages;
     args.stage_stride = stage_stride;
@@ -1077,40 +1054,109 @@ void transform_design_impl(const fstg_sketch* sk, const void* X, int64_t B, cons
     args.means = scratch.as<T>();
     ProfScope ps(name, st);
     cuda_check(launch_stream<T>(args, strict, grid, st), "stream kernel");
-  };
+  }
 
-  // row blocks: as many rows as ~70% of free device memory holds (or the caller's row_block)
-  const int64_t per_row = B * N * int64_t(sizeof(T));
-  if (row_block <= 0) {
-    size_t free_b = 0, total_b = 0;
-    cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-    row_block = std::max<int64_t>(ALIGN, int64_t(double(free_b) * 0.7) / std::max<int64_t>(per_row, 1));
+  // Rows [row_begin, row_end) of every vector's K batch means: vector v, batch b, row
+  // r at means[v * vstride + b * ld + (r - row_begin)] (PARTIAL mode, row blocks).
+  void partial(const uint64_t* seeds, int64_t row_begin, int64_t row_end, int64_t row_block, T* means,
+               int64_t vstride, int64_t ld) {
+    const int64_t B = args.B;
+    if (B == 0 || row_end <= row_begin) return;
+    if (row_begin < 0 || row_end > sk->m) throw InvalidArgument("design_partial_means: row range outside [0, m)");
+    if (ld < row_end - row_begin || vstride < p->K * ld) throw InvalidArgument("design_partial_means: bad strides");
+    const Design& D = sk->design;
+    DevBuf idx64(size_t(B) * N * 8, st), idx32(size_t(B) * N * 4, st);
+    {
+      ProfScope ps("draw", st);
+      cuda_check(launch_draw<int64_t>(seeds, p->seed, B, N, static_cast<uint64_t>(D.L), idx64.as<int64_t>(), st), "draw");
+    }
+    {
+      ProfScope ps("draw", st);
+      cuda_check(launch_draw<uint32_t>(seeds, p->seed, B, N, static_cast<uint64_t>(D.L), idx32.as<uint32_t>(), st),
+                 "draw");
+    }
+    constexpr int64_t SEG = 16384 / sizeof(T), ALIGN = 16 / sizeof(T);
+    const int64_t per_row = B * N * int64_t(sizeof(T));
+    if (row_block <= 0) {  // as many rows as ~70% of free device memory holds
+      size_t free_b = 0, total_b = 0;
+      cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+      row_block = std::max<int64_t>(ALIGN, int64_t(double(free_b) * 0.7) / std::max<int64_t>(per_row, 1));
+    }
+    row_block = std::max<int64_t>(ALIGN, row_block / ALIGN * ALIGN);
+    args.idx = idx32.as<uint32_t>();
+    args.means_io = means;
+    args.m_io = ld;
+    args.means_vstride = vstride;
+    for (int64_t r0 = row_begin; r0 < row_end; r0 += row_block) {
+      const int64_t r1 = std::min(row_end, r0 + row_block);
+      const int64_t ldh = (r1 - r0 + ALIGN - 1) / ALIGN * ALIGN;
+      DevBuf cols(size_t(B) * N * ldh * sizeof(T), st);
+      sample_columns_impl<T>(sk, idx64.as<int64_t>(), B * N, cols.p, st, r0, r1, ldh);
+      args.means_mode = kMeansPartial;
+      args.cols = nullptr;
+      args.gathered = cols.as<T>();
+      args.ldc = ldh;
+      args.m = r1 - r0;
+      args.m_pad = ldh;
+      args.row0 = r0 - row_begin;
+      args.nseg = static_cast<int>((ldh + SEG - 1) / SEG);
+      launch("stream_partial");
+    }
   }
-  row_block = std::max<int64_t>(ALIGN, row_block / ALIGN * ALIGN);
-  for (int64_t r0 = 0; r0 < m; r0 += row_block) {
-    const int64_t r1 = std::min(m, r0 + row_block);
-    const int64_t ldh = (r1 - r0 + ALIGN - 1) / ALIGN * ALIGN;
-    DevBuf cols(size_t(B) * N * ldh * sizeof(T), st);
-    sample_columns_impl<T>(sk, idx64.as<int64_t>(), B * N, cols.p, st, r0, r1, ldh);
-    args.means_mode = kMeansPartial;
+
+  // Median / top-want / refinement from K batch means per vector (means[v * vstride
+  // + b * ld + row], slot K receives mu) (TAIL mode).
+  void tail(T* means, int64_t vstride, int64_t ld, const Outputs& out) {
+    if (args.B == 0) return;
+    if (out.counts == nullptr || out.support == nullptr || out.values == nullptr)
+      throw InvalidArgument("transform_design: counts/support/values must be non-null");
+    if (!is_device_ptr(out.counts) || !is_device_ptr(out.support) || !is_device_ptr(out.values) ||
+        (out.cands && !is_device_ptr(out.cands)) || (out.mu && !is_device_ptr(out.mu)))
+      throw InvalidArgument("transform_design: outputs must be device memory");
+    constexpr int64_t SEG = 16384 / sizeof(T), VEC = 16 / sizeof(T);
+    if (ld < sk->m || ld % VEC != 0 || vstride < (p->K + 1) * ld)
+      throw InvalidArgument("transform_from_means: bad strides (ld >= m, multiple of 16 bytes; vstride >= (K+1) ld)");
+    args.counts = out.counts;
+    args.support = out.support;
+    args.values = static_cast<T*>(out.values);
+    args.cands = out.cands;
+    args.mu = static_cast<T*>(out.mu);
+    args.means_mode = kMeansTail;
+    args.means_io = means;
+    args.m_io = ld;
+    args.means_vstride = vstride;
+    args.idx = nullptr;
+    args.gathered = nullptr;
     args.cols = nullptr;
-    args.gathered = cols.as<T>();
-    args.ldc = ldh;
-    args.m = r1 - r0;
-    args.m_pad = ldh;
-    args.row0 = r0;
-    args.nseg = static_cast<int>((ldh + SEG - 1) / SEG);
-    launch("stream_partial");
+    args.ldc = ld;
+    args.m = sk->m;
+    args.m_pad = ld;
+    args.row0 = 0;
+    args.nseg = static_cast<int>((ld + SEG - 1) / SEG);
+    launch("stream_tail");
   }
-  args.means_mode = kMeansTail;
-  args.gathered = nullptr;
-  args.cols = nullptr;
-  args.ldc = m_io;
-  args.m = m;
-  args.m_pad = m_io;
-  args.row0 = 0;
-  args.nseg = static_cast<int>((m_io + SEG - 1) / SEG);
-  launch("stream_tail");
+};
+
+// ------------------------------------------- row-blocked design transform ----
+// transform (stream.hpp:272-275) on a design-only sketch whose columns cannot
+// exist (n = 16384: 8.8 TB). Rows of the estimator are independent — row i's
+// batch sum is sum_j t_j C[i, ell_j] in j order — so the columns are produced
+// and consumed one row block at a time: per block, the retain-sampled FWHT
+// computes rows [r0, r1) of every sampled column of every vector (one pass over
+// all Kerdock bases for those rows only), and the stream kernel in PARTIAL mode
+// writes those rows of each vector's K batch means; then TAIL mode runs median /
+// select / refinement. Per call the Kerdock work is ONE full pass whatever the
+// batch size, and the batch means are bit-identical to the full-column path.
+template <typename T>
+void transform_design_impl(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p,
+                           const uint64_t* seeds, int64_t row_block, const Outputs& out, cudaStream_t st) {
+  DesignRun<T> run(sk, X, B, p, st);
+  if (B == 0) return;
+  if (seeds && !is_device_ptr(seeds)) throw InvalidArgument("transform_design: seeds must be device memory");
+  const int64_t m_io = sk->ldc, vstride = (p->K + 1) * m_io;
+  DevBuf means(size_t(B) * vstride * sizeof(T), st);
+  run.partial(seeds, 0, sk->m, row_block, means.as<T>(), vstride, m_io);
+  run.tail(means.as<T>(), vstride, m_io, out);
   cuda_check(cudaStreamSynchronize(st), "sync");
 }
 
@@ -1652,6 +1698,44 @@ int fstg_transform_design_batch(const fstg_sketch* sk, const void* X, int64_t B,
       transform_design_impl<float>(sk, X, B, p, seeds, row_block, o, static_cast<cudaStream_t>(stream));
     else
       transform_design_impl<double>(sk, X, B, p, seeds, row_block, o, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fstg_design_partial_means(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p,
+                              const uint64_t* seeds, int64_t row_begin, int64_t row_end, int64_t row_block,
+                              void* means, int64_t vstride, int64_t ld, void* stream) {
+  return guarded([&] {
+    if (!sk) throw InvalidArgument("null sketch");
+    if (B > 0 && (means == nullptr || !is_device_ptr(means))) throw InvalidArgument("design_partial_means: means must be device memory");
+    if (seeds && !is_device_ptr(seeds)) throw InvalidArgument("design_partial_means: seeds must be device memory");
+    const auto st = static_cast<cudaStream_t>(stream);
+    if (sk->dtype == FSTG_F32) {
+      DesignRun<float> run(sk, X, B, p, st);
+      run.partial(seeds, row_begin, row_end, row_block, static_cast<float*>(means), vstride, ld);
+    } else {
+      DesignRun<double> run(sk, X, B, p, st);
+      run.partial(seeds, row_begin, row_end, row_block, static_cast<double*>(means), vstride, ld);
+    }
+    cuda_check(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int fstg_transform_from_means(const fstg_sketch* sk, const void* X, int64_t B, const fstg_stream_params* p,
+                              void* means, int64_t vstride, int64_t ld, int32_t* counts, int32_t* support, void* values,
+                              int32_t* candidates, void* mu, void* stream) {
+  return guarded([&] {
+    if (!sk) throw InvalidArgument("null sketch");
+    if (B > 0 && (means == nullptr || !is_device_ptr(means))) throw InvalidArgument("transform_from_means: means must be device memory");
+    const Outputs o{counts, support, values, candidates, mu};
+    const auto st = static_cast<cudaStream_t>(stream);
+    if (sk->dtype == FSTG_F32) {
+      DesignRun<float> run(sk, X, B, p, st);
+      run.tail(static_cast<float*>(means), vstride, ld, o);
+    } else {
+      DesignRun<double> run(sk, X, B, p, st);
+      run.tail(static_cast<double*>(means), vstride, ld, o);
+    }
+    cuda_check(cudaStreamSynchronize(st), "sync");
   });
 }
 

@@ -98,6 +98,7 @@ struct StreamArgs {
   int means_mode;
   T* means_io;
   int64_t m_io, row0;
+  int64_t means_vstride;  // elements between vectors in means_io (0: (K + 1) * m_io)
   // experiment switches (env FSTG_STREAM_DEBUG; 0 in production):
   // bit 0: column pipeline only (coefficient warps idle, t = 1)
   // bit 1: coefficient pipeline only (no column loads, consumers skip the ring)

@@ -611,7 +611,9 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
       const uint32_t slot = lv & 1u, su = lv >> 1, xb = lv % static_cast<uint32_t>(A.xbufs),
                      xu = lv / static_cast<uint32_t>(A.xbufs);
-      T* means = A.means_mode == kMeansTail ? A.means_io + v * (A.K + 1) * A.m_pad : scratch + slot * slot_elems;
+      T* means = A.means_mode == kMeansTail
+                     ? A.means_io + v * (A.means_vstride > 0 ? A.means_vstride : (A.K + 1) * A.m_pad)
+                     : scratch + slot * slot_elems;
       T* mus = means + A.K * A.m_pad;
       wp.wait(&m_full[slot], su & 1u, kWTailMFull);
 
@@ -915,7 +917,8 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     }
     const bool partial = A.means_mode == kMeansPartial;
     // PARTIAL: rows [row0, row0 + m) of vector v's K batch means in means_io
-    T* means = partial ? A.means_io + v * (A.K + 1) * A.m_io + A.row0 : scratch + slot * slot_elems;
+    const int64_t vstride = A.means_vstride > 0 ? A.means_vstride : (A.K + 1) * A.m_io;
+    T* means = partial ? A.means_io + v * vstride + A.row0 : scratch + slot * slot_elems;
     const int64_t bstride = partial ? A.m_io : A.m_pad;
     const int64_t rows_out = partial ? A.m : A.m_pad;
     const uint64_t g0 = uint64_t(lv) * uint64_t(A.N);

@@ -93,7 +93,7 @@ EXPORTED = [
     "fstg_gen_sparse_targets", "fstg_save", "fstg_load", "fstg_gen_mixture_targets",
     "fstg_preprocess_design", "fstg_sample_columns", "fstg_transform_gathered_batch",
     "fstg_verify_mub", "fstg_verify_design_moments", "fstg_design_moment_target", "fstg_verify_kerdock_set",
-    "fstg_transform_design_batch",
+    "fstg_transform_design_batch", "fstg_design_partial_means", "fstg_transform_from_means",
 ]
 
 
@@ -404,6 +404,52 @@ def transform_design_batch(sk: Sketch, X, p: StreamParams, seeds=None, *, row_bl
                                              C.c_int64(row_block), _ptr(out.counts), _ptr(out.support),
                                              _ptr(out.values), _ptr(out.candidates), _ptr(out.mu),
                                              C.c_void_p(stream)))
+    return out
+
+
+def _dev_seeds(seeds, device):
+    import torch
+    if seeds is None or (_is_torch(seeds) and seeds.is_cuda):
+        return seeds
+    return torch.from_numpy(np.ascontiguousarray(seeds, dtype=np.uint64).view(np.int64)).to(device)
+
+
+def design_partial_means(sk: Sketch, X, p: StreamParams, seeds=None, row_begin: int = 0, row_end: Optional[int] = None,
+                         *, row_block: int = 0, out=None, stream: Optional[int] = None):
+    """Rows [row_begin, row_end) of every vector's K batch means on a design-only sketch:
+    a (B, K, row_end - row_begin) device tensor (one Kerdock pass over those rows)."""
+    import torch
+    X = _prep_x(sk, X)
+    if not (_is_torch(X) and X.is_cuda):
+        raise ValueError("design_partial_means: X must be a CUDA tensor")
+    p.validate()
+    row_end = sk.m if row_end is None else row_end
+    B, h = X.shape[0], row_end - row_begin
+    if out is None:
+        out = torch.empty((B, p.K, h), dtype=X.dtype, device=X.device)
+    seeds = _dev_seeds(seeds, X.device)
+    _check(lib().fstg_design_partial_means(sk.handle, _ptr(X), C.c_int64(B), C.byref(p._c()), _ptr(seeds),
+                                           C.c_int64(row_begin), C.c_int64(row_end), C.c_int64(row_block), _ptr(out),
+                                           C.c_int64(out.stride(0)), C.c_int64(out.stride(1)), C.c_void_p(stream)))
+    return out
+
+
+def transform_from_means(sk: Sketch, X, p: StreamParams, means, *, candidates: bool = False, mu: bool = False,
+                         out: Optional[BatchResult] = None, stream: Optional[int] = None) -> BatchResult:
+    """Median / top-want / refinement from complete batch means: means is a (B, K + 1, ld)
+    device tensor (ld >= m, 16-byte multiple; slot K is overwritten with mu)."""
+    X = _prep_x(sk, X)
+    if not (_is_torch(X) and X.is_cuda):
+        raise ValueError("transform_from_means: X must be a CUDA tensor")
+    p.validate()
+    B = X.shape[0]
+    want = candidate_count(p.s, p.widen, sk.m)
+    if out is None:
+        out = _alloc_outputs(True, B, want, sk.m, sk.dtype, candidates, mu, sk.device)
+    _check(lib().fstg_transform_from_means(sk.handle, _ptr(X), C.c_int64(B), C.byref(p._c()), _ptr(means),
+                                           C.c_int64(means.stride(0)), C.c_int64(means.stride(1)), _ptr(out.counts),
+                                           _ptr(out.support), _ptr(out.values), _ptr(out.candidates), _ptr(out.mu),
+                                           C.c_void_p(stream)))
     return out
 
 

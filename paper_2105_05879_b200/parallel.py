@@ -18,6 +18,12 @@ collectives are in preparation:
     the rank that owns its vector, which scatters them into the
     draw_and_gather layout (stream.hpp:184-191). The O(n^3 log n) Kerdock
     pass splits across ranks, and a chunk can hold world x more vectors.
+  * ``route_partial_means`` — config 4 row-sharded (preferred): rank r computes
+    the batch means of its ROW shard for every vector of the step (the
+    retain-sampled FWHT restricted to those rows is 1/W of the Kerdock pass)
+    and one all-to-all of means (K x rows per vector, ~1 GB per step instead
+    of the retained columns) gives each vector owner complete means for the
+    estimator's tail.
   * ``max_over_ranks``     — step time = max over ranks (device-timed).
 
 Everything here is host logic; it is tested on CPU with the gloo backend
@@ -148,6 +154,34 @@ def route_retained_columns(plan: RoutingPlan, sample_fn, ldc: int, dtype, device
     gathered = torch.empty((plan.local_rows, ldc), dtype=dtype, device=device)
     gathered.index_copy_(0, torch.from_numpy(plan.recv_positions).to(device), recv)
     return gathered
+
+
+def route_partial_means(part, vec_ranges: List[Tuple[int, int]], row_ranges: List[Tuple[int, int]], rank: int,
+                        ld: int, group=None):
+    """part: (B_all, K, rows of my row shard) batch means of every vector for this rank's rows;
+    vec_ranges[q] = (first, count) vectors owned by rank q, row_ranges[r] = (begin, end) rows of
+    rank r's shard. Returns (B_mine, K + 1, ld) complete means of this rank's vectors (slot K
+    left for mu), via one all_to_all_single: rank r sends rows-shard r of q's vectors to q."""
+    import torch
+    import torch.distributed as dist
+    world = len(vec_ranges)
+    B_all, K, h_me = part.shape
+    first, count = vec_ranges[rank]
+    # send: for every destination q its vectors' block of my rows (contiguous in part)
+    send = part.contiguous()
+    send_counts = [c * K * h_me for _, c in vec_ranges]
+    recv_counts = [count * K * (row_ranges[r][1] - row_ranges[r][0]) for r in range(world)]
+    recv = torch.empty(sum(recv_counts), dtype=part.dtype, device=part.device)
+    dist.all_to_all_single(recv, send.view(-1), output_split_sizes=recv_counts, input_split_sizes=send_counts,
+                           group=group)
+    full = torch.zeros((count, K + 1, ld), dtype=part.dtype, device=part.device)
+    off = 0
+    for r in range(world):
+        r0, r1 = row_ranges[r]
+        n = recv_counts[r]
+        full[:, :K, r0:r1] = recv[off:off + n].view(count, K, r1 - r0)
+        off += n
+    return full
 
 
 def broadcast_matrix(a, src: int = 0, group=None):

@@ -207,3 +207,32 @@ def test_transform_design_batch_config4_shape(fst):
     got = fst.transform_design_batch(des, X, p, seeds=seeds, row_block=96, candidates=True, mu=True)
     for f in ("counts", "support", "values", "candidates", "mu"):
         assert _same(getattr(ref, f), getattr(got, f)), f
+
+
+@pytest.mark.parametrize("dtype,mode", [(np.float32, 0), (np.float64, 0)])
+def test_row_sharded_partial_means_equal_design_batch(fst, dtype, mode):
+    """Two 'ranks' emulated in one process: each computes the batch means of its row
+    shard for every vector (fstg_design_partial_means), the shards are assembled per
+    vector owner (what parallel.route_partial_means does over NCCL), and
+    fstg_transform_from_means gives outputs bit-identical to fstg_transform_design_batch."""
+    import torch
+    rng = np.random.default_rng(8)
+    m, n, B = 200, 256, 6
+    a = rng.standard_normal((m, n)).astype(dtype)
+    des = fst.preprocess_design(a)
+    X = torch.from_numpy(rng.standard_normal((B, n)).astype(dtype)).cuda()
+    seeds = torch.from_numpy(rng.integers(0, 2**63, size=B, dtype=np.int64)).cuda()
+    p = fst.StreamParams(epsilon=0.5, s=3, J=17, K=3, mode=mode)
+    ref = fst.transform_design_batch(des, X, p, seeds=seeds, candidates=True, mu=True)
+    rows = [(0, 96), (96, 200)]
+    vecs = [(0, 4), (4, 2)]
+    parts = [fst.design_partial_means(des, X, p, seeds=seeds, row_begin=r0, row_end=r1, row_block=40)
+             for r0, r1 in rows]
+    ld = (m + 3) // 4 * 4
+    for first, count in vecs:
+        full = torch.zeros((count, p.K + 1, ld), dtype=X.dtype, device="cuda:0")
+        for (r0, r1), part in zip(rows, parts):
+            full[:, :p.K, r0:r1] = part[first:first + count]
+        got = fst.transform_from_means(des, X[first:first + count], p, full, candidates=True, mu=True)
+        for f in ("counts", "support", "values", "candidates", "mu"):
+            assert _same(getattr(ref, f)[first:first + count], getattr(got, f)), f

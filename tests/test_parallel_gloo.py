@@ -151,3 +151,32 @@ def test_routing_plan_single_process():
     assert parallel.column_owner(np.array([0]), parallel.basis_shards(1, 4), d, 1)[0] == 0
     with pytest.raises(ValueError):
         parallel.RoutingPlan(idx_all, vec_ranges[:2], shards, d, nk, 0)
+
+
+def _means_worker(rank, world, port, tmpdir):
+    """Config-4 row-sharded routing: each rank holds the batch means of its row
+    shard for every vector; after route_partial_means every rank holds the
+    complete means of its own vectors."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ok = []
+        for B, m, K in [(5, 10, 2), (7, 33, 3), (2, 8, 1)]:
+            M = torch.from_numpy(np.random.default_rng(B * m + K).standard_normal((B, K, m)))
+            vec_ranges = [parallel.strong_shard(q, world, B) for q in range(world)]
+            row_ranges = [(f, f + c) for f, c in (parallel.strong_shard(r, world, m) for r in range(world))]
+            r0, r1 = row_ranges[rank]
+            ld = (m + 3) // 4 * 4
+            full = parallel.route_partial_means(M[:, :, r0:r1].contiguous(), vec_ranges, row_ranges, rank, ld)
+            first, count = vec_ranges[rank]
+            ok.append(bool(full.shape == (count, K + 1, ld) and torch.equal(full[:, :K, :m], M[first:first + count])))
+        np.save(os.path.join(tmpdir, f"means{rank}.npy"), {"ok": ok}, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_row_sharded_means(tmp_path):
+    world, port = 2, _free_port()
+    mp.spawn(_means_worker, args=(world, port, str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        assert all(np.load(tmp_path / f"means{r}.npy", allow_pickle=True).item()["ok"])

@@ -1,7 +1,5 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-for v in k14nt256 k14nt128; do
-cp tools/variants/lib_$v.so paper_2105_05879_b200/libfst_b200.so
-timeout 900 python bench.py --config 4 --steps 1 --warmup 1 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo "$v c4 rc=$?"; tail -2 gpurun_out/bench_c4.err
+timeout 900 python -m pytest tests/test_gpu_retain.py -x -q --timeout 600 -m gpu > gpurun_out/design_tests.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/design_tests.log; grep -E "^E " gpurun_out/design_tests.log | head -5
+timeout 900 python bench.py --config 4 --steps 2 --warmup 1 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo "c4 rc=$?"; tail -2 gpurun_out/bench_c4.err
 python -c "
 import json; d=json.load(open('gpurun_out/bench_c4.json')); print(round(d['value']), d['preprocess']['kerdock_pass_ms'], d['ms_per_step'])"
-done
