@@ -191,10 +191,18 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the N > 1 host path on a one-GPU box (never a measurement):
+    # every rank on cuda:0, gloo collectives; no kernel waits on another rank's
+    one_dev = os.environ.get("FSTG_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(dev))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(dev))
 
     cfg = WORKLOADS[args.config]
     n_dim = cfg["n"]
