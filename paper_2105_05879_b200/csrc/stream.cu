@@ -70,25 +70,35 @@ enum WaitSite {
 };
 __device__ unsigned long long g_wait_cycles[kWSites];
 
+#ifndef FSTG_WAIT_PROFILE
+#define FSTG_WAIT_PROFILE 0
+#endif
+// Compiled out unless built with -DFSTG_WAIT_PROFILE=1 (then FSTG_STREAM_DEBUG bit 8
+// turns it on): a runtime check on every wait costs the small-d configs ~20%.
+constexpr bool kWaitProfile = FSTG_WAIT_PROFILE != 0;
 struct WaitProf {
   bool on;
   unsigned long long* acc;  // kWSites shared-memory counters, acc[kWSites] = warps finished
   __device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity, int site) {
-    if (on) {
-      const long long t0 = clock64();
-      mbar_wait(bar, parity);
-      if ((threadIdx.x & 31) == 0) atomicAdd(&acc[site], static_cast<unsigned long long>(clock64() - t0));
-    } else {
-      mbar_wait(bar, parity);
+    if constexpr (kWaitProfile) {
+      if (on) {
+        const long long t0 = clock64();
+        mbar_wait(bar, parity);
+        if ((threadIdx.x & 31) == 0) atomicAdd(&acc[site], static_cast<unsigned long long>(clock64() - t0));
+        return;
+      }
     }
+    mbar_wait(bar, parity);
   }
   // called once per warp when its role ends; the last warp publishes the CTA's totals
   __device__ __forceinline__ void done(int site, long long t_start) {
-    if (!on || (threadIdx.x & 31) != 0) return;
-    atomicAdd(&acc[site], static_cast<unsigned long long>(clock64() - t_start));
-    __threadfence_block();
-    if (atomicAdd(&acc[kWSites], 1ull) == static_cast<unsigned long long>(blockDim.x / 32 - 1)) {
-      for (int i = 0; i < kWSites; ++i) atomicAdd(&g_wait_cycles[i], atomicAdd(&acc[i], 0ull));
+    if constexpr (kWaitProfile) {
+      if (!on || (threadIdx.x & 31) != 0) return;
+      atomicAdd(&acc[site], static_cast<unsigned long long>(clock64() - t_start));
+      __threadfence_block();
+      if (atomicAdd(&acc[kWSites], 1ull) == static_cast<unsigned long long>(blockDim.x / 32 - 1)) {
+        for (int i = 0; i < kWSites; ++i) atomicAdd(&g_wait_cycles[i], atomicAdd(&acc[i], 0ull));
+      }
     }
   }
 };
@@ -415,9 +425,9 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
   uint8_t* cflag = reinterpret_cast<uint8_t*>(smem + Ls.cflag);
   __shared__ uint32_t wbase[32];
   __shared__ unsigned long long wait_acc[kWSites + 1];
-  const long long t_start = clock64();
-  WaitProf wp{(A.debug & 8) != 0, wait_acc};
-  if (threadIdx.x <= kWSites) wait_acc[threadIdx.x] = 0;
+  const long long t_start = kWaitProfile ? clock64() : 0;
+  WaitProf wp{kWaitProfile && (A.debug & 8) != 0, wait_acc};
+  if (kWaitProfile && threadIdx.x <= kWSites) wait_acc[threadIdx.x] = 0;
 
   const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
   const int S = A.stages;
