@@ -803,10 +803,13 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   // Host buffers: chunks grow geometrically from kFirstChunk to kMaxChunk vectors, so
   // the one copy that cannot overlap (the first chunk's H2D) is short while later
   // launches are long (each launch pays a pipeline fill and an unoverlapped tail).
-  constexpr int64_t kFirstChunk = 2048, kMaxChunk = 16384;
+  // The first chunk carries ~64 MiB of x (at least 2048 vectors): small batches run as one launch.
+  constexpr int64_t kMaxChunk = 16384;
+  const int64_t first_chunk =
+      std::max<int64_t>(2048, (int64_t(64) << 20) / std::max<int64_t>(1, n * int64_t(sizeof(T))));
   int64_t chunk = all_dev ? B : std::min<int64_t>(B, kMaxChunk);
   chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, (int64_t(1) << 29) / std::max<int64_t>(N, 1)));
-  int64_t next_chunk = all_dev ? chunk : std::min<int64_t>(chunk, kFirstChunk);
+  int64_t next_chunk = all_dev ? chunk : std::min<int64_t>(chunk, first_chunk);
 
   StreamArgs<T> args{};
   args.cols = static_cast<const T*>(sk->cols);
@@ -849,10 +852,24 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   // chunk i computes (one shared copy stream would queue the next H2D behind the
   // previous chunk's D2H, which waits for that chunk's kernel).
   const int nbuf = all_dev ? 1 : 2;
+  // copy streams and events are cached per host thread and device (created once)
+  struct HostPathRes {
+    cudaStream_t in = nullptr, out = nullptr;
+    cudaEvent_t ev[3][2] = {};
+  };
+  thread_local std::map<int, HostPathRes> t_res;
   cudaStream_t copy_st = nullptr, out_st = nullptr;
+  HostPathRes* res = nullptr;
   if (!all_dev) {
-    cuda_check(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking), "stream");
-    cuda_check(cudaStreamCreateWithFlags(&out_st, cudaStreamNonBlocking), "stream");
+    res = &t_res[sk->device];
+    if (res->in == nullptr) {
+      cuda_check(cudaStreamCreateWithFlags(&res->in, cudaStreamNonBlocking), "stream");
+      cuda_check(cudaStreamCreateWithFlags(&res->out, cudaStreamNonBlocking), "stream");
+      for (auto& row : res->ev)
+        for (auto& e : row) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    copy_st = res->in;
+    out_st = res->out;
   }
   struct Bufs {
     DevBuf X, idx, counts, support, values, cands, mu, seeds, idx64;
@@ -861,11 +878,13 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   DevBuf means(size_t(stream_scratch_elems<T>(args, grid_max)) * sizeof(T), st);
   DevBuf bad(sizeof(int), st);
   cuda_check(cudaMemsetAsync(bad.p, 0, sizeof(int), st), "memset");
-  std::vector<cudaEvent_t> ev_in(nbuf), ev_done(nbuf), ev_out(nbuf);
+  cudaEvent_t ev_in[2] = {}, ev_done[2] = {}, ev_out[2] = {};
   for (int b = 0; b < nbuf; ++b) {
-    cuda_check(cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming), "event");
-    cuda_check(cudaEventCreateWithFlags(&ev_done[b], cudaEventDisableTiming), "event");
-    cuda_check(cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming), "event");
+    if (res != nullptr) {
+      ev_in[b] = res->ev[0][b];
+      ev_done[b] = res->ev[1][b];
+      ev_out[b] = res->ev[2][b];
+    }
     Bufs& bf = bufs[b];
     bf.idx = DevBuf(size_t(chunk) * N * sizeof(uint32_t), st);
     if (!x_dev) bf.X = DevBuf(size_t(chunk) * n * sizeof(T), st);
@@ -879,7 +898,10 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
     if (seeds != nullptr && !seeds_dev) bf.seeds = DevBuf(size_t(chunk) * sizeof(uint64_t), st);
     if (indices != nullptr && !idx_dev) bf.idx64 = DevBuf(size_t(chunk) * N * sizeof(int64_t), st);
   }
-  if (!all_dev) cuda_check(cudaStreamSynchronize(st), "sync allocations");
+  if (!all_dev) {  // the copy stream starts after the stream-ordered allocations on st
+    cuda_check(cudaEventRecord(ev_in[0], st), "event");
+    cuda_check(cudaStreamWaitEvent(copy_st, ev_in[0], 0), "wait");
+  }
 
   int it = 0;
   for (int64_t v0 = 0, cb = 0; v0 < B; v0 += cb, ++it) {
@@ -974,13 +996,6 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
     cuda_check(cudaStreamSynchronize(copy_st), "sync copies");
     cuda_check(cudaStreamSynchronize(out_st), "sync copies");
     cuda_check(cudaStreamSynchronize(st), "sync compute");
-    cudaStreamDestroy(copy_st);
-    cudaStreamDestroy(out_st);
-  }
-  for (int b = 0; b < nbuf; ++b) {
-    cudaEventDestroy(ev_in[b]);
-    cudaEventDestroy(ev_done[b]);
-    cudaEventDestroy(ev_out[b]);
   }
 }
 
