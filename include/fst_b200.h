@@ -236,6 +236,19 @@ int fstg_transform_from_means(const fstg_sketch* sk, const void* X, int64_t B, c
                               void* means, int64_t vstride, int64_t ld, int32_t* counts, int32_t* support, void* values,
                               int32_t* candidates, void* mu, void* stream);
 
+/* ------------------------------------------------------- public helpers ---- */
+/* The reference's smaller public functions on this path, as GPU kernels (host
+ * or device pointers; device selects the GPU). */
+/* stream.hpp:109-121 inner_product_with_design: s_ell^T x, the Kerdock case by
+ * the reference's sequential Gray-code walk (bit-exact fp64). */
+int fstg_inner_product_with_design(int k, const double* x, int64_t n, int64_t ell, double* out, int device);
+/* stream.hpp:147-155 median_of_means: samples m x (J*K), column j at samples + j*m. */
+int fstg_median_of_means(const double* samples, int64_t m, int64_t J, int64_t K, double* out, int device);
+/* stream.hpp:158-162 hard_threshold (|t| = eps kept). */
+int fstg_hard_threshold(const double* v, int64_t len, double eps, double* out, int device);
+/* kerdock.hpp:156-167 projected_design_column: s_ell, n entries. */
+int fstg_projected_design_column(int k, int64_t n, int64_t ell, double* out, int device);
+
 /* ------------------------------------------------------ design verifiers --- */
 /* kerdock.hpp:198-317, cli.hpp:45-82, on the GPU (sign tables of the design
  * expanded on `device`). All reported quantities are exact: every inner

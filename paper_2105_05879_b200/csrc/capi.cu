@@ -1175,6 +1175,148 @@ void transform_design_impl(const fstg_sketch* sk, const void* X, int64_t B, cons
   cuda_check(cudaStreamSynchronize(st), "sync");
 }
 
+
+// ------------------------------------------------------- public helpers ----
+// Host-or-device double buffers for the small helpers (copied in / out).
+struct DoubleIn {
+  DevBuf buf;
+  const double* p = nullptr;
+  DoubleIn(const double* src, int64_t count, cudaStream_t st) {
+    if (count <= 0) return;
+    if (is_device_ptr(src)) {
+      p = src;
+    } else {
+      buf = DevBuf(size_t(count) * 8, st);
+      cuda_check(cudaMemcpyAsync(buf.p, src, size_t(count) * 8, cudaMemcpyHostToDevice, st), "H2D");
+      p = buf.as<double>();
+    }
+  }
+};
+
+void finish_out(double* dst, const DevBuf& tmp, int64_t count, cudaStream_t st) {
+  if (tmp.p != nullptr)
+    cuda_check(cudaMemcpyAsync(dst, tmp.p, size_t(count) * 8, cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+}
+
+void helper_prologue(int device) {
+  require_device(device);
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+}
+
+// kerdock.hpp:111-129 DesignIndex::from_linear -> (identity?, basis s, wpos) and the basis' reversed rows
+bool decode_design_index(const Design& D, int64_t ell, uint64_t* wpos, std::vector<uint32_t>& rev) {
+  if (ell < 0 || ell >= D.L) throw OutOfRange("DesignIndex: linear index out of range");
+  const int64_t kb = D.kerdock_bases() * D.d;
+  rev.assign(16, 0u);
+  if (ell >= kb) {
+    *wpos = static_cast<uint64_t>(ell - kb);
+    return true;
+  }
+  const Field f(D.k - 1, D.modulus);
+  const auto rows = kerdock_matrix(D, f, static_cast<uint64_t>(ell / D.d));
+  reversed_rows(rows.data(), D.k, rev.data());
+  *wpos = static_cast<uint64_t>(ell % D.d);
+  return false;
+}
+
+void inner_product_impl(int k, const double* x, int64_t n, int64_t ell, double* out, int device) {
+  const Design D = Design::make(k);
+  if (!x || !out) throw InvalidArgument("inner_product_with_design: null pointer");
+  if (n < 1 || n > D.d) throw InvalidArgument("inner_product_with_design: bad vector length");
+  uint64_t wpos = 0;
+  std::vector<uint32_t> rev;
+  const bool identity = decode_design_index(D, ell, &wpos, rev);
+  if (identity) {  // stream.hpp:113-116: sqrt(d) x_w or 0 (one multiply; no kernel needed)
+    double xv = 0;
+    if (static_cast<int64_t>(wpos) < n) {
+      helper_prologue(device);
+      cuda_check(cudaMemcpy(&xv, x + wpos, 8, is_device_ptr(x) ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost),
+                 "copy");
+      *out = std::sqrt(static_cast<double>(D.d)) * xv;
+    } else {
+      *out = 0.0;
+    }
+    return;
+  }
+  helper_prologue(device);
+  cudaStream_t st = nullptr;
+  DoubleIn xin(x, n, st);
+  DevBuf drev(16 * 4, st), dout(8, st);
+  cuda_check(cudaMemcpyAsync(drev.p, rev.data(), 16 * 4, cudaMemcpyHostToDevice, st), "H2D");
+  {
+    ProfScope ps("inner_product", st);
+    cuda_check(launch_inner_product(xin.p, n, D.d, drev.as<uint32_t>(), wpos, dout.as<double>(), st), "kernel");
+  }
+  cuda_check(cudaMemcpyAsync(out, dout.p, 8, is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st),
+             "copy out");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+}
+
+void median_of_means_impl(const double* samples, int64_t m, int64_t J, int64_t K, double* out, int device) {
+  if (J < 1 || K < 1 || m < 0) throw InvalidArgument("median_of_means: samples must have J*K columns");
+  if (m > 0 && (!samples || !out)) throw InvalidArgument("median_of_means: null pointer");
+  if (m == 0) return;
+  helper_prologue(device);
+  cudaStream_t st = nullptr;
+  DoubleIn in(samples, m * J * K, st);
+  DevBuf tmp;
+  double* dst = out;
+  if (!is_device_ptr(out)) {
+    tmp = DevBuf(size_t(m) * 8, st);
+    dst = tmp.as<double>();
+  }
+  {
+    ProfScope ps("median_of_means", st);
+    cuda_check(launch_median_of_means(in.p, m, J, K, dst, st), "kernel");
+  }
+  finish_out(out, tmp, m, st);
+}
+
+void hard_threshold_impl(const double* v, int64_t len, double eps, double* out, int device) {
+  if (len < 0 || (len > 0 && (!v || !out))) throw InvalidArgument("hard_threshold: bad arguments");
+  if (len == 0) return;
+  helper_prologue(device);
+  cudaStream_t st = nullptr;
+  DoubleIn in(v, len, st);
+  DevBuf tmp;
+  double* dst = out;
+  if (!is_device_ptr(out)) {
+    tmp = DevBuf(size_t(len) * 8, st);
+    dst = tmp.as<double>();
+  }
+  {
+    ProfScope ps("hard_threshold", st);
+    cuda_check(launch_hard_threshold(in.p, len, eps, dst, st), "kernel");
+  }
+  finish_out(out, tmp, len, st);
+}
+
+void design_column_impl(int k, int64_t n, int64_t ell, double* out, int device) {
+  const Design D = Design::make(k);
+  if (n < 1 || n > D.d) throw InvalidArgument("projected_design_column: n out of [1,d]");
+  if (!out) throw InvalidArgument("projected_design_column: null pointer");
+  uint64_t wpos = 0;
+  std::vector<uint32_t> rev;
+  const bool identity = decode_design_index(D, ell, &wpos, rev);
+  helper_prologue(device);
+  cudaStream_t st = nullptr;
+  DevBuf drev(16 * 4, st), tmp;
+  cuda_check(cudaMemcpyAsync(drev.p, rev.data(), 16 * 4, cudaMemcpyHostToDevice, st), "H2D");
+  double* dst = out;
+  if (!is_device_ptr(out)) {
+    tmp = DevBuf(size_t(n) * 8, st);
+    dst = tmp.as<double>();
+  }
+  {
+    ProfScope ps("design_column", st);
+    cuda_check(launch_design_column(n, D.d, identity ? 1 : 0, drev.as<uint32_t>(), D.k, wpos,
+                                    std::sqrt(static_cast<double>(D.d)), dst, st),
+               "kernel");
+  }
+  finish_out(out, tmp, n, st);
+}
+
 // ----------------------------------------------------- design verifiers ----
 // kerdock.hpp:198-317 / cli.hpp:45-60 on the GPU (verify.cu). Inner products
 // are F/d with integer F, so every report field is assembled exactly from the
@@ -1752,6 +1894,22 @@ int fstg_transform_from_means(const fstg_sketch* sk, const void* X, int64_t B, c
     }
     cuda_check(cudaStreamSynchronize(st), "sync");
   });
+}
+
+int fstg_inner_product_with_design(int k, const double* x, int64_t n, int64_t ell, double* out, int device) {
+  return guarded([&] { inner_product_impl(k, x, n, ell, out, device); });
+}
+
+int fstg_median_of_means(const double* samples, int64_t m, int64_t J, int64_t K, double* out, int device) {
+  return guarded([&] { median_of_means_impl(samples, m, J, K, out, device); });
+}
+
+int fstg_hard_threshold(const double* v, int64_t len, double eps, double* out, int device) {
+  return guarded([&] { hard_threshold_impl(v, len, eps, out, device); });
+}
+
+int fstg_projected_design_column(int k, int64_t n, int64_t ell, double* out, int device) {
+  return guarded([&] { design_column_impl(k, n, ell, out, device); });
 }
 
 }  // extern "C"

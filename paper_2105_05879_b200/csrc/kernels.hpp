@@ -43,6 +43,15 @@ cudaError_t launch_verify_samples(int k, const uint32_t* qplain, const int64_t* 
 // Pairs a < b of Kerdock matrices (nk x k row words) whose sum has rank < k.
 cudaError_t launch_verify_ranks(int k, const uint32_t* rows, int64_t nk, unsigned long long* bad, cudaStream_t st);
 
+// ---- public helpers (helpers.cu): stream.hpp:86-162, kerdock.hpp:156-167 ----
+cudaError_t launch_inner_product(const double* x, int64_t n, int64_t d, const uint32_t* rev, uint64_t wpos,
+                                 double* out, cudaStream_t st);
+cudaError_t launch_median_of_means(const double* samples, int64_t m, int64_t J, int64_t K, double* out,
+                                   cudaStream_t st);
+cudaError_t launch_hard_threshold(const double* v, int64_t len, double eps, double* out, cudaStream_t st);
+cudaError_t launch_design_column(int64_t n, int64_t d, int identity, const uint32_t* rev, int k, uint64_t wpos,
+                                 double sqrt_d, double* out, cudaStream_t st);
+
 // ---- draws (draw.cu) ----
 template <typename IdxT>
 cudaError_t launch_draw(const uint64_t* seeds, uint64_t seed_base, int64_t B, int64_t N, uint64_t L, IdxT* out,

@@ -94,6 +94,7 @@ EXPORTED = [
     "fstg_preprocess_design", "fstg_sample_columns", "fstg_transform_gathered_batch",
     "fstg_verify_mub", "fstg_verify_design_moments", "fstg_design_moment_target", "fstg_verify_kerdock_set",
     "fstg_transform_design_batch", "fstg_design_partial_means", "fstg_transform_from_means",
+    "fstg_inner_product_with_design", "fstg_median_of_means", "fstg_hard_threshold", "fstg_projected_design_column",
 ]
 
 
@@ -575,6 +576,44 @@ def transform_with_samples(sk: Sketch, x, p: StreamParams, indices) -> Transform
     r = transform_with_samples_batch(sk, x.reshape(1, -1), p, np.asarray(indices, dtype=np.int64).reshape(1, -1),
                                      candidates=True, mu=True)
     return r.result(0, p.J * p.K)
+
+
+# -------------------------------------------------------- public helpers ----
+def inner_product_with_design(x, k: int, ell: int, device: int = 0) -> float:
+    """stream.hpp:109-121 on the GPU: s_ell^T x (Kerdock: the reference's Gray-code walk, bit-exact)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    out = C.c_double()
+    _check(lib().fstg_inner_product_with_design(C.c_int(k), _ptr(x), C.c_int64(x.size), C.c_int64(ell),
+                                                C.byref(out), C.c_int(device)))
+    return out.value
+
+
+def median_of_means(samples, J: int, K: int, device: int = 0) -> np.ndarray:
+    """stream.hpp:147-155 on the GPU: samples (m, J*K), batch b = columns [b*J, (b+1)*J)."""
+    samples = np.asarray(samples, dtype=np.float64)
+    if samples.ndim != 2 or J < 1 or K < 1 or samples.shape[1] != J * K:
+        raise ValueError("median_of_means: samples must have J*K columns")
+    m = samples.shape[0]
+    cols = np.ascontiguousarray(samples.T)          # row j = column j of the reference's m x N matrix
+    out = np.zeros(m)
+    _check(lib().fstg_median_of_means(_ptr(cols), C.c_int64(m), C.c_int64(J), C.c_int64(K), _ptr(out),
+                                      C.c_int(device)))
+    return out
+
+
+def hard_threshold(v, eps: float, device: int = 0) -> np.ndarray:
+    """stream.hpp:158-162 on the GPU (|t| = eps kept)."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    out = np.zeros_like(v)
+    _check(lib().fstg_hard_threshold(_ptr(v), C.c_int64(v.size), C.c_double(eps), _ptr(out), C.c_int(device)))
+    return out
+
+
+def projected_design_column(k: int, n: int, ell: int, device: int = 0) -> np.ndarray:
+    """kerdock.hpp:156-167 on the GPU: s_ell (n entries)."""
+    out = np.zeros(n)
+    _check(lib().fstg_projected_design_column(C.c_int(k), C.c_int64(n), C.c_int64(ell), _ptr(out), C.c_int(device)))
+    return out
 
 
 # ------------------------------------------------------- design verifiers ----

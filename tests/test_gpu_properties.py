@@ -117,3 +117,32 @@ def test_concurrent_transforms_on_one_sketch(fst):
         assert np.array_equal(results[t].values[valid], serial[t].values[valid])
         assert results[t].mu.tobytes() == serial[t].mu.tobytes()
     sk.close()
+
+
+def test_public_helpers_match_oracle(fst, orc):
+    """inner_product_with_design (bit-exact Gray-code walk), median_of_means,
+    hard_threshold and projected_design_column on the GPU vs the oracle
+    (test_stream.cpp 'inner_product_with_design fixed values / matches the
+    materialized oracle', 'median_of_means fixed values', 'hard_threshold ...')."""
+    rng = np.random.default_rng(12)
+    for k, n in ((2, 4), (4, 13), (6, 64), (8, 200), (12, 4096)):
+        d = 1 << k
+        L = d * (d // 2 + 1)
+        x = rng.standard_normal(n)
+        for ell in list(rng.integers(0, L, size=20)) + [0, L - 1, L - d, d * (d // 2) - 1]:
+            g = fst.inner_product_with_design(x, k, int(ell))
+            assert g == orc.inner_product_with_design(x, k, int(ell)), (k, ell)
+            col = fst.projected_design_column(k, n, int(ell))
+            assert np.array_equal(col, orc.projected_design_column(k, n, int(ell)))
+    for m, J, K in ((7, 5, 1), (9, 4, 2), (16, 3, 5), (33, 2, 4)):
+        smp = rng.standard_normal((m, J * K))
+        np.testing.assert_allclose(fst.median_of_means(smp, J, K), orc.median_of_means(smp, J, K), rtol=1e-12,
+                                   atol=1e-15)
+    v = np.array([0.5, -0.1, 0.1, 0.09999, -0.2, 0.0])
+    assert np.array_equal(fst.hard_threshold(v, 0.1), orc.hard_threshold(v, 0.1))
+    with pytest.raises(ValueError):
+        fst.inner_product_with_design(np.zeros(17), 4, 0)
+    with pytest.raises(IndexError):
+        fst.projected_design_column(4, 16, 16 * 9)
+    with pytest.raises(ValueError):
+        fst.median_of_means(np.zeros((3, 5)), 2, 2)
