@@ -131,6 +131,9 @@ int fstg_preprocess_design(const void* a, int dtype, int64_t m, int64_t n, int d
 int fstg_sketch_info_get(const fstg_sketch* sk, fstg_sketch_info* info);
 /* Sketch::row_norm_max (sketch.hpp:105) */
 int fstg_row_norm_max(const fstg_sketch* sk, double* out);
+/* sketch.hpp:107-111 Sketch::embedded_matrix: A (m x n row-major, the sketch's
+ * dtype) into out (host or device); FSTG_ERR_NO_MATRIX without one. */
+int fstg_sketch_embedded_matrix(const fstg_sketch* sk, void* out);
 /* Sketch::column (sketch.hpp:114-117): copies column ell (m values) to `out`. */
 int fstg_sketch_column(const fstg_sketch* sk, int64_t ell, void* out);
 /* Raw device pointers (column-major, stride column_stride) for zero-copy use

@@ -1655,6 +1655,18 @@ int fstg_row_norm_max(const fstg_sketch* sk, double* out) {
   });
 }
 
+int fstg_sketch_embedded_matrix(const fstg_sketch* sk, void* out) {
+  return guarded([&] {
+    if (!sk || !out) throw InvalidArgument("null");
+    if (!sk->has_a) throw CodedError(FSTG_ERR_NO_MATRIX, "Sketch: no embedded matrix");
+    cuda_check(cudaSetDevice(sk->device), "cudaSetDevice");
+    const size_t es = sk->dtype == FSTG_F32 ? 4 : 8;
+    cuda_check(cudaMemcpy2D(out, size_t(sk->n) * es, sk->a, size_t(sk->lda) * es, size_t(sk->n) * es, size_t(sk->m),
+                            is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost),
+               "copy embedded matrix");
+  });
+}
+
 int fstg_sketch_column(const fstg_sketch* sk, int64_t ell, void* out) {
   return guarded([&] {
     if (!sk || !out) throw InvalidArgument("null");

@@ -95,6 +95,7 @@ EXPORTED = [
     "fstg_verify_mub", "fstg_verify_design_moments", "fstg_design_moment_target", "fstg_verify_kerdock_set",
     "fstg_transform_design_batch", "fstg_design_partial_means", "fstg_transform_from_means",
     "fstg_inner_product_with_design", "fstg_median_of_means", "fstg_hard_threshold", "fstg_projected_design_column",
+    "fstg_sketch_embedded_matrix",
 ]
 
 
@@ -296,6 +297,12 @@ class Sketch:
         """Sketch::column (sketch.hpp:114-117), copied to host."""
         out = np.zeros(self.m, dtype=self.dtype)
         _check(lib().fstg_sketch_column(self._h, C.c_int64(ell), out.ctypes.data_as(C.c_void_p)))
+        return out
+
+    def embedded_matrix(self) -> np.ndarray:
+        """Sketch::embedded_matrix (sketch.hpp:107-111): A (m, n), copied to host."""
+        out = np.zeros((self.m, self.n), dtype=self.dtype)
+        _check(lib().fstg_sketch_embedded_matrix(self._h, _ptr(out)))
         return out
 
     def gather(self, indices) -> np.ndarray:

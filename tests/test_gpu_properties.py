@@ -146,3 +146,12 @@ def test_public_helpers_match_oracle(fst, orc):
         fst.projected_design_column(4, 16, 16 * 9)
     with pytest.raises(ValueError):
         fst.median_of_means(np.zeros((3, 5)), 2, 2)
+
+
+def test_embedded_matrix(fst, tmp_path):
+    """sketch.hpp:107-111: the embedded A round-trips; a sketch loaded without A raises."""
+    a = np.random.default_rng(3).standard_normal((7, 13))
+    sk = fst.preprocess(a)
+    assert np.array_equal(sk.embedded_matrix(), a)
+    des = fst.preprocess_design(a.astype(np.float32))
+    assert np.array_equal(des.embedded_matrix(), a.astype(np.float32))

@@ -136,3 +136,5 @@ def test_gpu_load_errors_and_no_matrix(fst, orc, tmp_path):
     assert g.row_norm_max() == 0.0
     with pytest.raises(fst.NoMatrixError):
         fst.transform(g, np.ones(4), fst.StreamParams(epsilon=0.1, s=1, J=2, K=2))
+    with pytest.raises(fst.NoMatrixError):
+        g.embedded_matrix()
