@@ -418,7 +418,7 @@ def design_columns(k: int, n: int, ells) -> np.ndarray:
     return out
 
 
-def bench_gathered(a, X, p: StreamParams, seeds, gathered, L: int, threads: int, total: int):
+def bench_gathered(a, X, p: StreamParams, seeds, gathered, L: int, threads: int, total: int, predrawn: bool = False):
     """Times the reference transform() over `total` vectors cycling a pool of P prepared vectors.
     gathered: (P, J*K, m) fp64 host columns. Returns (pool support counts, wall seconds)."""
     a = np.ascontiguousarray(a, dtype=np.float64)
@@ -432,7 +432,8 @@ def bench_gathered(a, X, p: StreamParams, seeds, gathered, L: int, threads: int,
     _check(lib().orc_bench_gathered(_ptr(a), C.c_int64(m), C.c_int64(n), _ptr(X), C.c_int64(P),
                                     C.c_double(p.epsilon), C.c_double(p.delta), C.c_int64(p.s), C.c_int64(p.J),
                                     C.c_int64(p.K), C.c_int64(p.widen), _ptr(seeds), _ptr(gathered), C.c_int64(L),
-                                    C.c_int(threads), C.c_int64(total), _ptr(counts), C.byref(secs)))
+                                    C.c_int(threads), C.c_int64(total), _ptr(counts), C.byref(secs),
+                                    C.c_int(1 if predrawn else 0)))
     return counts, secs.value
 
 

@@ -358,9 +358,13 @@ int orc_design_columns(int k, std::int64_t n, const std::int64_t* ells, std::int
 int orc_bench_gathered(const double* a, std::int64_t m, std::int64_t n, const double* X, std::int64_t P,
                        double eps, double delta, std::int64_t s, std::int64_t J, std::int64_t K, std::int64_t widen,
                        const std::uint64_t* seeds, const double* gathered, std::int64_t L, int threads,
-                       std::int64_t total, std::int64_t* counts_out, double* seconds) {
+                       std::int64_t total, std::int64_t* counts_out, double* seconds, int predrawn) {
   return guarded([&] {
     const std::int64_t N = J * K;
+    // predrawn: the paper's timing convention (experiment.hpp:178-181) - draws done before the clock
+    std::vector<std::vector<std::int64_t>> drawn;
+    if (predrawn)
+      for (std::int64_t v = 0; v < P; ++v) drawn.push_back(draw_samples(L, make_params(eps, delta, s, J, K, widen, seeds[v])));
     const auto t0 = std::chrono::steady_clock::now();
     std::vector<std::thread> pool;
     threads = std::max(1, threads);
@@ -371,8 +375,9 @@ int orc_bench_gathered(const double* a, std::int64_t m, std::int64_t n, const do
           for (std::int64_t t = th; t < total; t += threads) {
             const std::int64_t v = t % P;
             StreamParams p = make_params(eps, delta, s, J, K, widen, seeds[v]);
-            const auto idx = draw_samples(L, p);
-            const auto r = transform_gathered(a, m, n, X + v * n, p, idx, gathered + v * N * m);
+            const auto r = predrawn ? transform_gathered(a, m, n, X + v * n, p, drawn[v], gathered + v * N * m)
+                                    : transform_gathered(a, m, n, X + v * n, p, draw_samples(L, p),
+                                                         gathered + v * N * m);
             if (t < P) counts_out[v] = static_cast<std::int64_t>(r.support.size());
           }
         } catch (...) {
