@@ -49,6 +49,7 @@ constexpr int kTRing = 64;                  // slots of the coefficient ring
 #endif
 constexpr int kNS = FSTG_NS;
 constexpr int kSegBytes = 16384;            // one ring stage at most
+constexpr int kSmallGroup = 4;              // samples per consumer iteration for small columns
 constexpr int kMaxStages = 64;
 // x buffers: coefficients on v+1 while the tail refines v. A third buffer (coefficients two
 // vectors ahead) measured 5% slower at config 3 (profiles/r01_stream_pipeline.txt).
@@ -399,7 +400,13 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
   constexpr int VEC = Vec<T>::N;
   constexpr int SEG = kSegBytes / static_cast<int>(sizeof(T));  // rows per segment
   constexpr int CPS = SEG / VEC;                                  // 16-byte chunks per segment
-  constexpr int CPT = CPS / kNC;                                  // chunks per consumer thread per segment
+  // NSEG == 0: small columns (m_pad <= kNC * VEC): one 16-byte chunk per consumer thread
+  // and kSmallGroup samples per consumer iteration (the per-sample handshake, not
+  // bandwidth, bounds small-m configs; the ring has >= 32 stages there).
+  constexpr bool SMALL = NSEG == 0;
+  constexpr int NSG = SMALL ? 1 : NSEG;                          // segments held per column
+  constexpr int CPT = SMALL ? 1 : CPS / kNC;                      // chunks per consumer thread per segment
+  constexpr int CG = SMALL ? kSmallGroup : 1;                     // samples per consumer iteration
 
   extern __shared__ __align__(1024) unsigned char smem[];
   const SmemLayout Ls = smem_layout<T>(A.d, A.stages, A.stage_stride, A.want, A.rstride, A.xbufs);
@@ -933,59 +940,119 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     const int64_t rows_out = partial ? A.m : A.m_pad;
     const uint64_t g0 = uint64_t(lv) * uint64_t(A.N);
 
-    T acc[NSEG][CPT][VEC];
+    T acc[NSG][CPT][VEC];
 #pragma unroll
-    for (int sg = 0; sg < NSEG; ++sg)
+    for (int sg = 0; sg < NSG; ++sg)
 #pragma unroll
       for (int c = 0; c < CPT; ++c)
 #pragma unroll
         for (int e = 0; e < VEC; ++e) acc[sg][c][e] = T(0);
 
+    auto accumulate = [&](T& a, T t, T x) {
+      if constexpr (STRICT) {
+        if constexpr (sizeof(T) == 8)
+          a = __dadd_rn(a, __dmul_rn(t, x));
+        else
+          a = __fadd_rn(a, __fmul_rn(t, x));
+      } else {
+        a = fma(t, x, a);
+      }
+    };
     int64_t jb = 0, b = 0;  // position inside the batch, batch index
     uint32_t tslot = static_cast<uint32_t>(g0 % kTRing), tphase = static_cast<uint32_t>((g0 / kTRing) & 1);
-    for (int64_t j = 0; j < A.N; ++j) {
-      T t = T(1);
-      if (!(A.debug & 1)) {
-        wp.wait(&t_full[tslot], tphase, kWConsT);
-        t = tring[tslot];
-      }
+    for (int64_t j = 0; j < A.N;) {
+      bool grouped = false;
+      if constexpr (CG > 1) {
+        if (jb + CG <= A.J && !(A.debug & 3)) {
+          // CG samples of the same batch: all waits, all loads, then the updates in j
+          // order (per element the same sequence as one sample at a time)
+          uint32_t ts[CG], tp[CG], ph[CG];
+          int st[CG];
 #pragma unroll
-      for (int sg = 0; sg < NSEG; ++sg) {
-        if (sg < A.nseg && !(A.debug & 2)) {
-          wp.wait(&full[stage], phase, kWConsCol);
-          const typename Vec<T>::V* src = reinterpret_cast<const typename Vec<T>::V*>(ring + size_t(stage) * A.stage_stride);
-          const int64_t rows_here = (sg == A.nseg - 1) ? seg_last_rows : SEG;
-#pragma unroll
-          for (int c = 0; c < CPT; ++c) {
-            const int chunk = tid + c * kNC;
-            if (int64_t(chunk) * VEC < rows_here) {
-              T vv[VEC];
-              Vec<T>::get(src[chunk], vv);
-#pragma unroll
-              for (int e = 0; e < VEC; ++e) {
-                if constexpr (STRICT) {
-                  if constexpr (sizeof(T) == 8)
-                    acc[sg][c][e] = __dadd_rn(acc[sg][c][e], __dmul_rn(t, vv[e]));
-                  else
-                    acc[sg][c][e] = __fadd_rn(acc[sg][c][e], __fmul_rn(t, vv[e]));
-                } else {
-                  acc[sg][c][e] = fma(t, vv[e], acc[sg][c][e]);
-                }
-              }
+          for (int g = 0; g < CG; ++g) {
+            ts[g] = tslot;
+            tp[g] = tphase;
+            if (++tslot == kTRing) {
+              tslot = 0;
+              tphase ^= 1u;
+            }
+            st[g] = stage;
+            ph[g] = phase;
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1u;
             }
           }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[stage]);
-          if (++stage == S) {
-            stage = 0;
-            phase ^= 1u;
+          T tg[CG];
+#pragma unroll
+          for (int g = 0; g < CG; ++g) {
+            wp.wait(&t_full[ts[g]], tp[g], kWConsT);
+            tg[g] = tring[ts[g]];
           }
+          T vv[CG][VEC];
+          const bool have = int64_t(tid) * VEC < seg_last_rows;
+#pragma unroll
+          for (int g = 0; g < CG; ++g) {
+            wp.wait(&full[st[g]], ph[g], kWConsCol);
+            if (have)
+              Vec<T>::get(reinterpret_cast<const typename Vec<T>::V*>(ring + size_t(st[g]) * A.stage_stride)[tid], vv[g]);
+          }
+          if (have) {
+#pragma unroll
+            for (int g = 0; g < CG; ++g)
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) accumulate(acc[0][0][e], tg[g], vv[g][e]);
+          }
+          __syncwarp();
+          if (lane == 0) {
+#pragma unroll
+            for (int g = 0; g < CG; ++g) {
+              mbar_arrive(&empty[st[g]]);
+              mbar_arrive(&t_empty[ts[g]]);
+            }
+          }
+          j += CG;
+          jb += CG - 1;  // + 1 below
+          grouped = true;
         }
       }
-      if (lane == 0 && !(A.debug & 1)) mbar_arrive(&t_empty[tslot]);
-      if (++tslot == kTRing) {
-        tslot = 0;
-        tphase ^= 1u;
+      if (!grouped) {
+        T t = T(1);
+        if (!(A.debug & 1)) {
+          wp.wait(&t_full[tslot], tphase, kWConsT);
+          t = tring[tslot];
+        }
+#pragma unroll
+        for (int sg = 0; sg < NSG; ++sg) {
+          if (sg < A.nseg && !(A.debug & 2)) {
+            wp.wait(&full[stage], phase, kWConsCol);
+            const typename Vec<T>::V* src =
+                reinterpret_cast<const typename Vec<T>::V*>(ring + size_t(stage) * A.stage_stride);
+            const int64_t rows_here = (sg == A.nseg - 1) ? seg_last_rows : SEG;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+              const int chunk = tid + c * kNC;
+              if (int64_t(chunk) * VEC < rows_here) {
+                T vv[VEC];
+                Vec<T>::get(src[chunk], vv);
+#pragma unroll
+                for (int e = 0; e < VEC; ++e) accumulate(acc[sg][c][e], t, vv[e]);
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1u;
+            }
+          }
+        }
+        if (lane == 0 && !(A.debug & 1)) mbar_arrive(&t_empty[tslot]);
+        if (++tslot == kTRing) {
+          tslot = 0;
+          tphase ^= 1u;
+        }
+        ++j;
       }
       if (++jb == A.J) {
         // batch b complete: mean = sum / J (IEEE division, stream.hpp:237)
@@ -993,7 +1060,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
         T* mb = means + b * bstride;
         const T Jt = static_cast<T>(A.J);
 #pragma unroll
-        for (int sg = 0; sg < NSEG; ++sg)
+        for (int sg = 0; sg < NSG; ++sg)
 #pragma unroll
           for (int c = 0; c < CPT; ++c) {
             const int64_t row0 = int64_t(sg) * SEG + int64_t(tid + c * kNC) * VEC;
@@ -1073,6 +1140,9 @@ template <typename T>
 cudaError_t launch_stream(const StreamArgs<T>& args, bool strict, int grid, cudaStream_t st) {
   const SmemLayout L = smem_layout<T>(args.d, args.stages, args.stage_stride, args.want, args.rstride, args.xbufs);
   if (L.total > static_cast<size_t>(kSmemBudget)) return cudaErrorInvalidConfiguration;
+  if (args.nseg <= 1 && args.m_pad <= int64_t(kNC) * (16 / int64_t(sizeof(T))) && args.stages >= 4 * kSmallGroup) {
+    return strict ? launch_one<T, true, 0>(args, grid, L.total, st) : launch_one<T, false, 0>(args, grid, L.total, st);
+  }
   if (args.nseg <= 1) {
     return strict ? launch_one<T, true, 1>(args, grid, L.total, st) : launch_one<T, false, 1>(args, grid, L.total, st);
   }
