@@ -49,7 +49,10 @@ constexpr int kTRing = 64;                  // slots of the coefficient ring
 #endif
 constexpr int kNS = FSTG_NS;
 constexpr int kSegBytes = 16384;            // one ring stage at most
-constexpr int kSmallGroup = 4;              // samples per consumer iteration for small columns
+#ifndef FSTG_SMALL_GROUP
+#define FSTG_SMALL_GROUP 4
+#endif
+constexpr int kSmallGroup = FSTG_SMALL_GROUP;  // samples per consumer iteration for small columns
 constexpr int kMaxStages = 64;
 // x buffers: coefficients on v+1 while the tail refines v. A third buffer (coefficients two
 // vectors ahead) measured 5% slower at config 3 (profiles/r01_stream_pipeline.txt).

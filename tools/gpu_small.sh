@@ -1,9 +1,8 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -x -q --timeout 900 -m gpu > gpurun_out/small_tests.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/small_tests.log; grep -E "^E |FAILED" gpurun_out/small_tests.log | head -5
-run() { timeout 300 python bench.py --config $1 --steps $2 --warmup 3 --no-cpu > gpurun_out/rg.json 2>gpurun_out/rg.err; python -c "
-import json,sys; d=json.load(open('gpurun_out/rg.json')); print(sys.argv[1], round(d['value']), 'e2e', d['e2e'] and round(d['e2e']['value']), d['clocks']['sm_mhz'])" "$3 config $1" 2>/dev/null || echo "$3 config $1 FAILED"; }
-for lib in n8 small; do
+run() { timeout 300 python bench.py --config $1 --steps $2 --warmup 3 --no-cpu --no-e2e > gpurun_out/rg.json 2>gpurun_out/rg.err; python -c "
+import json,sys; d=json.load(open('gpurun_out/rg.json')); print(sys.argv[1], round(d['value']), d['clocks']['sm_mhz'])" "$3 config $1" 2>/dev/null || echo "$3 config $1 FAILED"; }
+for lib in g2 g4 g8 g4 g8; do
   cp tools/variants/lib_$lib.so paper_2105_05879_b200/libfst_b200.so
-  run 1 10 $lib; run 2 10 $lib; run 3 3 $lib
+  run 1 10 $lib; run 2 10 $lib
 done
-cp tools/variants/lib_small.so paper_2105_05879_b200/libfst_b200.so
+cp tools/variants/lib_g4.so paper_2105_05879_b200/libfst_b200.so
