@@ -232,6 +232,17 @@ void keep_pool_warm(int device) {
   done.push_back(device);
 }
 
+// After calls whose transient buffers were large (retained columns: ~100 GB), give the
+// pool's free blocks back so the caller's own allocations do not find HBM reserved.
+void trim_pool(int device, cudaStream_t st, size_t keep = size_t(4) << 30) {
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    cudaStreamSynchronize(st);
+    cudaMemPoolTrimTo(pool, keep);
+  }
+  cudaGetLastError();
+}
+
 // Device scratch released at scope exit (stream-ordered).
 struct DevBuf {
   void* p = nullptr;
@@ -1173,6 +1184,7 @@ void transform_design_impl(const fstg_sketch* sk, const void* X, int64_t B, cons
   run.partial(seeds, 0, sk->m, row_block, means.as<T>(), vstride, m_io);
   run.tail(means.as<T>(), vstride, m_io, out);
   cuda_check(cudaStreamSynchronize(st), "sync");
+  trim_pool(sk->device, st);
 }
 
 
@@ -1607,6 +1619,10 @@ int fstg_sample_columns(const fstg_sketch* sk, const int64_t* indices, int64_t c
       sample_columns_impl<float>(sk, indices, count, out, static_cast<cudaStream_t>(stream));
     else
       sample_columns_impl<double>(sk, indices, count, out, static_cast<cudaStream_t>(stream));
+    // host output: the device staging buffer can be large (count columns); hand it back
+    const size_t staged = size_t(count) * size_t(sk->ldc) * (sk->dtype == FSTG_F32 ? 4 : 8);
+    if (out != nullptr && !is_device_ptr(out) && staged > (size_t(1) << 30))
+      trim_pool(sk->device, static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -1886,6 +1902,7 @@ int fstg_design_partial_means(const fstg_sketch* sk, const void* X, int64_t B, c
       run.partial(seeds, row_begin, row_end, row_block, static_cast<double*>(means), vstride, ld);
     }
     cuda_check(cudaStreamSynchronize(st), "sync");
+    trim_pool(sk->device, st);
   });
 }
 

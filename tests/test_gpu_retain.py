@@ -236,3 +236,21 @@ def test_row_sharded_partial_means_equal_design_batch(fst, dtype, mode):
         got = fst.transform_from_means(des, X[first:first + count], p, full, candidates=True, mu=True)
         for f in ("counts", "support", "values", "candidates", "mu"):
             assert _same(getattr(ref, f)[first:first + count], getattr(got, f)), f
+
+
+def test_design_transform_returns_pool_memory(fst):
+    """After a design-only transform whose transient column buffers fill most of HBM
+    (auto row blocks: ~70% of free memory) the library's pool is trimmed, so the
+    caller can allocate most of HBM again."""
+    import torch
+    rng = np.random.default_rng(4)
+    a = rng.standard_normal((4096, 1024)).astype(np.float32)
+    des = fst.preprocess_design(a)
+    B = 16384
+    X = torch.from_numpy(rng.standard_normal((B, 1024)).astype(np.float32)).cuda()
+    p = fst.StreamParams(epsilon=0.5, s=4, J=375, K=2)
+    out = fst.transform_design_batch(des, X, p, seeds=np.arange(B, dtype=np.uint64))
+    torch.cuda.synchronize()
+    assert int(out.counts.max()) >= 0
+    free, total = torch.cuda.mem_get_info()
+    assert free > 0.5 * total, (free, total)
