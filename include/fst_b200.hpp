@@ -12,7 +12,10 @@
 //   fst::transform               stream.hpp:272   -> fst_b200::transform
 //   fst::transform_with_samples  stream.hpp:197   -> fst_b200::transform_with_samples
 //   fst::TransformResult         stream.hpp:53    -> fst_b200::TransformResult
-// plus the batched stream entry point transform_batch. Errors are rethrown as
+//   fst::save / fst::load        sketch.hpp:215,241 -> fst_b200::save / load (FSTK, into HBM)
+//   inner_product_with_design, median_of_means, hard_threshold (stream.hpp:109-162),
+//   projected_design_column (kerdock.hpp:156), verify_mub / verify_design_moments
+// plus the batched entry points transform_batch / transform_design_batch. Errors are rethrown as
 // std::invalid_argument / std::out_of_range / std::overflow_error /
 // std::runtime_error exactly where the reference throws them; CUDA failures
 // (no CPU fallback exists) throw fst_b200::cuda_error.
@@ -34,6 +37,22 @@ struct cuda_error : std::runtime_error {
 struct not_supported : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+/// io.hpp:23-37 IoError family (FSTK load/save)
+struct IoError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct MagicMismatchError : IoError {
+  using IoError::IoError;
+};
+struct VersionUnsupportedError : IoError {
+  using IoError::IoError;
+};
+struct TruncatedPayloadError : IoError {
+  using IoError::IoError;
+};
+struct MalformedHeaderError : IoError {
+  using IoError::IoError;
+};
 
 inline void check(int rc) {
   if (rc == FSTG_OK) return;
@@ -44,6 +63,12 @@ inline void check(int rc) {
     case FSTG_ERR_OVERFLOW: throw std::overflow_error(msg);
     case FSTG_ERR_RUNTIME: throw std::runtime_error(msg);
     case FSTG_ERR_NOT_SUPPORTED: throw not_supported(msg);
+    case FSTG_ERR_IO: throw IoError(msg);
+    case FSTG_ERR_MAGIC: throw MagicMismatchError(msg);
+    case FSTG_ERR_VERSION: throw VersionUnsupportedError(msg);
+    case FSTG_ERR_TRUNCATED: throw TruncatedPayloadError(msg);
+    case FSTG_ERR_MALFORMED: throw MalformedHeaderError(msg);
+    case FSTG_ERR_NO_MATRIX: throw std::logic_error(msg);  // sketch.hpp:109
     default: throw cuda_error(msg);
   }
 }
@@ -117,6 +142,38 @@ class Sketch {
     return out;
   }
 
+  /// Sketch::embedded_matrix (sketch.hpp:107-111): A, m x n row-major, as double.
+  std::vector<double> embedded_matrix() const {
+    std::vector<double> out(static_cast<std::size_t>(m() * n()));
+    if (is_f64()) {
+      check(fstg_sketch_embedded_matrix(h_, out.data()));
+    } else {
+      std::vector<float> f(out.size());
+      check(fstg_sketch_embedded_matrix(h_, f.data()));
+      for (std::size_t i = 0; i < f.size(); ++i) out[i] = f[i];
+    }
+    return out;
+  }
+
+  /// Retain-sampled columns A s_ell (any sketch, including a design-only one):
+  /// indices.size() x m, row j = column indices[j], as double.
+  std::vector<double> sample_columns(const std::vector<std::int64_t>& indices) const {
+    const std::int64_t ldc = info_.column_stride;
+    std::vector<double> out(indices.size() * static_cast<std::size_t>(m()));
+    if (is_f64()) {
+      std::vector<double> buf(indices.size() * static_cast<std::size_t>(ldc));
+      check(fstg_sample_columns(h_, indices.data(), static_cast<std::int64_t>(indices.size()), buf.data(), nullptr));
+      for (std::size_t j = 0; j < indices.size(); ++j)
+        for (std::int64_t i = 0; i < m(); ++i) out[j * m() + i] = buf[j * ldc + i];
+    } else {
+      std::vector<float> buf(indices.size() * static_cast<std::size_t>(ldc));
+      check(fstg_sample_columns(h_, indices.data(), static_cast<std::int64_t>(indices.size()), buf.data(), nullptr));
+      for (std::size_t j = 0; j < indices.size(); ++j)
+        for (std::int64_t i = 0; i < m(); ++i) out[j * m() + i] = buf[j * ldc + i];
+    }
+    return out;
+  }
+
  private:
   void reset() {
     if (h_) fstg_destroy(h_);
@@ -137,6 +194,53 @@ inline Sketch preprocess(const float* a, std::int64_t m, std::int64_t n, int dev
   fstg_sketch* h = nullptr;
   check(fstg_preprocess(a, FSTG_F32, m, n, device, nullptr, &h));
   return Sketch(h);
+}
+
+/// Design-only sketch (embedded A + Kerdock tables, no columns) for n whose sketch
+/// cannot exist (n = 16384); use sample_columns / transform_design_batch on it.
+inline Sketch preprocess_design(const float* a, std::int64_t m, std::int64_t n, int device = 0) {
+  fstg_sketch* h = nullptr;
+  check(fstg_preprocess_design(a, FSTG_F32, m, n, device, nullptr, &h));
+  return Sketch(h);
+}
+
+/// sketch.hpp:215-232: FSTK v1 (float64, the reference's file) or v2 (float32).
+inline void save(const Sketch& sk, const std::string& path, int version = 1) {
+  check(fstg_save(sk.handle(), path.c_str(), version));
+}
+/// sketch.hpp:241-302 straight into HBM (dtype FSTG_F64 or FSTG_F32).
+inline Sketch load(const std::string& path, int dtype = FSTG_F64, int device = 0) {
+  fstg_sketch* h = nullptr;
+  check(fstg_load(path.c_str(), dtype, device, nullptr, &h));
+  return Sketch(h);
+}
+
+/// stream.hpp:109-121 (Kerdock index: the reference's Gray-code walk, bit-exact).
+inline double inner_product_with_design(const std::vector<double>& x, int k, std::int64_t ell, int device = 0) {
+  double out = 0;
+  check(fstg_inner_product_with_design(k, x.data(), static_cast<std::int64_t>(x.size()), ell, &out, device));
+  return out;
+}
+/// stream.hpp:147-155: samples m x (J*K), column-major (column j at j*m).
+inline std::vector<double> median_of_means(const std::vector<double>& samples, std::int64_t m, std::int64_t J,
+                                           std::int64_t K, int device = 0) {
+  if (J < 1 || K < 1 || static_cast<std::int64_t>(samples.size()) != m * J * K)
+    throw std::invalid_argument("median_of_means: samples must have J*K columns");
+  std::vector<double> out(static_cast<std::size_t>(m));
+  check(fstg_median_of_means(samples.data(), m, J, K, out.data(), device));
+  return out;
+}
+/// stream.hpp:158-162
+inline std::vector<double> hard_threshold(const std::vector<double>& v, double eps, int device = 0) {
+  std::vector<double> out(v.size());
+  check(fstg_hard_threshold(v.data(), static_cast<std::int64_t>(v.size()), eps, out.data(), device));
+  return out;
+}
+/// kerdock.hpp:156-167
+inline std::vector<double> projected_design_column(int k, std::int64_t n, std::int64_t ell, int device = 0) {
+  std::vector<double> out(static_cast<std::size_t>(n));
+  check(fstg_projected_design_column(k, n, ell, out.data(), device));
+  return out;
 }
 
 /// stream.hpp:58-69
@@ -209,6 +313,16 @@ inline void transform_batch(const Sketch& sk, const void* X, std::int64_t B, con
                             void* stream = nullptr) {
   const fstg_stream_params c = p.c();
   check(fstg_transform_batch(sk.handle(), X, B, &c, seeds, counts, support, values, nullptr, nullptr, stream));
+}
+
+/// The batched stream on a design-only sketch (row blocks of sampled columns;
+/// device memory; bit-identical to transform_batch on the full sketch).
+inline void transform_design_batch(const Sketch& sk, const void* X, std::int64_t B, const StreamParams& p,
+                                   const std::uint64_t* seeds, std::int32_t* counts, std::int32_t* support,
+                                   void* values, std::int64_t row_block = 0, void* stream = nullptr) {
+  const fstg_stream_params c = p.c();
+  check(fstg_transform_design_batch(sk.handle(), X, B, &c, seeds, row_block, counts, support, values, nullptr,
+                                    nullptr, stream));
 }
 
 // kerdock.hpp:198-317 design verifiers (GPU; policy FSTG_VERIFY_REFERENCE

@@ -198,6 +198,53 @@ int main() {
     }
     check_throws<std::invalid_argument>([&] { verify_mub(6, 4); }, "cap");
   }
+  // FSTK save/load round trip, embedded matrix, sampled columns, helpers
+  {
+    const std::vector<double> a = random_orthogonal(16, 21);
+    Sketch sk = preprocess(a.data(), 16, 16);
+    const std::string path = "/tmp/fst_b200_cpp_test.fstk";
+    save(sk, path);
+    Sketch back = load(path);
+    const std::vector<std::int64_t> idx = {0, 5, 100, sk.L() - 1};
+    const std::vector<double> c1 = sk.sample_columns(idx), c2 = back.sample_columns(idx);
+    if (c1 != c2 || back.embedded_matrix() != a || c1.size() != idx.size() * 16) {
+      std::printf("FAIL save/load/sample_columns\n");
+      ++failures;
+    }
+    for (std::size_t j = 0; j < idx.size(); ++j) {
+      const std::vector<double> col = sk.column(idx[j]);
+      for (int i = 0; i < 16; ++i)
+        if (col[i] != c1[j * 16 + i]) {
+          std::printf("FAIL sample_columns vs column\n");
+          ++failures;
+          j = idx.size();
+          break;
+        }
+    }
+    check_throws<MagicMismatchError>([&] {
+      std::FILE* f = std::fopen(path.c_str(), "r+b");
+      std::fputc('X', f);
+      std::fclose(f);
+      load(path);
+    }, "magic");
+    std::vector<double> x(16, 0.0);
+    x[3] = 1.0;
+    const std::vector<double> s5 = projected_design_column(4, 16, 5);
+    if (inner_product_with_design(x, 4, 5) != s5[3]) {
+      std::printf("FAIL inner_product_with_design\n");
+      ++failures;
+    }
+    const std::vector<double> h = hard_threshold({0.5, -0.05, 0.1}, 0.1);
+    if (h[0] != 0.5 || h[1] != 0.0 || h[2] != 0.1) {
+      std::printf("FAIL hard_threshold\n");
+      ++failures;
+    }
+    const std::vector<double> mom = median_of_means({1, 2, 3, 4, 5, 6, 7, 8}, 2, 2, 2);  // m=2: means (2,3),(6,7)
+    if (mom[0] != 4.0 || mom[1] != 5.0) {
+      std::printf("FAIL median_of_means %g %g\n", mom[0], mom[1]);
+      ++failures;
+    }
+  }
   std::printf("cpp api: %s (%d failures)\n", failures ? "FAIL" : "ok", failures);
   return failures ? 1 : 0;
 }
