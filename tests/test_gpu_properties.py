@@ -155,3 +155,21 @@ def test_embedded_matrix(fst, tmp_path):
     assert np.array_equal(sk.embedded_matrix(), a)
     des = fst.preprocess_design(a.astype(np.float32))
     assert np.array_equal(des.embedded_matrix(), a.astype(np.float32))
+
+
+def test_size_limits_fail_loudly(fst):
+    """Largest supported column height (m = 16384 fp32, four 16 KiB segments) works;
+    one row more is rejected with NotSupportedError (no silent fallback)."""
+    import torch
+    p = fst.StreamParams(epsilon=0.5, s=1, J=3, K=2)
+    for m, ok in ((16384, True), (16385, False)):
+        a = torch.randn(m, 8, device="cuda:0", generator=torch.Generator("cuda:0").manual_seed(m))
+        sk = fst.preprocess(a)
+        X = torch.randn(2, 8, device="cuda:0")
+        if ok:
+            out = fst.transform_batch(sk, X, p, seeds=np.arange(2, dtype=np.uint64))
+            assert int(out.counts.max()) >= 0
+        else:
+            with pytest.raises(fst.NotSupportedError):
+                fst.transform_batch(sk, X, p, seeds=np.arange(2, dtype=np.uint64))
+        sk.close()
