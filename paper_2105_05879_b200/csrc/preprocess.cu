@@ -609,7 +609,9 @@ static cudaError_t launch_fwht_tmem(const float* a, int64_t lda, int64_t m, int6
   const int64_t nb = b1 - b0;
   if (nb <= 0) return cudaSuccess;
   const int64_t row_tiles = (m - row0 + C::R - 1) / C::R;
-  int bpc = RETAIN ? 256 : 32;  // the A tile is reused across bpc bases (TMEM)
+  // the A tile is reused across bpc bases (TMEM); full sketch: 128 (32/64/128/256 measured
+  // 37.5/37.0/36.3/36.8 ms at n = 4096, profiles/r01_preprocess_writepath.txt)
+  int bpc = RETAIN ? 256 : 128;
   while (bpc > 1 && row_tiles * ((nb + bpc - 1) / bpc) < 148 * 8) bpc /= 2;
   const int64_t gy = (nb + bpc - 1) / bpc;
   if (row_tiles > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
