@@ -36,12 +36,18 @@ namespace fstg {
 #endif
 constexpr int kNCW = FSTG_NCW;              // consumer warps
 constexpr int kNC = kNCW * 32;              // consumer threads
-constexpr int kCW = 8;                      // coefficient warps
+#ifndef FSTG_CW
+#define FSTG_CW 8
+#endif
+constexpr int kCW = FSTG_CW;                // coefficient warps
 constexpr int kTLW = 7;                     // tail warps (median / select / refine / compact); 24 warps total
 constexpr int kTL = kTLW * 32;              // tail threads
 constexpr int kThreads = kNC + kCW * 32 + kTL + 32;  // + producer warp (768 threads with 8 consumer warps: 80 regs)
 constexpr int kWarpCoef = kNCW, kWarpTail = kNCW + kCW, kWarpProd = kNCW + kCW + kTLW;
-constexpr int kTRing = 64;                  // slots of the coefficient ring
+#ifndef FSTG_TRING
+#define FSTG_TRING 64
+#endif
+constexpr int kTRing = FSTG_TRING;          // slots of the coefficient ring
 // Samples per coefficient-warp group: one x read from shared memory serves kNS
 // samples (8 vs 4: +8% at config 3, profiles/r01_stream_pipeline.txt; 16 spills).
 #ifndef FSTG_NS
