@@ -57,15 +57,13 @@ def test_design_params_and_log2(fst, orc):
 @pytest.mark.parametrize("k", [2, 4, 6, 8, 10, 12])
 def test_kerdock_matrices_match_oracle(fst, orc, k):
     d, _ = orc.design_params(k)
-    bases = range(d // 2) if k <= 10 else list(range(64)) + list(range(d // 2 - 64, d // 2))
-    for s in bases:
+    for s in range(d // 2):                      # every basis (k = 12: 2048)
         assert fst.kerdock_matrix(k, s).tolist() == orc.kerdock_matrix(k, s).tolist(), (k, s)
 
 
-def test_kerdock_k14_sampled(fst, orc):
-    rng = np.random.default_rng(14)
-    for s in rng.integers(0, 8192, size=40):
-        assert fst.kerdock_matrix(14, int(s)).tolist() == orc.kerdock_matrix(14, int(s)).tolist()
+def test_kerdock_k14_all_bases(fst, orc):
+    for s in range(8192):                        # the config-4 design: every basis
+        assert fst.kerdock_matrix(14, s).tolist() == orc.kerdock_matrix(14, s).tolist(), s
     with pytest.raises(ValueError):
         fst.kerdock_matrix(4, 8)
 
