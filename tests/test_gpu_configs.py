@@ -70,3 +70,30 @@ def test_config5_large_candidate_sets_full_size(fst, orc, s, eps):
     sk = fst.preprocess(prob.A)
     _check_vs_gathered(fst, orc, sk, prob, 375, 2, 2)
     sk.close()
+
+
+def test_fp64_strict_bit_exact_at_n1024(fst, orc):
+    """The reference's own precision at a larger scale: fp64 STRICT at n = 1024
+    (4.3 GB sketch), mu bit-exact, candidate sets and supports identical, values
+    within 1e-12, against the oracle on the GPU's gathered fp64 columns."""
+    from paper_2105_05879_b200 import generators
+    n = 1024
+    A64 = generators.iid_gaussian(n, 1024, "cuda:0")
+    sk = fst.preprocess(A64)
+    rng = np.random.default_rng(7)
+    X = rng.standard_normal((3, n))
+    X /= np.linalg.norm(X, axis=1, keepdims=True)
+    seeds = np.array([101, 202, 303], dtype=np.uint64)
+    p = fst.StreamParams(epsilon=0.05, s=16, J=120, K=3)
+    out = fst.transform_batch(sk, X, p, seeds=seeds, candidates=True, mu=True)
+    idx = fst.draw_samples(sk, p, seeds=seeds)
+    a64 = A64.cpu().numpy()
+    for v in range(3):
+        gathered = fst.sample_columns(sk, idx[v])[:, :n]
+        r = orc.transform_gathered(a64, X[v], orc.StreamParams(epsilon=0.05, s=16, J=120, K=3), idx[v], gathered)
+        g = out.result(v)
+        assert g.mu.tobytes() == r.mu.tobytes()
+        assert g.candidate_set.tolist() == r.candidate_set.tolist()
+        assert g.support.tolist() == r.support.tolist()
+        np.testing.assert_allclose(g.values, r.values, rtol=1e-12)
+    sk.close()
