@@ -8,11 +8,10 @@
 //
 // Pinning: the restatement is checked against (1) every known-answer and
 // property test the reference's own suites hold for this path
-// (proj/tests/test_{gf2,fwht,kerdock,sketch,stream}.cpp, acceptance.cpp), and
+// (proj/tests/test_{gf2,fwht,kerdock,sketch,stream,...}.cpp, acceptance.cpp), and
 // (2) golden vectors produced by the reference's own gf2.hpp / rng.hpp compiled
-// unmodified from /root/reference (oracle/ref_golden.cpp -> oracle/_ref/), and
-// (3) the reference's full path compiled against a minimal Eigen-API shim
-// when available (oracle/_ref/ref_path). See DESIGN.md §Oracle.
+// unmodified from /root/reference (oracle/ref_golden.cpp -> oracle/_ref/). The
+// rest of the reference needs Eigen (absent, not shimmed). See DESIGN.md §4.
 //
 // Compile with -ffp-contract=off: the reference builds without -march, i.e.
 // SSE2 with no FMA, so every a*b+c is two roundings.
