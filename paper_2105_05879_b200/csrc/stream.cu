@@ -1,23 +1,23 @@
 // Fused streaming estimator + support refinement (reference stream.hpp:197-268).
 //
-// One persistent CTA works through vectors v = blockIdx.x, += gridDim.x.
-// Warp roles:
-//   * producer warp (last warp, one elected lane): streams the sampled sketch
-//     columns C[:, ell_j] (16 KiB segments) HBM -> shared memory with 1-D bulk
-//     copies (cp.async.bulk, SASS UBLKCP) into an S-stage ring guarded by
-//     full/empty mbarriers; it runs ahead across vector boundaries and marks
-//     the stream evict-first in L2.
-//   * consumer warps (NC threads): per chunk of samples compute the sample
-//     coefficients t_j = s_ell^T x (stream.hpp:89-103, 218-229) from the
-//     lane-transposed Kerdock sign tables and x in shared memory; then
-//     accumulate the per-batch running sums acc += t_j * C[:, ell_j]
-//     (stream.hpp:231-234) in registers, divide by J (stream.hpp:237), take
-//     the entrywise median of the K batch means (stream.hpp:126-143), select
-//     the `want` largest |mu| with ties to the smaller index by an MSB radix
-//     select plus an index-ordered ballot scan (stream.hpp:245-257), refine
-//     the candidates with exact fp64-accumulated row dots of A (kept
-//     L2-resident with an evict-last policy; stream.hpp:259-266) and compact
-//     the surviving (|v| >= eps) support in order.
+// One persistent CTA per SM works through vectors v = blockIdx.x, += gridDim.x,
+// with warp-specialised roles (see the role map above stream_kernel):
+//   * producer (P lanes of the last warp): streams the sampled sketch columns
+//     C[:, ell_j] (16 KiB segments) HBM -> shared memory with 1-D bulk copies
+//     (cp.async.bulk, SASS UBLKCP) into an S-stage ring guarded by full/empty
+//     mbarriers, evict-first in L2, running ahead across vector boundaries.
+//   * coefficient warps: t_j = s_ell^T x (stream.hpp:89-103, 218-229) from the
+//     lane-transposed Kerdock sign tables and x in shared memory, 8 samples per
+//     pass over x, into a 64-slot ring.
+//   * consumer warps: per-batch running sums acc += t_j * C[:, ell_j]
+//     (stream.hpp:231-234) in registers, / J (stream.hpp:237) into a
+//     double-buffered scratch slot (PARTIAL mode: into means_io).
+//   * tail warps, overlapping the next vector: entrywise median of the K batch
+//     means (stream.hpp:126-143), the `want` largest |mu| with ties to the
+//     smaller index by an MSB radix select plus an index-ordered ballot scan
+//     (stream.hpp:245-257), the exact fp64-accumulated refinement of those rows
+//     of A through a TMA row ring (A L2-resident, evict-last; stream.hpp:259-266)
+//     and the ordered compaction of the |v| >= eps support.
 // STRICT mode reproduces the reference's operation order exactly: Gray-code
 // sequential coefficient sums and separately-rounded multiply/add.
 #include <cuda_runtime.h>
@@ -395,14 +395,15 @@ __device__ __forceinline__ T coeff_strict(const StreamArgs<T>& A, const T* xs, u
 }
 
 // --------------------------------------------------------------- kernel ----
-// One persistent CTA per SM; warp roles:
+// One persistent CTA per SM; warp roles (24 warps, 768 threads):
 //   [0, 8)   consumers   : wait t_j and the column ring, acc += t_j * C[:, ell_j],
 //                          per-batch means -> L2 scratch slot (lv & 1)
-//   [8, 16)  coefficients: x -> smem (3 buffers), t_j -> 64-slot ring
-//   [16, 24) tail        : median, radix select, candidate compaction,
-//                          refinement, support compaction for vector lv while
-//                          the consumers already stream lv + 1
-//   24       producer    : bulk copies of the sampled columns (16 KiB stages)
+//   [8, 16)  coefficients: x -> smem (2 buffers), t_j -> 64-slot ring
+//   [16, 23) tail        : median, radix select, candidate compaction,
+//                          refinement (warp 16 issues the row copies, 17-22
+//                          own the 6 ring stages), support compaction for
+//                          vector lv while the consumers already stream lv + 1
+//   23       producer    : bulk copies of the sampled columns (16 KiB stages)
 template <typename T, bool STRICT, int NSEG>
 __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T> A) {
   using KT = typename KeyOf<T>::K;
