@@ -12,6 +12,12 @@
 //                      the reference order h = 1, 2, 4, ... with (x+y, x-y)
 //                      (fwht.hpp:20-29), so fp64 output is bit-identical to the
 //                      reference and fp32 output to the same algorithm in fp32.
+//  * fwht_tmem_kernel<k> — the fp32 k = 12 / 14 path of the same computation:
+//                      the CTA's A rows are parked in TMEM (tcgen05.st once,
+//                      tcgen05.ld per basis) and the next basis' sign words are
+//                      prefetched; RETAIN mode walks only bases holding a
+//                      requested column and keeps just those (fstg_sample_columns,
+//                      rows [row0, m) for the row-blocked design transform).
 //  * identity_kernel — column (d/2)*d + w = sqrt(d) * A[:, w] (sketch.hpp:200-208).
 #include <cuda_runtime.h>
 
