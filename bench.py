@@ -495,11 +495,19 @@ def run_config4(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    one_dev = os.environ.get("FSTG_BENCH_ONE_DEVICE") == "1"   # functional check only (see run_b200)
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     dev = f"cuda:{local}"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(dev))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device(dev))
     n, B, s_val, eps_val = 16384, 8192, 64, 0.05
+    if one_dev and os.environ.get("FSTG_C4_VECTORS"):          # functional check with small batches
+        B = int(os.environ["FSTG_C4_VECTORS"])
     A64 = generators.iid_gaussian(n, 16384, dev) if rank == 0 else torch.empty((n, n), dtype=torch.float64, device=dev)
     if world > 1:
         parallel.broadcast_matrix(A64, src=0)
