@@ -849,6 +849,12 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   size_t smem = 0;
   int stages = 0, stage_stride = 0, rstride = 0, xbufs = 0;
   const int grid_max = stream_grid_size<T>(args, strict, chunk, &smem, &stages, &stage_stride, &rstride, &xbufs);
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (const char* e = std::getenv("FSTG_NO_BATCH_SPLIT")) if (std::atoi(e) != 0) sms = 0;  // experiments
   if (smem > 227 * 1024) throw NotSupported("transform: shared-memory plan exceeds 227 KiB (d or want too large)");
   args.stages = stages;
   args.stage_stride = stage_stride;
@@ -963,7 +969,31 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
     args.mu = out.mu == nullptr ? nullptr : (o_dev ? static_cast<T*>(out.mu) + v0 * m : bf.mu.as<T>());
     args.means = means.as<T>();
     const int grid = static_cast<int>(std::min<int64_t>(grid_max, cb));
-    {
+    if (cb < sms && p->K > 1) {
+      // Small batch: one CTA per vector would leave SMs idle. Every (vector, batch)
+      // pair becomes a work item writing its batch mean (bit-identical: each batch
+      // sum runs over its J samples in j order), then the tail runs per vector.
+      DevBuf means_io(size_t(cb) * (p->K + 1) * args.m_pad * sizeof(T), st);
+      args.means_mode = kMeansPartial;
+      args.batch_split = 1;
+      args.means_io = means_io.as<T>();
+      args.m_io = args.m_pad;
+      args.row0 = 0;
+      args.means_vstride = 0;
+      {
+        ProfScope ps("stream", st);
+        cuda_check(launch_stream<T>(args, strict, static_cast<int>(std::min<int64_t>(sms, cb * p->K)), st),
+                   "stream kernel (batch split)");
+      }
+      args.means_mode = kMeansTail;
+      args.batch_split = 0;
+      {
+        ProfScope ps("stream_tail", st);
+        cuda_check(launch_stream<T>(args, strict, grid, st), "stream kernel (tail)");
+      }
+      args.means_mode = kMeansFull;
+      args.means_io = nullptr;
+    } else {
       ProfScope ps("stream", st);
       cuda_check(launch_stream<T>(args, strict, grid, st), "stream kernel");
     }

@@ -108,6 +108,9 @@ struct StreamArgs {
   T* means_io;
   int64_t m_io, row0;
   int64_t means_vstride;  // elements between vectors in means_io (0: (K + 1) * m_io)
+  // With kMeansPartial: 1 = every (vector, batch) pair is its own work item (small batches:
+  // B < #SMs), item w = v * K + b covering samples [b * J, (b + 1) * J) of vector v.
+  int batch_split;
   // experiment switches (env FSTG_STREAM_DEBUG; 0 in production):
   // bit 0: column pipeline only (coefficient warps idle, t = 1)
   // bit 1: coefficient pipeline only (no column loads, consumers skip the ring)

@@ -404,7 +404,7 @@ __device__ __forceinline__ T coeff_strict(const StreamArgs<T>& A, const T* xs, u
 //                          own the 6 ring stages), support compaction for
 //                          vector lv while the consumers already stream lv + 1
 //   23       producer    : bulk copies of the sampled columns (16 KiB stages)
-template <typename T, bool STRICT, int NSEG>
+template <typename T, bool STRICT, int NSEG, bool SPLIT>
 __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T> A) {
   using KT = typename KeyOf<T>::K;
   constexpr int VEC = Vec<T>::N;
@@ -448,6 +448,12 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
 
   const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
   const int S = A.stages;
+  // Work items: vectors, or (vector, batch) pairs when A.batch_split (small batches).
+  constexpr bool split = SPLIT;  // (vector, batch) work items: compile-time, so the normal path pays nothing
+  const int64_t items = split ? A.B * A.K : A.B;
+  const int64_t NI = split ? A.J : A.N;  // samples per item
+  auto item_vec = [&](int64_t w) { return split ? w / A.K : w; };
+  auto item_j0 = [&](int64_t w) { return split ? (w % A.K) * A.J : int64_t(0); };
   const int64_t dx = A.d < 4 ? 4 : A.d;
   const int64_t seg_last_rows = A.m_pad - int64_t(A.nseg - 1) * SEG;
   const uint32_t stage_bytes_full = static_cast<uint32_t>((A.nseg > 1 ? SEG : A.m_pad) * sizeof(T));
@@ -502,29 +508,31 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     if (lane < P && !(A.debug & 2) && A.means_mode != kMeansTail) {
       const uint64_t pol = policy_evict_first();
       const int nseg = A.nseg;
-      int64_t v = blockIdx.x, j = 0;
+      int64_t w = blockIdx.x, j = 0;  // work item, sample within the item
       int sg = 0;
       auto advance = [&](int by) {
         sg += by;
         while (sg >= nseg) {
           sg -= nseg;
-          if (++j == A.N) {
+          if (++j == NI) {
             j = 0;
-            v += gridDim.x;
+            w += gridDim.x;
           }
         }
       };
+      // flat sample position v * N + j0 + j of the current copy
+      auto flat = [&](int64_t ww, int64_t jj) { return item_vec(ww) * A.N + item_j0(ww) + jj; };
       advance(lane);
-      uint32_t ell_next = (v < A.B && !A.gathered) ? __ldg(A.idx + v * A.N + j) : 0u;
+      uint32_t ell_next = (w < items && !A.gathered) ? __ldg(A.idx + flat(w, j)) : 0u;
       int stage = lane;
       uint32_t phase = 0, used = 0;
-      while (v < A.B) {
-        const int64_t vc = v, jc = j;
+      while (w < items) {
+        const int64_t fc = flat(w, j);
         const int sgc = sg;
         const uint32_t ell = ell_next;
         advance(P);
-        if (v < A.B && !A.gathered) ell_next = __ldg(A.idx + v * A.N + j);
-        const T* col = A.gathered ? A.gathered + (vc * A.N + jc) * A.ldc : A.cols + static_cast<int64_t>(ell) * A.ldc;
+        if (w < items && !A.gathered) ell_next = __ldg(A.idx + flat(w, j));
+        const T* col = A.gathered ? A.gathered + fc * A.ldc : A.cols + static_cast<int64_t>(ell) * A.ldc;
         if (used) wp.wait(&empty[stage], phase ^ 1u, kWProdEmpty);
         const uint32_t bytes = (sgc == nseg - 1) ? stage_bytes_last : stage_bytes_full;
         mbar_arrive_expect_tx(&full[stage], bytes);
@@ -546,7 +554,8 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     const int cw = warp - kWarpCoef;
     const int ctid = tid - kWarpCoef * 32;  // 0 .. kCW*32-1
     uint32_t lv = 0;
-    for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
+    for (int64_t w = blockIdx.x; w < items; w += gridDim.x, ++lv) {
+      const int64_t v = item_vec(w);
       const uint32_t xb = lv % static_cast<uint32_t>(A.xbufs), xu = lv / static_cast<uint32_t>(A.xbufs);
       // (PARTIAL: no tail reads x; this role's own end-of-vector barrier orders the reuse)
       if (xu > 0 && A.means_mode != kMeansPartial) wp.wait(&x_empty[xb], (xu - 1) & 1u, kWCoefXEmpty);
@@ -555,8 +564,8 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
       for (int64_t p = ctid; p < A.d; p += kCW * 32) xs[p] = (p < A.n) ? xv[p] : T(0);
       named_bar_sync(kBarCoef, kCW * 32);
       if (ctid == 0) mbar_arrive(&x_full[xb]);
-      const uint32_t* vidx = A.idx + v * A.N;
-      const uint64_t g0 = uint64_t(lv) * uint64_t(A.N);
+      const uint32_t* vidx = A.idx + v * A.N + item_j0(w);
+      const uint64_t g0 = uint64_t(lv) * uint64_t(NI);
       if ((A.debug & 1) || A.means_mode == kMeansTail) {
         // TAIL mode (no columns) or the column-pipeline experiment: no coefficients
       } else if constexpr (STRICT) {
@@ -564,7 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
         // produced in order by the same thread, so a parity wait is never two
         // phases ahead.
         static_assert(kCW * 32 >= kTRing, "strict producers need kTRing threads");
-        for (int64_t j = ctid; ctid < kTRing && j < A.N; j += kTRing) {
+        for (int64_t j = ctid; ctid < kTRing && j < NI; j += kTRing) {
           const uint64_t g = g0 + uint64_t(j);
           const uint32_t slot = static_cast<uint32_t>(g % kTRing), u = static_cast<uint32_t>(g / kTRing);
           const T t = coeff_strict<T>(A, xs, __ldg(vidx + j));
@@ -578,22 +587,22 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
 #pragma unroll
         for (int k = 0; k < kNS; ++k) {
           const int64_t j = cw + int64_t(kCW) * k;
-          nxt[k] = j < A.N ? __ldg(vidx + j) : 0u;
+          nxt[k] = j < NI ? __ldg(vidx + j) : 0u;
         }
-        for (int64_t j0 = cw; j0 < A.N; j0 += int64_t(kCW) * kNS) {
+        for (int64_t j0 = cw; j0 < NI; j0 += int64_t(kCW) * kNS) {
           uint32_t ells[kNS];
           T t[kNS];
 #pragma unroll
           for (int k = 0; k < kNS; ++k) {
             ells[k] = nxt[k];
             const int64_t jn = j0 + int64_t(kCW) * (kNS + k);  // prefetch the next group's indices
-            nxt[k] = jn < A.N ? __ldg(vidx + jn) : 0u;
+            nxt[k] = jn < NI ? __ldg(vidx + jn) : 0u;
           }
           coeff_fast_multi<T, kNS>(A, xs, wbase, ells, lane, t);
 #pragma unroll
           for (int k = 0; k < kNS; ++k) {
             const int64_t j = j0 + int64_t(kCW) * k;
-            if (j < A.N) {
+            if (j < NI) {
               const uint64_t g = g0 + uint64_t(j);
               const uint32_t slot = static_cast<uint32_t>(g % kTRing), u = static_cast<uint32_t>(g / kTRing);
               if (u > 0) wp.wait(&t_empty[slot], (u - 1) & 1u, kWCoefTEmpty);
@@ -606,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
           __syncwarp();
         }
       } else {
-        for (int64_t j = cw; j < A.N; j += kCW) {
+        for (int64_t j = cw; j < NI; j += kCW) {
           const uint64_t g = g0 + uint64_t(j);
           const uint32_t slot = static_cast<uint32_t>(g % kTRing), u = static_cast<uint32_t>(g / kTRing);
           const T t = coeff_generic<T>(A, xs, __ldg(vidx + j), lane);
@@ -934,7 +943,8 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
   int stage = 0;
   uint32_t phase = 0;
   uint32_t lv = 0;
-  for (int64_t v = blockIdx.x; v < A.B; v += gridDim.x, ++lv) {
+  for (int64_t w = blockIdx.x; w < items; w += gridDim.x, ++lv) {
+    const int64_t v = item_vec(w);
     const uint32_t slot = lv & 1u, su = lv >> 1;
     if (A.means_mode == kMeansTail) {  // means come from means_io: only the slot handshake
       if (su > 0) wp.wait(&m_empty[slot], (su - 1) & 1u, kWConsMEmpty);
@@ -948,7 +958,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     T* means = partial ? A.means_io + v * vstride + A.row0 : scratch + slot * slot_elems;
     const int64_t bstride = partial ? A.m_io : A.m_pad;
     const int64_t rows_out = partial ? A.m : A.m_pad;
-    const uint64_t g0 = uint64_t(lv) * uint64_t(A.N);
+    const uint64_t g0 = uint64_t(lv) * uint64_t(NI);
 
     T acc[NSG][CPT][VEC];
 #pragma unroll
@@ -968,9 +978,9 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
         a = fma(t, x, a);
       }
     };
-    int64_t jb = 0, b = 0;  // position inside the batch, batch index
+    int64_t jb = 0, b = split ? w % A.K : 0;  // position inside the batch, batch index
     uint32_t tslot = static_cast<uint32_t>(g0 % kTRing), tphase = static_cast<uint32_t>((g0 / kTRing) & 1);
-    for (int64_t j = 0; j < A.N;) {
+    for (int64_t j = 0; j < NI;) {
       bool grouped = false;
       if constexpr (CG > 1) {
         if (jb + CG <= A.J && !(A.debug & 3)) {
@@ -1139,7 +1149,7 @@ int64_t stream_scratch_elems(const StreamArgs<T>& args, int grid) {
 
 template <typename T, bool STRICT, int NSEG>
 static cudaError_t launch_one(const StreamArgs<T>& args, int grid, size_t smem, cudaStream_t st) {
-  auto kern = stream_kernel<T, STRICT, NSEG>;
+  auto kern = args.batch_split ? stream_kernel<T, STRICT, NSEG, true> : stream_kernel<T, STRICT, NSEG, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   kern<<<grid, kThreads, smem, st>>>(args);

@@ -173,3 +173,25 @@ def test_size_limits_fail_loudly(fst):
             with pytest.raises(fst.NotSupportedError):
                 fst.transform_batch(sk, X, p, seeds=np.arange(2, dtype=np.uint64))
         sk.close()
+
+
+@pytest.mark.parametrize("dtype,mode,K", [(np.float32, 0, 2), (np.float64, 0, 16), (np.float32, 2, 3)])
+def test_small_batch_split_equals_large_batch(fst, dtype, mode, K):
+    """Batches smaller than the SM count run one (vector, batch) pair per work item,
+    then the tail from the batch means. Every output equals the same vectors run
+    inside a large (unsplit) batch, bit for bit."""
+    rng = np.random.default_rng(K)
+    a = rng.standard_normal((200, 256)).astype(dtype)
+    sk = fst.preprocess(a)
+    p = fst.StreamParams(epsilon=0.5, s=3, J=37, K=K, mode=mode)
+    X = rng.standard_normal((300, 256)).astype(dtype)
+    seeds = rng.integers(0, 2**63, size=300, dtype=np.int64).view(np.uint64)
+    big = fst.transform_batch(sk, X, p, seeds=seeds, candidates=True, mu=True)      # 300 >= #SMs: unsplit
+    small = fst.transform_batch(sk, X[:5], p, seeds=seeds[:5], candidates=True, mu=True)  # split
+    assert np.array_equal(big.counts[:5], small.counts)
+    valid = np.arange(small.support.shape[1])[None, :] < small.counts[:, None]
+    assert np.array_equal(big.support[:5][valid], small.support[valid])
+    assert np.array_equal(big.values[:5][valid], small.values[valid])
+    assert np.array_equal(big.candidates[:5], small.candidates)
+    assert big.mu[:5].tobytes() == small.mu.tobytes()
+    sk.close()
