@@ -527,16 +527,18 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
       int stage = lane;
       uint32_t phase = 0, used = 0;
       while (w < items) {
-        const int64_t fc = flat(w, j);
+        // everything for this copy is ready before the wait; the next index load and
+        // the bookkeeping happen after the copy is issued (the wait ends when a
+        // consumer frees the slot, so nothing else sits on the refill path)
         const int sgc = sg;
-        const uint32_t ell = ell_next;
+        const T* col = (A.gathered ? A.gathered + flat(w, j) * A.ldc : A.cols + static_cast<int64_t>(ell_next) * A.ldc) +
+                       int64_t(sgc) * SEG;
+        const uint32_t bytes = (sgc == nseg - 1) ? stage_bytes_last : stage_bytes_full;
+        if (used) wp.wait(&empty[stage], phase ^ 1u, kWProdEmpty);
+        mbar_arrive_expect_tx(&full[stage], bytes);
+        bulk_g2s(ring + size_t(stage) * A.stage_stride, col, bytes, &full[stage], pol);
         advance(P);
         if (w < items && !A.gathered) ell_next = __ldg(A.idx + flat(w, j));
-        const T* col = A.gathered ? A.gathered + fc * A.ldc : A.cols + static_cast<int64_t>(ell) * A.ldc;
-        if (used) wp.wait(&empty[stage], phase ^ 1u, kWProdEmpty);
-        const uint32_t bytes = (sgc == nseg - 1) ? stage_bytes_last : stage_bytes_full;
-        mbar_arrive_expect_tx(&full[stage], bytes);
-        bulk_g2s(ring + size_t(stage) * A.stage_stride, col + int64_t(sgc) * SEG, bytes, &full[stage], pol);
         stage += P;
         if (stage >= S) {
           stage -= S;
