@@ -35,6 +35,9 @@ J_DEFAULT, K_DEFAULT, WIDEN = 375, 2, 10
 N_DIM, S, EPS = 4096, 32, 0.1
 A_SEED, X_SEED = 4096, 20251019
 METRIC = "thresholded-Ax vectors/sec at n=4096,s=32 (1/2/4/8 B200); preprocess time"
+# FP32 adds/s of the CUDA cores, measured on a B200 at the 1965 MHz max clock (tools/micro/fadd_peak.cu:
+# 126 adds/clk/SM for FADD and FADD2 alike; profiles/r01_fadd_peak.txt)
+FP32_ADD_PEAK_TADD = 36.7
 
 
 def parse():
@@ -48,6 +51,8 @@ def parse():
     ap.add_argument("--K", type=int, default=K_DEFAULT)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--row-block", type=int, default=0,
+                    help="config 4: rows per retain-sampled block (0 = as many as ~70%% of free HBM holds)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--config", default="3", choices=["1", "2", "3", "4", "5"],
                     help="BASELINE.json configs: 3 = headline (default); 1, 2 = parity-case workloads; "
@@ -531,6 +536,9 @@ def run_config4(args):
     N = args.J * args.K
     want = fst.candidate_count(s_val, WIDEN, n)
     fst.profile_enable(True)
+    # a stream of design-only batches: keep the ~100 GB of retained-column scratch cached in the
+    # library pool between calls instead of re-mapping it every step (fstg_set_pool_retain)
+    fst.set_pool_retain(True)
     out = fst.BatchResult(torch.zeros(B, dtype=torch.int32, device=dev),
                           torch.zeros((B, want), dtype=torch.int32, device=dev),
                           torch.zeros((B, want), dtype=torch.float32, device=dev))
@@ -549,11 +557,14 @@ def run_config4(args):
         vec_ranges = [(q * B, B) for q in range(world)]
         ld = des.column_stride
 
+    breakdown = {}  # library CUDA-event scopes of the last step (ms)
+
     def step(timing):
         fst.profile_reset()
         if world == 1:
             # row-blocked design transform: one Kerdock pass for all B vectors (fstg_transform_design_batch)
-            fst.transform_design_batch(des, X, p, seeds=seeds_all[:B], out=out, stream=stream.cuda_stream)
+            fst.transform_design_batch(des, X, p, seeds=seeds_all[:B], row_block=args.row_block, out=out,
+                                       stream=stream.cuda_stream)
         else:
             # row-sharded: rank r's rows of every vector's batch means (1/W of the Kerdock pass),
             # one NCCL all-to-all of means (K x rows per vector), then the tail for my vectors
@@ -565,6 +576,9 @@ def run_config4(args):
             fst.transform_from_means(des, X, p, full, out=out, stream=stream.cuda_stream)
         ms_fwht, launches = fst.profile_read("sample_columns_fwht")
         timing.append((ms_fwht, launches))
+        breakdown.clear()
+        for name in ("draw", "sample_columns_fwht", "sample_columns_identity", "stream_partial", "stream_tail"):
+            breakdown[name] = fst.profile_read(name)[0]
 
     warm = []
     for _ in range(max(1, args.warmup)):
@@ -586,7 +600,9 @@ def run_config4(args):
     retain_ms = sum(t for t, _ in timing)
     passes = len(timing)                             # steps; each is one Kerdock pass over this rank's rows
     adds_per_pass = (des.d // 2) * n * des.d * 14 / world  # (d/2) m d log2 d over this rank's row shard
-    fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12     # nominal FP32 TFLOP/s (no measured CUDA-core peak)
+    # measured FP32 add ceiling of the CUDA cores (tools/micro/fadd_peak.cu, profiles/r01_fadd_peak.txt):
+    # FADD and packed FADD2 both retire ~126 adds/clk/SM (FADD2 halves issue slots, not pipe time)
+    fp32_peak = FP32_ADD_PEAK_TADD
     achieved = adds_per_pass * passes / (retain_ms / 1e3) / 1e12
     mean_support = float(out.counts.float().mean())
     if world > 1:
@@ -601,12 +617,14 @@ def run_config4(args):
                                     ("row-blocked design transform, one Kerdock pass per step)" if world == 1 else
                                      "row-sharded batch means, 1/N of the Kerdock pass per rank, NCCL all-to-all "
                                      "of means)")),
-                       "mean_support": mean_support},
+                       "mean_support": mean_support, "row_block": args.row_block or "auto",
+                       "scratch": "library pool retained across steps (fstg_set_pool_retain)"},
             "preprocess": {"design_ms": design_ms, "kerdock_pass_ms": retain_ms / passes,
                            "kerdock_passes_per_step": passes // args.steps,
+                           "step_breakdown_ms": {k: round(v, 2) for k, v in breakdown.items()},
                            "roofline": {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "Tadd/s",
-                                        "frac": achieved / fp32_peak, "peak_source": "nominal 148 SM x 128 lanes x "
-                                        "2 (FADD2) x 1.965 GHz"}},
+                                        "frac": achieved / fp32_peak, "peak_source": "measured FADD/FADD2 rate, "
+                                        "tools/micro/fadd_peak.cu (profiles/r01_fadd_peak.txt)"}},
             "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -303,6 +303,16 @@ int fstg_profile_read(const char* name, double* ms, int64_t* launches);
 /* Total kernel launches issued by the library since the last reset. */
 int fstg_launch_count(int64_t* launches);
 
+/* ----------------------------------------------------------- memory pool --- */
+/* Calls with very large transient buffers (the design-only transforms: ~70% of
+ * free HBM of retained columns) trim the library's stream-ordered pool on
+ * return so the caller can allocate that HBM again (default, retain = 0). With
+ * retain = 1 the pool keeps them cached for the next call: a stream of
+ * design-only batches then skips re-mapping ~100 GB per call (config 4:
+ * 4.8 -> 2.5 s per 8192-vector step), at the cost of that HBM staying reserved
+ * until retain is cleared (which trims at once). Process-wide. */
+int fstg_set_pool_retain(int retain);
+
 #ifdef __cplusplus
 }
 #endif

@@ -234,7 +234,10 @@ void keep_pool_warm(int device) {
 
 // After calls whose transient buffers were large (retained columns: ~100 GB), give the
 // pool's free blocks back so the caller's own allocations do not find HBM reserved.
+std::atomic<bool> g_pool_retain{false};  // fstg_set_pool_retain
+
 void trim_pool(int device, cudaStream_t st, size_t keep = size_t(4) << 30) {
+  if (g_pool_retain.load()) return;
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     cudaStreamSynchronize(st);
@@ -415,6 +418,13 @@ __global__ void identity_requests_kernel(const T* __restrict__ a, int64_t lda, i
   }
 }
 
+// (w = ell mod d, slot) u32 records of the sorted requests for the fp32 TMEM retain kernels
+__global__ void pack_requests_kernel(const uint64_t* __restrict__ sorted, const int64_t* __restrict__ pos,
+                                     int64_t count, uint64_t d, uint2* __restrict__ rec) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < count; r += int64_t(gridDim.x) * blockDim.x)
+    rec[r] = make_uint2(static_cast<uint32_t>(sorted[r] & (d - 1)), static_cast<uint32_t>(pos[r]));
+}
+
 __global__ void iota_kernel(int64_t* v, int64_t count) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x) v[i] = i;
 }
@@ -478,12 +488,19 @@ void sample_columns_impl(const fstg_sketch* sk, const int64_t* indices, int64_t 
   basis_ranges_kernel<<<static_cast<unsigned>((nk + 256) / 256), 256, 0, st>>>(keys_sorted.as<uint64_t>(), count, nk,
                                                                              D.d, start.as<int64_t>());
   cuda_check(cudaGetLastError(), "basis ranges");
+  DevBuf rec;
+  if (sizeof(T) == 4 && count < (int64_t{1} << 32)) {
+    rec = DevBuf(size_t(count) * sizeof(uint2), st);
+    pack_requests_kernel<<<blocks, 256, 0, st>>>(keys_sorted.as<uint64_t>(), pos_sorted.as<int64_t>(), count,
+                                                 static_cast<uint64_t>(D.d), rec.as<uint2>());
+    cuda_check(cudaGetLastError(), "pack requests");
+  }
   {
     ProfScope ps("sample_columns_fwht", st);
     const cudaError_t e = launch_fwht_retain<T>(D.k, static_cast<const T*>(sk->a), sk->lda, row1, sk->n, sk->qplain,
                                                 nk, dst, ldc_out, start.as<int64_t>(),
                                                 reinterpret_cast<const int64_t*>(keys_sorted.p), pos_sorted.as<int64_t>(),
-                                                st, row0);
+                                                st, row0, rec.p ? rec.as<uint2>() : nullptr);
     if (e == cudaErrorNotSupported) {
       cudaGetLastError();
       throw NotSupported("sample_columns: this (k, dtype) needs more than 227 KiB of shared memory per CTA");
@@ -1136,6 +1153,14 @@ struct DesignRun {
     if (row_block <= 0) {  // as many rows as ~70% of free device memory holds
       size_t free_b = 0, total_b = 0;
       cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+      cudaMemPool_t pool;  // memory the pool holds but does not use (fstg_set_pool_retain) is free to us
+      if (cudaDeviceGetDefaultMemPool(&pool, sk->device) == cudaSuccess) {
+        uint64_t reserved = 0, used = 0;
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        if (reserved > used) free_b += size_t(reserved - used);
+      }
+      cudaGetLastError();
       row_block = std::max<int64_t>(ALIGN, int64_t(double(free_b) * 0.7) / std::max<int64_t>(per_row, 1));
     }
     row_block = std::max<int64_t>(ALIGN, row_block / ALIGN * ALIGN);
@@ -1875,6 +1900,25 @@ int fstg_profile_read(const char* name, double* ms, int64_t* launches) {
   if (ms) *ms = it == g_prof.end() ? 0.0 : it->second.ms;
   if (launches) *launches = it == g_prof.end() ? 0 : it->second.launches;
   return FSTG_OK;
+}
+
+int fstg_set_pool_retain(int retain) {
+  return guarded([&] {
+    g_pool_retain.store(retain != 0);
+    if (retain == 0) {
+      int n = 0;
+      cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+      for (int dev = 0; dev < n; ++dev) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+          cuda_check(cudaDeviceSynchronize(), "sync");
+          cudaMemPoolTrimTo(pool, size_t(4) << 30);
+        }
+      }
+      cudaGetLastError();
+    }
+  });
 }
 
 int fstg_launch_count(int64_t* launches) {

@@ -15,11 +15,15 @@ cudaError_t launch_fwht_sketch(int k, const T* a, int64_t lda, int64_t m, int64_
                                int64_t basis_begin, int64_t basis_end, T* cols, int64_t ldc, cudaStream_t st);
 // Retain-sampled FWHT: only requested columns (sorted by ell; basis s owns
 // [req_start[s], req_start[s+1])) are written, to out[req_pos[r] * ldc], for
-// rows [row0, m) (row i lands at out[... + i - row0]).
+// rows [row0, m) (row i lands at out[... + i - row0]). req_rec (optional, the
+// fp32 k = 12 / 14 kernels) holds the same requests packed as (w = ell mod d,
+// slot) u32 pairs; those kernels prefetch the next basis' records into shared
+// memory while transforming the current one.
 template <typename T>
 cudaError_t launch_fwht_retain(int k, const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
                                int64_t nbases, T* out, int64_t ldc, const int64_t* req_start, const int64_t* req_ell,
-                               const int64_t* req_pos, cudaStream_t st, int64_t row0 = 0);
+                               const int64_t* req_pos, cudaStream_t st, int64_t row0 = 0,
+                               const uint2* req_rec = nullptr);
 template <typename T>
 cudaError_t launch_identity(const T* a, int64_t lda, int64_t m, int64_t n, int64_t d, int64_t nk, T* cols,
                             int64_t ldc, cudaStream_t st);

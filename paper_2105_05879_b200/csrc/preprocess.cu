@@ -331,6 +331,49 @@ __device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, float* v) {
       : "memory");
 }
 
+// 8-byte cp.async (LDGSTS) for the request-record prefetch
+__device__ __forceinline__ void cp_async_8(void* dst_smem, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// Distributed shared memory (thread-block cluster) helpers
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Cluster hand-over without cluster-scope fences (a release / acquire at
+// cluster scope compiles to MEMBAR.ALL.GPU / CCTL.IVALL, which drain this
+// SM's outstanding global stores): data moves with st.async (completes bytes
+// on the receiver's mbarrier), slots are released with relaxed remote arrivals.
+__device__ __forceinline__ void st_async_f32(uint32_t local_dst, float v, uint32_t rank, uint32_t local_bar) {
+  asm volatile(
+      "{\n\t.reg .b32 rd, rb;\n\t"
+      "mapa.shared::cluster.u32 rd, %0, %2;\n\t"
+      "mapa.shared::cluster.u32 rb, %3, %2;\n\t"
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.f32 [rd], %1, [rb];\n\t}" ::"r"(local_dst),
+      "f"(v), "r"(rank), "r"(local_bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t local_bar, uint32_t rank) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(local_bar),
+      "r"(rank)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx_cta(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void stg_f32x4(float* p, float4 v) {
+  asm volatile("st.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -353,20 +396,46 @@ struct TmemCfg {
   static constexpr int CH = E / 4;               // 16-byte chunks per thread
   static constexpr int SWC = CH - 1;             // chunk swizzle mask
   static constexpr size_t SMEM = size_t(R) * RS * sizeof(float);
+  static constexpr int RCAP = 1024;              // RETAIN: request records per basis held in shared memory
+  static constexpr int MAXBPC = 256;             // RETAIN: bases per CTA (request ranges cached in shared memory)
 };
 
-template <int KB, bool RETAIN>
+// CL > 1 (k = 14 RETAIN, one row per CTA): the CL CTAs of a cluster hold CL
+// consecutive rows and walk the same bases; every CTA writes 1/CL of the
+// requests as CL-row column segments (two lanes x 16-byte stores per request)
+// assembled in its shared receive ring through distributed shared memory — full 32-byte
+// sectors instead of one scattered 4-byte store per request and row. Each CTA
+// pushes its row's value of request j with st.async into CTA j % CL's receive
+// slot (bytes complete on that CTA's full barrier); reader warps release a slot
+// with relaxed remote arrivals on every writer's empty barrier. No cluster-wide
+// barrier per basis: a CTA may run up to SS - 1 slots ahead of its slowest peer.
+template <int KB, bool RETAIN, int CL = 1>
 __global__ void __launch_bounds__(TmemCfg<KB>::NT, TmemCfg<KB>::MIN_CTAS) fwht_tmem_kernel(
     const float* __restrict__ a, int64_t lda, int64_t m, int64_t n, const uint32_t* __restrict__ qplain,
     int64_t basis_begin, int64_t basis_end, int bases_per_cta, float* __restrict__ cols, int64_t ldc,
     const int64_t* __restrict__ req_start, const int64_t* __restrict__ req_ell, const int64_t* __restrict__ req_pos,
-    int64_t row0) {
+    int64_t row0, const uint2* __restrict__ req_rec) {
+  static_assert(CL == 1 || (RETAIN && (CL == 4 || CL == 8) && TmemCfg<KB>::R == 1),
+                "cluster merge: one row per CTA, 4 or 8 CTAs");
+  constexpr bool kMerge = CL > 1;
   using C = TmemCfg<KB>;
   constexpr int E = C::E, R = C::R, RS = C::RS, D = C::D, NT = C::NT, WPT = C::WPT, CH = C::CH, SWC = C::SWC;
-  constexpr int WPB = D / 32;
+  constexpr int WPB = D / 32, RCAP = C::RCAP;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* tile = reinterpret_cast<float*>(smem_raw);
   __shared__ uint32_t tmem_base_slot;
+  // RETAIN: (w, slot) records of the current / next visited basis (double buffer,
+  // filled by cp.async one basis ahead so the copy loop reads no global memory)
+  __shared__ __align__(16) uint2 reqbuf[RETAIN ? 2 * RCAP : 2];
+  // RETAIN: req_start[s_first .. s_last] (the CTA's request ranges; read every basis)
+  __shared__ int64_t rstart[RETAIN ? C::MAXBPC + 1 : 1];
+  // CL > 1: receive ring (SS slots of [request][row] values pushed by the cluster's CTAs) and its barriers
+  constexpr int SS = 4, NW = NT / 32;
+  __shared__ __align__(16) float recv[CL > 1 ? SS * RCAP : 1];
+  __shared__ __align__(8) uint64_t full_bar[CL > 1 ? SS : 1], empty_bar[CL > 1 ? SS : 1];
+  __shared__ uint32_t rslot[CL > 1 ? SS * (RCAP / CL) : 1];  // output slot of each received request
+  __shared__ int rmine[CL > 1 ? SS : 1];                     // received requests per slot use
+  constexpr uint32_t DL = 2;  // uses between a push and its write-back (< SS; 3 measured the same)
 
   const int tid = threadIdx.x, warp = tid / 32;
   const int64_t i0 = row0 + int64_t(blockIdx.x) * R;  // rows [row0, m): retain-sampled row blocks
@@ -410,18 +479,81 @@ __global__ void __launch_bounds__(TmemCfg<KB>::NT, TmemCfg<KB>::MIN_CTAS) fwht_t
     tmem_wait_st();
   }
 
+  if constexpr (RETAIN) {
+    for (int64_t j = tid; j <= s_last - s_first; j += NT) rstart[j] = req_start[s_first + j];
+    __syncthreads();
+  }
+  if constexpr (kMerge) {
+    if (tid == 0) {
+      for (int i = 0; i < SS; ++i) {
+        mbar_init(&full_bar[i], 1);          // this CTA's expect_tx arrival + the pushed bytes
+        mbar_init(&empty_bar[i], CL * NW);   // every reader warp of the cluster
+      }
+      fence_mbar_init();
+    }
+    cluster_sync_all();  // every peer's barriers are initialised before any remote arrive
+  }
+  auto rs = [&](int64_t sb) { return rstart[sb - s_first]; };  // req_start[sb], sb in [s_first, s_last]
+  // staged transform value at position w of row rr (layouts written after phase 2)
+  auto staged = [&](uint32_t w, int rr) -> float { return tile[w * R + rr]; };
   // RETAIN visits only bases holding a requested column (uniform per CTA)
   auto next_basis = [&](int64_t s) {
     if constexpr (RETAIN) {
-      while (s < s_last && req_start[s] == req_start[s + 1]) ++s;
+      while (s < s_last && rs(s) == rs(s + 1)) ++s;
     }
     return s;
+  };
+  // request records of basis sb into reqbuf[buf] (one commit group per call, possibly empty)
+  auto prefetch_req = [&](int64_t sb, int buf) {
+    if constexpr (RETAIN) {
+      if (sb < s_last) {
+        const int64_t lo = rs(sb), cnt = rs(sb + 1) - lo;
+        if (cnt <= RCAP)
+          for (int j = tid; j < cnt; j += NT) cp_async_8(&reqbuf[buf * RCAP + j], req_rec + lo + j);
+      }
+      cp_async_commit();
+    }
+  };
+  const uint32_t crank = CL > 1 ? cluster_ctarank() : 0;
+  const int64_t cbase = i0 - crank;  // CL > 1: the cluster's first row
+  // CL > 1: write back use ud of the receive ring (CL-row segments of this CTA's
+  // requests), then release the slot to every writer in the cluster
+  auto drain_use = [&](uint32_t ud) {
+    if constexpr (kMerge) {
+      const int slot = static_cast<int>(ud % SS);
+      mbar_wait(&full_bar[slot], (ud / SS) & 1);  // all CL rows of this use landed
+      const float* const rv = recv + slot * RCAP;
+      const uint32_t* const rsl = rslot + slot * (RCAP / CL);
+      float* const cout = cols + (cbase - row0);
+      constexpr int QD = CL / 4;  // 4-row quads (16-byte stores) per request
+      const int mine = rmine[slot];
+      for (int t = tid; t < QD * mine; t += NT) {
+        const int jj = t / QD, h = t % QD;
+        const float4 val = *reinterpret_cast<const float4*>(rv + jj * CL + 4 * h);
+        float* dst = cout + int64_t(rsl[jj]) * ldc + 4 * h;
+        const int64_t r4 = cbase + 4 * h;
+        if (r4 + 3 < m) {
+          stg_f32x4(dst, val);
+        } else {
+          if (r4 + 0 < m) dst[0] = val.x;
+          if (r4 + 1 < m) dst[1] = val.y;
+          if (r4 + 2 < m) dst[2] = val.z;
+        }
+      }
+      __syncwarp();
+      if ((tid & 31) == 0)  // this warp's reads of the slot are done: release it to every writer
+        for (int r = 0; r < CL; ++r) mbar_arrive_remote_relaxed(smem_u32(&empty_bar[slot]), r);
+    }
   };
   // sign words of the next visited basis are prefetched one iteration ahead (L2 latency)
   int64_t s = next_basis(s_first);
   uint32_t qn[WPT];
 #pragma unroll
   for (int w = 0; w < WPT; ++w) qn[w] = (s < s_last) ? __ldg(qplain + s * WPB + WPT * p1 + w) : 0u;
+  int buf = 0;
+  uint32_t use = 0;  // CL > 1: staging-slot uses so far (uniform across the cluster)
+  (void)use;
+  if (req_rec != nullptr) prefetch_req(s, 0);
   while (s < s_last) {
     const int64_t s_next = next_basis(s + 1);
     float v[E];
@@ -441,6 +573,7 @@ __global__ void __launch_bounds__(TmemCfg<KB>::NT, TmemCfg<KB>::MIN_CTAS) fwht_t
       v[e] = __uint_as_float(__float_as_uint(v[e]) ^ ((q[e / 32] << (31 - (e % 32))) & 0x80000000u));
     reg_fwht_f32_packed<C::HALF>(v);  // position bits 0 .. HALF-1
     __syncthreads();                  // previous basis' tile reads done
+    if (RETAIN && req_rec != nullptr) prefetch_req(s_next, buf ^ 1);  // its buffer's readers are past the barrier
     {
       float* dst = tile + r1 * RS + p1 * E;
 #pragma unroll
@@ -459,15 +592,79 @@ __global__ void __launch_bounds__(TmemCfg<KB>::NT, TmemCfg<KB>::MIN_CTAS) fwht_t
     if constexpr (RETAIN) {
       __syncthreads();
 #pragma unroll
+      // (a thread-contiguous 16-byte-swizzled layout with 32 STS.128 measured 5% slower)
+#pragma unroll
       for (int e = 0; e < E; ++e) tile[(int64_t(e) * E + q2) * R + r2] = v[e];
+      if (req_rec != nullptr) cp_async_wait_1();  // this basis' records landed (the next basis' may be in flight)
       __syncthreads();
-      const int64_t r_lo = req_start[s], r_hi = req_start[s + 1];
-      for (int64_t it = tid; it < (r_hi - r_lo) * R; it += NT) {
-        const int64_t r = r_lo + it / R;
-        const int rr = static_cast<int>(it % R);
-        const int64_t w = req_ell[r] - s * D;
-        if (i0 + rr < m) cols[req_pos[r] * ldc + (i0 - row0) + rr] = tile[w * R + rr];
+      const int64_t r_lo = rs(s), r_hi = rs(s + 1);
+      float* const out = cols + (i0 - row0);
+      if constexpr (kMerge) {
+        // req_rec is non-null on this path (host); records from shared memory when they fit
+        const int cnt = static_cast<int>(r_hi - r_lo);
+        const uint2* recs = cnt <= RCAP ? reqbuf + buf * RCAP : req_rec + r_lo;
+        for (int c0 = 0; c0 < cnt; c0 += RCAP) {
+          const int nc = min(RCAP, cnt - c0);
+          const int slot = static_cast<int>(use % SS);
+          const uint32_t round = use / SS;
+          // this CTA receives requests j = crank (mod CL) of the chunk: CL row values each
+          const int mine = (nc - static_cast<int>(crank) + CL - 1) / CL;
+          if (tid == 0) {
+            mbar_arrive_expect_tx_cta(&full_bar[slot], static_cast<uint32_t>(4 * CL * mine));
+            rmine[slot] = mine;
+          }
+          for (int jj = tid; jj < mine; jj += NT) rslot[slot * (RCAP / CL) + jj] = recs[c0 + jj * CL + static_cast<int>(crank)].y;
+          // every reader has released this slot's previous round (its warps arrived here)
+          if (round >= 1) mbar_wait(&empty_bar[slot], (round - 1) & 1);
+          // push: value of request j (this CTA's row) -> reader j % CL, slot entry (j / CL, row crank)
+          const uint32_t rbase = smem_u32(recv + slot * RCAP) + 4u * crank, fbar = smem_u32(&full_bar[slot]);
+          constexpr int U = 8;  // batches: all shared-memory reads first, then the pushes
+          for (int j0 = tid; j0 < nc; j0 += U * NT) {
+            float val[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) val[u] = staged(recs[c0 + min(j0 + u * NT, nc - 1)].x, 0);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int j = j0 + u * NT;
+              if (j < nc)
+                st_async_f32(rbase + 4u * static_cast<uint32_t>((j / CL) * CL), val[u], static_cast<uint32_t>(j % CL),
+                             fbar);
+            }
+          }
+          ++use;
+          if (use > DL) drain_use(use - 1 - DL);  // write back an older use: its peers are most likely done
+          if (c0 + RCAP < cnt) __syncthreads();   // next chunk reuses rslot / rmine entries (uniform)
+        }
+      } else if (req_rec != nullptr && r_hi - r_lo <= RCAP) {
+        // batches of U items: all shared-memory reads first, then the stores
+        constexpr int U = 8;
+        const uint2* rb = reqbuf + buf * RCAP;
+        const int nit = static_cast<int>(r_hi - r_lo) * R;
+        for (int it0 = tid; it0 < nit; it0 += U * NT) {
+          uint32_t slot[U];
+          float val[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int it = it0 + u * NT;
+            const uint2 rec = rb[min(it, nit - 1) / R];
+            slot[u] = rec.y;
+            val[u] = staged(rec.x, it % R);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int it = it0 + u * NT, rr = it % R;
+            if (it < nit && i0 + rr < m) out[int64_t(slot[u]) * ldc + rr] = val[u];
+          }
+        }
+      } else {
+        for (int64_t it = tid; it < (r_hi - r_lo) * R; it += NT) {
+          const int64_t r = r_lo + it / R;
+          const int rr = static_cast<int>(it % R);
+          const int64_t w = req_ell[r] - s * D;
+          if (i0 + rr < m) out[req_pos[r] * ldc + rr] = staged(static_cast<uint32_t>(w), rr);
+        }
       }
+      buf ^= 1;
     } else if (row2 < m) {
       // transposed write-back (sketch.hpp:191-196): column s*d + e*E + q2, row row2
       float* ptr = cols + (s * D + q2) * ldc + row2;
@@ -482,6 +679,13 @@ __global__ void __launch_bounds__(TmemCfg<KB>::NT, TmemCfg<KB>::MIN_CTAS) fwht_t
     s = s_next;
   }
 
+  if constexpr (kMerge) {
+    __syncthreads();  // the last pushes' rslot / rmine entries are visible to every thread
+    for (uint32_t u = use > DL ? use - DL : 0; u < use; ++u) drain_use(u);
+    // peers may still read this CTA's slots: wait for the last use of each slot to be released
+    for (uint32_t u = use > SS ? use - SS : 0; u < use; ++u) mbar_wait(&empty_bar[u % SS], (u / SS) & 1);
+    cluster_sync_all();
+  }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
@@ -573,17 +777,19 @@ template <int KB, bool RETAIN>
 static cudaError_t launch_fwht_tmem(const float* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
                                     int64_t b0, int64_t b1, float* cols, int64_t ldc, cudaStream_t st,
                                     const int64_t* req_start, const int64_t* req_ell, const int64_t* req_pos,
-                                    int64_t row0);
+                                    int64_t row0, const uint2* req_rec = nullptr);
 
 template <typename T>
 cudaError_t launch_fwht_retain(int k, const T* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
                                int64_t nbases, T* out, int64_t ldc, const int64_t* req_start, const int64_t* req_ell,
-                               const int64_t* req_pos, cudaStream_t st, int64_t row0) {
+                               const int64_t* req_pos, cudaStream_t st, int64_t row0, const uint2* req_rec) {
   if constexpr (sizeof(T) == 4) {
     if (k == 12 && (lda % 4) == 0)
-      return launch_fwht_tmem<12, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos, row0);
+      return launch_fwht_tmem<12, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos, row0,
+                                        req_rec);
     if (k == 14 && (lda % 4) == 0)
-      return launch_fwht_tmem<14, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos, row0);
+      return launch_fwht_tmem<14, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos, row0,
+                                        req_rec);
   }
   switch (k) {
     case 2: return launch_fwht_k<T, 2, true>(a, lda, m, n, qplain, 0, nbases, out, ldc, st, req_start, req_ell, req_pos, row0);
@@ -598,16 +804,16 @@ cudaError_t launch_fwht_retain(int k, const T* a, int64_t lda, int64_t m, int64_
 }
 template cudaError_t launch_fwht_retain<float>(int, const float*, int64_t, int64_t, int64_t, const uint32_t*, int64_t,
                                                float*, int64_t, const int64_t*, const int64_t*, const int64_t*,
-                                               cudaStream_t, int64_t);
+                                               cudaStream_t, int64_t, const uint2*);
 template cudaError_t launch_fwht_retain<double>(int, const double*, int64_t, int64_t, int64_t, const uint32_t*, int64_t,
                                                 double*, int64_t, const int64_t*, const int64_t*, const int64_t*,
-                                                cudaStream_t, int64_t);
+                                                cudaStream_t, int64_t, const uint2*);
 
 template <int KB, bool RETAIN>
 static cudaError_t launch_fwht_tmem(const float* a, int64_t lda, int64_t m, int64_t n, const uint32_t* qplain,
                                     int64_t b0, int64_t b1, float* cols, int64_t ldc, cudaStream_t st,
                                     const int64_t* req_start, const int64_t* req_ell, const int64_t* req_pos,
-                                    int64_t row0) {
+                                    int64_t row0, const uint2* req_rec) {
   using C = TmemCfg<KB>;
   auto kern = fwht_tmem_kernel<KB, RETAIN>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
@@ -617,12 +823,44 @@ static cudaError_t launch_fwht_tmem(const float* a, int64_t lda, int64_t m, int6
   const int64_t row_tiles = (m - row0 + C::R - 1) / C::R;
   // the A tile is reused across bpc bases (TMEM); full sketch: 128 (32/64/128/256 measured
   // 37.5/37.0/36.3/36.8 ms at n = 4096, profiles/r01_preprocess_writepath.txt)
-  int bpc = RETAIN ? 256 : 128;
+  int bpc = RETAIN ? C::MAXBPC : 128;
   while (bpc > 1 && row_tiles * ((nb + bpc - 1) / bpc) < 148 * 8) bpc /= 2;
   const int64_t gy = (nb + bpc - 1) / bpc;
   if (row_tiles > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
+  if constexpr (RETAIN && C::R == 1) {
+    // cluster-merged write-back (8 rows per cluster): needs the packed records and
+    // 16-byte aligned 4-row column segments
+    bool merge = req_rec != nullptr && (ldc % 4) == 0 && (reinterpret_cast<uintptr_t>(cols) % 16) == 0;
+    // 4 CTAs (16-byte segments): config-4 pass 145 -> 134 ms per 1024 rows; 8 CTAs (32-byte
+    // segments) 147 ms — the merge's fixed per-basis cost grows with the cluster
+    // (profiles/r01_k14_retain.txt)
+    int CL = 4;
+    if (const char* ev = std::getenv("FSTG_RETAIN_CLUSTER")) {  // experiments: 0 = off, 4 or 8 CTAs
+      CL = std::atoi(ev);
+      merge = merge && (CL == 4 || CL == 8);
+    }
+    if (merge) {
+      auto kc = CL == 4 ? fwht_tmem_kernel<KB, RETAIN, 4> : fwht_tmem_kernel<KB, RETAIN, 8>;
+      e = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+      if (e != cudaSuccess) return e;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>((row_tiles + CL - 1) / CL * CL), static_cast<unsigned>(gy));
+      cfg.blockDim = dim3(C::NT);
+      cfg.dynamicSmemBytes = C::SMEM;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = CL;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, kc, a, lda, m, n, qplain, b0, b1, bpc, cols, ldc, req_start, req_ell, req_pos,
+                                row0, req_rec);
+    }
+  }
   kern<<<dim3(static_cast<unsigned>(row_tiles), static_cast<unsigned>(gy)), C::NT, C::SMEM, st>>>(
-      a, lda, m, n, qplain, b0, b1, bpc, cols, ldc, req_start, req_ell, req_pos, row0);
+      a, lda, m, n, qplain, b0, b1, bpc, cols, ldc, req_start, req_ell, req_pos, row0, req_rec);
   return cudaGetLastError();
 }
 

@@ -89,7 +89,7 @@ EXPORTED = [
     "fstg_preprocess", "fstg_preprocess_shard", "fstg_sketch_info_get", "fstg_row_norm_max",
     "fstg_sketch_column", "fstg_sketch_gather", "fstg_sketch_device_columns", "fstg_sketch_preprocess_ms", "fstg_destroy",
     "fstg_draw_samples", "fstg_transform_batch", "fstg_transform_with_samples_batch", "fstg_profile_enable",
-    "fstg_profile_reset", "fstg_profile_read", "fstg_launch_count", "fstg_gen_gaussian",
+    "fstg_profile_reset", "fstg_profile_read", "fstg_launch_count", "fstg_set_pool_retain", "fstg_gen_gaussian",
     "fstg_gen_sparse_targets", "fstg_save", "fstg_load", "fstg_gen_mixture_targets",
     "fstg_preprocess_design", "fstg_sample_columns", "fstg_transform_gathered_batch",
     "fstg_verify_mub", "fstg_verify_design_moments", "fstg_design_moment_target", "fstg_verify_kerdock_set",
@@ -703,6 +703,11 @@ def profile_read(name: str):
     ms, n = C.c_double(), C.c_int64()
     _check(lib().fstg_profile_read(name.encode(), C.byref(ms), C.byref(n)))
     return ms.value, n.value
+
+
+def set_pool_retain(retain: bool) -> None:
+    """Keep the library pool's large transient buffers cached across calls (see fstg_set_pool_retain)."""
+    _check(lib().fstg_set_pool_retain(C.c_int(1 if retain else 0)))
 
 
 def launch_count() -> int:

@@ -254,3 +254,73 @@ def test_design_transform_returns_pool_memory(fst):
     assert int(out.counts.max()) >= 0
     free, total = torch.cuda.mem_get_info()
     assert free > 0.5 * total, (free, total)
+    # retained pool: the scratch stays cached (and is reused) until retain is cleared
+    fst.set_pool_retain(True)
+    try:
+        for _ in range(2):
+            fst.transform_design_batch(des, X, p, seeds=np.arange(B, dtype=np.uint64))
+        torch.cuda.synchronize()
+        free_kept, _ = torch.cuda.mem_get_info()
+        assert free_kept < 0.5 * total, (free_kept, total)
+    finally:
+        fst.set_pool_retain(False)
+    free, _ = torch.cuda.mem_get_info()
+    assert free > 0.5 * total, (free, total)
+
+
+def _with_cluster(cl, fn):
+    """Runs fn() with the k = 14 cluster-merged retain write-back at cluster size cl
+    (4 or 8 CTAs) or disabled (0) (FSTG_RETAIN_CLUSTER, read by the launcher at every call)."""
+    import os
+    old = os.environ.get("FSTG_RETAIN_CLUSTER")
+    os.environ["FSTG_RETAIN_CLUSTER"] = str(cl)
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ["FSTG_RETAIN_CLUSTER"]
+        else:
+            os.environ["FSTG_RETAIN_CLUSTER"] = old
+
+
+@pytest.mark.parametrize("m,cl", [(77, 8), (8, 8), (3, 8), (77, 4), (6, 4)])
+def test_retain_cluster_merge_bit_identical(fst, orc, m, cl):
+    """k = 14 (n = 5000 pads to d = 16384): the 8-CTA cluster write-back (rows
+    merged into 32-byte column segments through distributed shared memory) gives
+    the same bits as the per-row write-back, with ragged row counts (m not a
+    multiple of 8, fewer rows than a cluster), a basis holding more requests than
+    the shared-memory record buffer (chunked), duplicates and identity columns;
+    and both match A s_ell in fp64."""
+    import torch
+    n = 5000
+    rng = np.random.default_rng(m)
+    a32 = torch.from_numpy(rng.standard_normal((m, n)).astype(np.float32)).cuda()
+    des = fst.preprocess_design(a32)
+    assert des.k == 14
+    d = des.d
+    dense = 3 * d + rng.integers(0, d, size=2500)              # 2500 requests in one basis (> 1024 records)
+    idx = np.concatenate([_idx(des.L, 3000, 5, extra=[0, d - 1, des.L - d, des.L - 1]), dense]).astype(np.int64)
+    on = _with_cluster(cl, lambda: fst.sample_columns(des, idx))
+    off = _with_cluster(0, lambda: fst.sample_columns(des, idx))
+    assert on[:, :m].tobytes() == off[:, :m].tobytes()
+    S = torch.from_numpy(orc.design_columns(14, n, idx[::37])).cuda()
+    expect = (S @ a32.double().T).cpu().numpy()
+    err = np.abs(on[::37, :m].astype(np.float64) - expect).max(axis=1)
+    assert np.all(err <= 2e-5 * np.maximum(np.abs(expect).max(axis=1), 1.0)), err.max()
+
+
+def test_retain_cluster_partial_means_row_offsets(fst):
+    """Row-sharded partial means at k = 14 with row ranges that are not multiples
+    of the cluster size: cluster and per-row write-back are bit-identical."""
+    import torch
+    rng = np.random.default_rng(21)
+    m, n, B = 150, 4500, 3
+    a = torch.from_numpy(rng.standard_normal((m, n)).astype(np.float32)).cuda()
+    des = fst.preprocess_design(a)
+    X = torch.from_numpy(rng.standard_normal((B, n)).astype(np.float32)).cuda()
+    seeds = torch.from_numpy(rng.integers(0, 2**63, size=B, dtype=np.int64)).cuda()
+    p = fst.StreamParams(epsilon=0.5, s=3, J=40, K=2)
+    run = lambda: fst.design_partial_means(des, X, p, seeds=seeds, row_begin=13, row_end=141, row_block=40)  # noqa: E731
+    off = _with_cluster(0, run)
+    for cl in (4, 8):
+        assert torch.equal(_with_cluster(cl, run), off), cl
