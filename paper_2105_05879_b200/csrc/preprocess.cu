@@ -337,6 +337,7 @@ __device__ __forceinline__ void cp_async_8(void* dst_smem, const void* src) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // Distributed shared memory (thread-block cluster) helpers
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -693,6 +694,247 @@ __global__ void __launch_bounds__(TmemCfg<KB>::NT, TmemCfg<KB>::MIN_CTAS) fwht_t
 }
 
 // ---------------------------------------------------------------------------
+// Warp-specialised k = 14 retain kernel (config 4): the cluster-merged
+// write-back of fwht_tmem_kernel<14, true, CL>, with the request handling moved
+// off the butterfly warps. 256 threads per CTA, one row, CL-CTA clusters:
+//   warpgroup 0 (warps 0-3, setmaxnreg 216): TMEM row -> sign mask -> FWHT
+//     (registers, swizzled shared transpose, registers) -> staged in place
+//     (each thread rewrites the tile words it read, so no barrier before it);
+//   warpgroup 1 (warps 4-7, setmaxnreg 40): record prefetch (cp.async),
+//     st.async pushes of the requested values to the cluster, deferred
+//     16-byte write-back of the receive ring.
+// Hand-over per basis with named barriers: STAGED (id 1: wg0 arrives, wg1
+// syncs) and FREED (id 2: wg1 arrives after its pushes read the tile, wg0
+// syncs before the next transpose overwrites it); wg0's own transpose barrier
+// is id 3 (128 threads), wg1's internal barrier id 4. The copy of basis s
+// overlaps the butterflies of basis s + 1.
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_arrive(uint32_t id, uint32_t n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <int CL>
+__global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
+    const float* __restrict__ a, int64_t lda, int64_t m, int64_t n, const uint32_t* __restrict__ qplain,
+    int64_t basis_end, int bases_per_cta, float* __restrict__ cols, int64_t ldc, const int64_t* __restrict__ req_start,
+    const uint2* __restrict__ req_rec, int64_t row0) {
+  using C = TmemCfg<14>;
+  constexpr int E = C::E, D = C::D, WPT = C::WPT, CH = C::CH, SWC = C::SWC;
+  constexpr int WPB = D / 32, RCAP = C::RCAP, SS = 4, NW1 = 4;
+  constexpr uint32_t DL = 2;  // write-back lag in slot uses (1 / 2 / 3 measured the same)
+  static_assert(C::R == 1 && (CL == 4 || CL == 8), "one row per CTA, 4- or 8-CTA clusters");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* tile = reinterpret_cast<float*>(smem_raw);
+  __shared__ uint32_t tmem_base_slot;
+  __shared__ __align__(16) uint2 reqbuf[2 * RCAP];
+  __shared__ int64_t rstart[C::MAXBPC + 1];
+  __shared__ __align__(16) float recv[SS * RCAP];
+  __shared__ __align__(8) uint64_t full_bar[SS], empty_bar[SS];
+  __shared__ uint32_t rslot[SS * (RCAP / CL)];
+  __shared__ int rmine[SS];
+
+  const int tid = threadIdx.x, warp = tid / 32;
+  const bool wg0 = __shfl_sync(0xffffffffu, tid / 128, 0) == 0;  // warp-uniform by construction (setmaxnreg regions)
+  const int t0 = tid & 127;  // index within the warpgroup
+  const int64_t i0 = row0 + int64_t(blockIdx.x);
+  const int64_t s_first = int64_t(blockIdx.y) * bases_per_cta;
+  const int64_t s_last = min(basis_end, s_first + bases_per_cta);
+  const uint32_t crank = cluster_ctarank();
+  const int64_t cbase = i0 - crank;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_slot)),
+                 "n"(C::TCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  for (int64_t j = tid; j <= s_last - s_first; j += 256) rstart[j] = req_start[s_first + j];
+  if (tid == 0) {
+    for (int i = 0; i < SS; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], CL * NW1);
+    }
+    fence_mbar_init();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  cluster_sync_all();  // peers' barriers initialised before any remote arrive
+
+  auto rs = [&](int64_t sb) { return rstart[sb - s_first]; };
+  auto next_basis = [&](int64_t sb) {
+    while (sb < s_last && rs(sb) == rs(sb + 1)) ++sb;
+    return sb;
+  };
+  auto staged = [&](uint32_t w) -> float {  // inverse of the in-place staging layout
+    const uint32_t e = w / E, q = w % E;
+    return tile[e * E + (q & 3) + 4 * ((q >> 2) ^ (e & SWC))];
+  };
+
+  if (wg0) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;" ::: "memory");  // 216 + 40 = 2 x 128 (no spills)
+    const uint32_t taddr = tmem_base_slot + (static_cast<uint32_t>(32 * warp) << 16);
+    const int p1 = t0, q2 = t0;
+    {
+      float v[E];
+      const int64_t pos0 = int64_t(p1) * E;
+      if (i0 < m && pos0 + E <= n) {
+        const float* arow = a + i0 * lda;
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(arow + pos0 + e));
+          v[e] = f.x;
+          v[e + 1] = f.y;
+          v[e + 2] = f.z;
+          v[e + 3] = f.w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = (i0 < m && pos0 + e < n) ? a[i0 * lda + pos0 + e] : 0.f;
+      }
+#pragma unroll
+      for (int c = 0; c < E / 32; ++c) tmem_st_x32(taddr + 32 * c, v + 32 * c);
+      tmem_wait_st();
+    }
+    int64_t s = next_basis(s_first);
+    uint32_t qn[WPT];
+#pragma unroll
+    for (int w = 0; w < WPT; ++w) qn[w] = (s < s_last) ? __ldg(qplain + s * WPB + WPT * p1 + w) : 0u;
+    bool first = true;
+    while (s < s_last) {
+      const int64_t s_next = next_basis(s + 1);
+      float v[E];
+#pragma unroll
+      for (int c = 0; c < E / 32; ++c) tmem_ld_x32(taddr + 32 * c, v + 32 * c);
+      uint32_t q[WPT];
+#pragma unroll
+      for (int w = 0; w < WPT; ++w) q[w] = qn[w];
+      if (s_next < s_last) {
+#pragma unroll
+        for (int w = 0; w < WPT; ++w) qn[w] = __ldg(qplain + s_next * WPB + WPT * p1 + w);
+      }
+      tmem_wait_ld();
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        v[e] = __uint_as_float(__float_as_uint(v[e]) ^ ((q[e / 32] << (31 - (e % 32))) & 0x80000000u));
+      reg_fwht_f32_packed<C::HALF>(v);
+      if (!first) named_sync(2, 256);  // FREED: the copy warps' reads of the previous staging are done
+      first = false;
+      {
+        float* dst = tile + p1 * E;
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+          *reinterpret_cast<float4*>(dst + 4 * (c ^ (p1 & SWC))) =
+              make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+      }
+      named_sync(3, 128);
+      float* src = tile + (q2 & 3);
+      const int cq = q2 >> 2;
+#pragma unroll
+      for (int e = 0; e < E; ++e) v[e] = src[e * E + 4 * (cq ^ (e & SWC))];
+      reg_fwht_f32_packed<C::HALF>(v);
+#pragma unroll
+      for (int e = 0; e < E; ++e) src[e * E + 4 * (cq ^ (e & SWC))] = v[e];  // in place
+      named_arrive(1, 256);  // STAGED
+      s = s_next;
+    }
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+    uint32_t use = 0;
+    int buf = 0;
+    float* const cout = cols + (cbase - row0);
+    auto prefetch = [&](int64_t sb, int b) {  // records of basis sb into reqbuf[b]; one commit group
+      if (sb < s_last) {
+        const int64_t lo = rs(sb), cnt = rs(sb + 1) - lo;
+        if (cnt <= RCAP)
+          for (int j = t0; j < cnt; j += 128) cp_async_8(&reqbuf[b * RCAP + j], req_rec + lo + j);
+      }
+      cp_async_commit();
+    };
+    auto drain_use = [&](uint32_t ud) {
+      const int slot = static_cast<int>(ud % SS);
+      mbar_wait(&full_bar[slot], (ud / SS) & 1);
+      const float* const rv = recv + slot * RCAP;
+      const uint32_t* const rsl = rslot + slot * (RCAP / CL);
+      constexpr int QD = CL / 4;
+      const int mine = rmine[slot];
+      for (int t = t0; t < QD * mine; t += 128) {
+        const int jj = t / QD, h = t % QD;
+        const float4 val = *reinterpret_cast<const float4*>(rv + jj * CL + 4 * h);
+        float* dst = cout + int64_t(rsl[jj]) * ldc + 4 * h;
+        const int64_t r4 = cbase + 4 * h;
+        if (r4 + 3 < m) {
+          stg_f32x4(dst, val);
+        } else {
+          if (r4 + 0 < m) dst[0] = val.x;
+          if (r4 + 1 < m) dst[1] = val.y;
+          if (r4 + 2 < m) dst[2] = val.z;
+        }
+      }
+      __syncwarp();
+      if ((tid & 31) == 0)
+        for (int r = 0; r < CL; ++r) mbar_arrive_remote_relaxed(smem_u32(&empty_bar[slot]), r);
+    };
+    int64_t s = next_basis(s_first);
+    prefetch(s, 0);
+    while (s < s_last) {
+      const int64_t s_next = next_basis(s + 1);
+      cp_async_wait_all();
+      named_sync(1, 256);  // STAGED: basis s is in the tile; every copy thread finished basis s - 1
+      prefetch(s_next, buf ^ 1);
+      const int64_t r_lo = rs(s), r_hi = rs(s + 1);
+      const int cnt = static_cast<int>(r_hi - r_lo);
+      const uint2* recs = cnt <= RCAP ? reqbuf + buf * RCAP : req_rec + r_lo;
+      for (int c0 = 0; c0 < cnt; c0 += RCAP) {
+        const int nc = min(RCAP, cnt - c0);
+        const int slot = static_cast<int>(use % SS);
+        const uint32_t round = use / SS;
+        const int mine = (nc - static_cast<int>(crank) + CL - 1) / CL;
+        if (t0 == 0) {
+          mbar_arrive_expect_tx_cta(&full_bar[slot], static_cast<uint32_t>(4 * CL * mine));
+          rmine[slot] = mine;
+        }
+        for (int jj = t0; jj < mine; jj += 128)
+          rslot[slot * (RCAP / CL) + jj] = recs[c0 + jj * CL + static_cast<int>(crank)].y;
+        // all of this thread's staged values of the chunk first (RCAP / 128 = 8 at most) ...
+        constexpr int U = RCAP / 128;
+        float val[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = t0 + u * 128;
+          val[u] = j < nc ? staged(recs[c0 + j].x) : 0.f;
+        }
+        // ... so the butterfly warps can overwrite the tile while the pushes go out
+        if (c0 + RCAP >= cnt && s_next < s_last) named_arrive(2, 256);  // FREED (last chunk of this basis)
+        if (round >= 1) mbar_wait(&empty_bar[slot], (round - 1) & 1);
+        const uint32_t rbase = smem_u32(recv + slot * RCAP) + 4u * crank, fbar = smem_u32(&full_bar[slot]);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int j = t0 + u * 128;
+          if (j < nc)
+            st_async_f32(rbase + 4u * static_cast<uint32_t>((j / CL) * CL), val[u], static_cast<uint32_t>(j % CL), fbar);
+        }
+        ++use;
+        if (use > DL) drain_use(use - 1 - DL);
+        if (c0 + RCAP < cnt) named_sync(4, 128);  // next chunk reuses rslot / rmine entries
+      }
+      buf ^= 1;
+      s = s_next;
+    }
+    named_sync(4, 128);  // the last pushes' rslot / rmine entries are visible
+    for (uint32_t u = use > DL ? use - DL : 0; u < use; ++u) drain_use(u);
+    for (uint32_t u = use > SS ? use - SS : 0; u < use; ++u) mbar_wait(&empty_bar[u % SS], (u / SS) & 1);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync_all();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_slot), "n"(C::TCOLS) : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // Identity block: column nk*d + w = sqrt(d) * A[:, w] for w < n, zero for
 // n <= w < d. 32x32 tiles transposed through shared memory.
 // ---------------------------------------------------------------------------
@@ -838,6 +1080,26 @@ static cudaError_t launch_fwht_tmem(const float* a, int64_t lda, int64_t m, int6
     if (const char* ev = std::getenv("FSTG_RETAIN_CLUSTER")) {  // experiments: 0 = off, 4 or 8 CTAs
       CL = std::atoi(ev);
       merge = merge && (CL == 4 || CL == 8);
+    }
+    bool ws = KB == 14;  // warp-specialised variant (copy warps off the butterfly warps)
+    if (const char* ev = std::getenv("FSTG_RETAIN_WS")) ws = ws && std::atoi(ev) != 0;  // experiments
+    if (merge && ws) {
+      auto kw = CL == 4 ? fwht14_retain_ws_kernel<4> : fwht14_retain_ws_kernel<8>;
+      e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+      if (e != cudaSuccess) return e;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>((row_tiles + CL - 1) / CL * CL), static_cast<unsigned>(gy));
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = C::SMEM;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = CL;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, kw, a, lda, m, n, qplain, b1, bpc, cols, ldc, req_start, req_rec, row0);
     }
     if (merge) {
       auto kc = CL == 4 ? fwht_tmem_kernel<KB, RETAIN, 4> : fwht_tmem_kernel<KB, RETAIN, 8>;
