@@ -1,6 +1,8 @@
 """Config-3 preprocessing time (n = m = 4096 fp32, 137.5 GB sketch) under FSTG_PRE_LOCKSTEP
 settings (experiment switch: clusters of 2 / 4 row tiles with one relaxed cluster barrier per
-basis before the write-back), alternated on one box. Tools only."""
+basis before the write-back), alternated on one box. Tools only. The switch was measured and
+removed (profiles/r01_preprocess_writepath.txt); against the current build all three settings
+run the default kernel."""
 import os
 import sys
 import numpy as np
