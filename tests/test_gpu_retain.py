@@ -283,15 +283,17 @@ def _with_cluster(cl, fn):
             os.environ["FSTG_RETAIN_CLUSTER"] = old
 
 
-@pytest.mark.parametrize("m,cl", [(77, 8), (8, 8), (3, 8), (77, 4), (6, 4)])
-def test_retain_cluster_merge_bit_identical(fst, orc, m, cl):
+@pytest.mark.parametrize("m,cl,ws", [(77, 8, 1), (8, 8, 1), (3, 8, 1), (77, 4, 1), (6, 4, 1), (77, 4, 0), (9, 8, 0)])
+def test_retain_cluster_merge_bit_identical(fst, orc, m, cl, ws, monkeypatch):
     """k = 14 (n = 5000 pads to d = 16384): the 8-CTA cluster write-back (rows
     merged into 32-byte column segments through distributed shared memory) gives
     the same bits as the per-row write-back, with ragged row counts (m not a
     multiple of 8, fewer rows than a cluster), a basis holding more requests than
     the shared-memory record buffer (chunked), duplicates and identity columns;
-    and both match A s_ell in fp64."""
+    and both match A s_ell in fp64. ws selects the warp-specialised kernel
+    (default) or the single-warpgroup merge (FSTG_RETAIN_WS=0)."""
     import torch
+    monkeypatch.setenv("FSTG_RETAIN_WS", str(ws))
     n = 5000
     rng = np.random.default_rng(m)
     a32 = torch.from_numpy(rng.standard_normal((m, n)).astype(np.float32)).cuda()
