@@ -715,6 +715,10 @@ __device__ __forceinline__ void named_arrive(uint32_t id, uint32_t n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// receive-ring depth (4 and 6 slots measured the same, profiles/r01_k14_retain.txt)
+constexpr int kWsSlots = 4;
+constexpr size_t kWsRecvBytes = size_t(kWsSlots) * TmemCfg<14>::RCAP * sizeof(float);
+
 template <int CL>
 __global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
     const float* __restrict__ a, int64_t lda, int64_t m, int64_t n, const uint32_t* __restrict__ qplain,
@@ -722,15 +726,16 @@ __global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
     const uint2* __restrict__ req_rec, int64_t row0) {
   using C = TmemCfg<14>;
   constexpr int E = C::E, D = C::D, WPT = C::WPT, CH = C::CH, SWC = C::SWC;
-  constexpr int WPB = D / 32, RCAP = C::RCAP, SS = 4, NW1 = 4;
+  constexpr int WPB = D / 32, RCAP = C::RCAP, SS = kWsSlots, NW1 = 4;
   constexpr uint32_t DL = 2;  // write-back lag in slot uses (1 / 2 / 3 measured the same)
+  static_assert(DL < SS, "write-back lag below the ring depth");
   static_assert(C::R == 1 && (CL == 4 || CL == 8), "one row per CTA, 4- or 8-CTA clusters");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* tile = reinterpret_cast<float*>(smem_raw);
   __shared__ uint32_t tmem_base_slot;
   __shared__ __align__(16) uint2 reqbuf[2 * RCAP];
   __shared__ int64_t rstart[C::MAXBPC + 1];
-  __shared__ __align__(16) float recv[SS * RCAP];
+  float* const recv = tile + C::SMEM / sizeof(float);  // receive ring: dynamic, after the tile
   __shared__ __align__(8) uint64_t full_bar[SS], empty_bar[SS];
   __shared__ uint32_t rslot[SS * (RCAP / CL)];
   __shared__ int rmine[SS];
@@ -1085,12 +1090,12 @@ static cudaError_t launch_fwht_tmem(const float* a, int64_t lda, int64_t m, int6
     if (const char* ev = std::getenv("FSTG_RETAIN_WS")) ws = ws && std::atoi(ev) != 0;  // experiments
     if (merge && ws) {
       auto kw = CL == 4 ? fwht14_retain_ws_kernel<4> : fwht14_retain_ws_kernel<8>;
-      e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+      e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM + kWsRecvBytes));
       if (e != cudaSuccess) return e;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(static_cast<unsigned>((row_tiles + CL - 1) / CL * CL), static_cast<unsigned>(gy));
       cfg.blockDim = dim3(256);
-      cfg.dynamicSmemBytes = C::SMEM;
+      cfg.dynamicSmemBytes = C::SMEM + kWsRecvBytes;
       cfg.stream = st;
       cudaLaunchAttribute attr[1];
       attr[0].id = cudaLaunchAttributeClusterDimension;
