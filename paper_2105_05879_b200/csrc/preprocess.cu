@@ -18,6 +18,11 @@
 //                      prefetched; RETAIN mode walks only bases holding a
 //                      requested column and keeps just those (fstg_sample_columns,
 //                      rows [row0, m) for the row-blocked design transform).
+//  * fwht14_retain_ws_kernel — the k = 14 RETAIN pass (config 4) with warp
+//                      specialisation: butterfly warpgroup + copy warpgroup
+//                      (setmaxnreg), and the retained values of a 4-CTA
+//                      cluster's rows merged into 16-byte column segments
+//                      through distributed shared memory (st.async).
 //  * identity_kernel — column (d/2)*d + w = sqrt(d) * A[:, w] (sketch.hpp:200-208).
 #include <cuda_runtime.h>
 
@@ -704,8 +709,8 @@ __global__ void __launch_bounds__(TmemCfg<KB>::NT, TmemCfg<KB>::MIN_CTAS) fwht_t
 //     st.async pushes of the requested values to the cluster, deferred
 //     16-byte write-back of the receive ring.
 // Hand-over per basis with named barriers: STAGED (id 1: wg0 arrives, wg1
-// syncs) and FREED (id 2: wg1 arrives after its pushes read the tile, wg0
-// syncs before the next transpose overwrites it); wg0's own transpose barrier
+// syncs) and FREED (id 2: wg1 arrives once it holds its requested values in
+// registers, wg0 syncs before the next transpose overwrites the tile); wg0's own transpose barrier
 // is id 3 (128 threads), wg1's internal barrier id 4. The copy of basis s
 // overlaps the butterflies of basis s + 1.
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
