@@ -1906,8 +1906,9 @@ int fstg_set_pool_retain(int retain) {
   return guarded([&] {
     g_pool_retain.store(retain != 0);
     if (retain == 0) {
-      int n = 0;
+      int n = 0, cur = 0;
       cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+      cuda_check(cudaGetDevice(&cur), "cudaGetDevice");  // the caller's current device is restored
       for (int dev = 0; dev < n; ++dev) {
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
@@ -1917,6 +1918,7 @@ int fstg_set_pool_retain(int retain) {
         }
       }
       cudaGetLastError();
+      cuda_check(cudaSetDevice(cur), "cudaSetDevice");
     }
   });
 }
