@@ -55,10 +55,16 @@ constexpr int kTRing = FSTG_TRING;          // slots of the coefficient ring
 #endif
 constexpr int kNS = FSTG_NS;
 constexpr int kSegBytes = 16384;            // one ring stage at most
-#ifndef FSTG_SMALL_GROUP
-#define FSTG_SMALL_GROUP 4
+// samples per consumer iteration for small columns: FAST mode (config 2, fp32 m = 1024:
+// 3 / 4 / 5 / 6 -> 1.12M / 1.21M / 1.25M / 1.28M vectors/s) and STRICT mode (config 1, fp64
+// m = 256: 4 / 5 / 6 -> 405k / 384k / 364k), profiles/r01_stream_pipeline.txt
+#ifndef FSTG_SMALL_GROUP_FAST
+#define FSTG_SMALL_GROUP_FAST 6
 #endif
-constexpr int kSmallGroup = FSTG_SMALL_GROUP;  // samples per consumer iteration for small columns
+#ifndef FSTG_SMALL_GROUP_STRICT
+#define FSTG_SMALL_GROUP_STRICT 4
+#endif
+constexpr int kSmallGroupFast = FSTG_SMALL_GROUP_FAST, kSmallGroupStrict = FSTG_SMALL_GROUP_STRICT;
 constexpr int kMaxStages = 64;
 // x buffers: coefficients on v+1 while the tail refines v. A third buffer (coefficients two
 // vectors ahead) measured 5% slower at config 3 (profiles/r01_stream_pipeline.txt).
@@ -411,12 +417,12 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
   constexpr int SEG = kSegBytes / static_cast<int>(sizeof(T));  // rows per segment
   constexpr int CPS = SEG / VEC;                                  // 16-byte chunks per segment
   // NSEG == 0: small columns (m_pad <= kNC * VEC): one 16-byte chunk per consumer thread
-  // and kSmallGroup samples per consumer iteration (the per-sample handshake, not
+  // and kSmallGroupFast / kSmallGroupStrict samples per consumer iteration (the per-sample handshake, not
   // bandwidth, bounds small-m configs; the ring has >= 32 stages there).
   constexpr bool SMALL = NSEG == 0;
   constexpr int NSG = SMALL ? 1 : NSEG;                          // segments held per column
   constexpr int CPT = SMALL ? 1 : CPS / kNC;                      // chunks per consumer thread per segment
-  constexpr int CG = SMALL ? kSmallGroup : 1;                     // samples per consumer iteration
+  constexpr int CG = SMALL ? (STRICT ? kSmallGroupStrict : kSmallGroupFast) : 1;  // samples per consumer iteration
 
   extern __shared__ __align__(1024) unsigned char smem[];
   const SmemLayout Ls = smem_layout<T>(A.d, A.stages, A.stage_stride, A.want, A.rstride, A.xbufs);
@@ -1162,7 +1168,8 @@ template <typename T>
 cudaError_t launch_stream(const StreamArgs<T>& args, bool strict, int grid, cudaStream_t st) {
   const SmemLayout L = smem_layout<T>(args.d, args.stages, args.stage_stride, args.want, args.rstride, args.xbufs);
   if (L.total > static_cast<size_t>(kSmemBudget)) return cudaErrorInvalidConfiguration;
-  if (args.nseg <= 1 && args.m_pad <= int64_t(kNC) * (16 / int64_t(sizeof(T))) && args.stages >= 4 * kSmallGroup) {
+  if (args.nseg <= 1 && args.m_pad <= int64_t(kNC) * (16 / int64_t(sizeof(T))) &&
+      args.stages >= 4 * (strict ? kSmallGroupStrict : kSmallGroupFast)) {
     return strict ? launch_one<T, true, 0>(args, grid, L.total, st) : launch_one<T, false, 0>(args, grid, L.total, st);
   }
   if (args.nseg <= 1) {
