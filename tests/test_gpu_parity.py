@@ -346,15 +346,16 @@ def test_preprocess_shards_assemble_full_sketch(fst, orc):
         fst.preprocess_shard(a, 0, nk + 1, True)
 
 
-def test_host_buffers_chunked_equal_device_path(fst):
-    """Host-buffer batches run in growing chunks (2048, 4096, ... vectors) with
-    copies overlapped on a second stream; every output must equal the
-    device-resident path bit for bit (B = 7000: chunks 2048 + 4096 + 856)."""
+@pytest.mark.parametrize("B", [7000, 1100])
+def test_host_buffers_chunked_equal_device_path(fst, B):
+    """Host-buffer batches run in growing chunks (the first a quarter of the batch,
+    then doubling) with copies overlapped on their own streams; every output must
+    equal the device-resident path bit for bit (B = 7000: chunks 1750 + 3500 +
+    1750; B = 1100: 275 + 550 + 275)."""
     import torch
     rng = np.random.default_rng(5)
     a = rng.standard_normal((200, 256)).astype(np.float32)
     sk = fst.preprocess(a)
-    B = 7000
     X = rng.standard_normal((B, 256)).astype(np.float32)
     seeds = rng.integers(0, 2**63, size=B, dtype=np.int64)
     p = fst.StreamParams(epsilon=0.5, s=4, J=20, K=3)
