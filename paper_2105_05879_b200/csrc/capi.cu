@@ -1166,6 +1166,10 @@ struct DesignRun {
       }
       cudaGetLastError();
       row_block = std::max<int64_t>(ALIGN, int64_t(double(free_b) * 0.7) / std::max<int64_t>(per_row, 1));
+      // then equal blocks: as few as memory allows, but no ragged last block (config 4,
+      // 16384 rows: 4 x 4096 instead of 3 x ~4800 + 1984 -> 2.50 -> 2.26 s per step)
+      const int64_t rows = row_end - row_begin, nblk = (rows + row_block - 1) / row_block;
+      row_block = ((rows + nblk - 1) / nblk + ALIGN - 1) / ALIGN * ALIGN;
     }
     row_block = std::max<int64_t>(ALIGN, row_block / ALIGN * ALIGN);
     args.idx = idx32.as<uint32_t>();
