@@ -254,6 +254,8 @@ void kerdock_block(const T* a, std::int64_t m, std::int64_t n, const DesignParam
 }
 template void kerdock_block<double>(const double*, std::int64_t, std::int64_t, const DesignParams&,
                                     const std::uint64_t*, double*, std::vector<double>&, std::vector<double>&);
+template void kerdock_block<float>(const float*, std::int64_t, std::int64_t, const DesignParams&,
+                                   const std::uint64_t*, float*, std::vector<float>&, std::vector<float>&);
 
 template <typename T>
 Sketch<T> preprocess(const T* a, std::int64_t m, std::int64_t n, int threads) {
@@ -518,9 +520,9 @@ template TransformResult<double> transform_with_samples<double>(const Sketch<dou
 template TransformResult<float> transform_with_samples<float>(const Sketch<float>&, const float*,
                                                               const StreamParams&, const std::vector<std::int64_t>&);
 
-TransformResult<double> transform_gathered(const double* a, std::int64_t m, std::int64_t n, const double* x,
-                                           const StreamParams& p, const std::vector<std::int64_t>& indices,
-                                           const double* gathered) {
+template <typename T>
+TransformResult<T> transform_gathered(const T* a, std::int64_t m, std::int64_t n, const T* x, const StreamParams& p,
+                                      const std::vector<std::int64_t>& indices, const T* gathered) {
   // Same steps as transform_with_samples; sk.column(ell) replaced by the
   // gathered copy (stream.hpp:235-236).
   p.validate();
@@ -528,20 +530,20 @@ TransformResult<double> transform_gathered(const double* a, std::int64_t m, std:
     throw std::invalid_argument("transform: drawn sample count does not match J*K");
   const DesignParams design = DesignParams::make(even_log2_ceil(n));
   const std::int64_t kb = design.kerdock_bases() * design.d;
-  const double sqrt_d = std::sqrt(static_cast<double>(design.d));
-  std::vector<double> means(static_cast<std::size_t>(m * p.K), 0.0);
+  const T sqrt_d = static_cast<T>(std::sqrt(static_cast<double>(design.d)));
+  std::vector<T> means(static_cast<std::size_t>(m * p.K), T(0));
   std::uint64_t rev[16];
   std::int64_t cached_s = -1;
   for (std::int64_t b = 0; b < p.K; ++b) {
-    double* col_sum = means.data() + b * m;
+    T* col_sum = means.data() + b * m;
     for (std::int64_t j = 0; j < p.J; ++j) {
       const std::int64_t jj = b * p.J + j;
       const std::int64_t ell = indices[static_cast<std::size_t>(jj)];
       if (ell < 0 || ell >= design.L) throw std::out_of_range("Sketch::column: index out of range");
-      double t;
+      T t;
       if (ell >= kb) {
         const std::int64_t pos = ell - kb;
-        t = pos < n ? sqrt_d * x[pos] : 0.0;
+        t = pos < n ? sqrt_d * x[pos] : T(0);
       } else {
         const std::int64_t s = ell / design.d;
         if (s != cached_s) {
@@ -551,13 +553,13 @@ TransformResult<double> transform_gathered(const double* a, std::int64_t m, std:
         }
         t = kerdock_inner_product(x, n, design.d, rev, static_cast<std::uint64_t>(ell % design.d));
       }
-      if (t == 0.0) continue;
-      const double* col = gathered + jj * m;
+      if (t == T(0)) continue;
+      const T* col = gathered + jj * m;
       for (std::int64_t i = 0; i < m; ++i) col_sum[i] += t * col[i];
     }
   }
-  for (auto& v : means) v /= static_cast<double>(p.J);
-  TransformResult<double> res;
+  for (auto& v : means) v /= static_cast<T>(p.J);
+  TransformResult<T> res;
   res.mu = median_of_batch_means(means.data(), m, p.K);
   res.samples_used = p.J * p.K;
   const std::int64_t want = candidate_count(p.s, p.widen, m);
@@ -565,21 +567,27 @@ TransformResult<double> transform_gathered(const double* a, std::int64_t m, std:
   std::iota(order.begin(), order.end(), std::int64_t{0});
   const auto& mu = res.mu;
   std::nth_element(order.begin(), order.begin() + want, order.end(), [&mu](std::int64_t u, std::int64_t w) {
-    const double mu_u = std::abs(mu[u]), mu_w = std::abs(mu[w]);
+    const T mu_u = std::abs(mu[u]), mu_w = std::abs(mu[w]);
     return mu_u != mu_w ? mu_u > mu_w : u < w;
   });
   res.candidate_set.assign(order.begin(), order.begin() + want);
   std::sort(res.candidate_set.begin(), res.candidate_set.end());
   for (const std::int64_t i : res.candidate_set) {
-    double v = 0;
+    T v = 0;
     for (std::int64_t j = 0; j < n; ++j) v += a[i * n + j] * x[j];
-    if (std::abs(v) >= p.epsilon) {
+    if (std::abs(v) >= static_cast<T>(p.epsilon)) {
       res.support.push_back(i);
       res.values.push_back(v);
     }
   }
   return res;
 }
+template TransformResult<double> transform_gathered<double>(const double*, std::int64_t, std::int64_t, const double*,
+                                                            const StreamParams&, const std::vector<std::int64_t>&,
+                                                            const double*);
+template TransformResult<float> transform_gathered<float>(const float*, std::int64_t, std::int64_t, const float*,
+                                                          const StreamParams&, const std::vector<std::int64_t>&,
+                                                          const float*);
 
 // ----------------------------------------------------------- generators ----
 

@@ -175,9 +175,9 @@ TransformResult<T> transform_with_samples(const Sketch<T>& sk, const T* x, const
 /// drawn.use_gathered): identical arithmetic, columns supplied by the caller
 /// (gathered: N x m, row j = column ell_j). Used to check full-size (n=4096)
 /// GPU runs without materialising the 275 GB fp64 sketch.
-TransformResult<double> transform_gathered(const double* a, std::int64_t m, std::int64_t n, const double* x,
-                                           const StreamParams& p, const std::vector<std::int64_t>& indices,
-                                           const double* gathered);
+template <typename T>
+TransformResult<T> transform_gathered(const T* a, std::int64_t m, std::int64_t n, const T* x, const StreamParams& p,
+                                      const std::vector<std::int64_t>& indices, const T* gathered);
 
 // ----------------------------------------------- kerdock.hpp:198-317 verifiers --
 

@@ -387,27 +387,41 @@ def _transform(sk: Sketch, x, p: StreamParams, indices) -> TransformResult:
     return TransformResult(sup[:k].copy(), vals[:k].copy(), cand, mu, p.J * p.K)
 
 
-def transform_gathered(a, x, p: StreamParams, indices, gathered) -> TransformResult:
-    """draw_and_gather path (stream.hpp:184-191): gathered is (J*K, m), row j = column indices[j]."""
-    a = np.ascontiguousarray(a, dtype=np.float64)
-    x = np.ascontiguousarray(x, dtype=np.float64)
+def transform_gathered(a, x, p: StreamParams, indices, gathered, dtype=np.float64) -> TransformResult:
+    """draw_and_gather path (stream.hpp:184-191): gathered is (J*K, m), row j = column indices[j].
+    dtype float32 runs the same arithmetic in float (Scalar = float)."""
+    dtype = np.dtype(dtype)
+    a = np.ascontiguousarray(a, dtype=dtype)
+    x = np.ascontiguousarray(x, dtype=dtype)
     m, n = a.shape
     indices = np.ascontiguousarray(indices, dtype=np.int64)
-    gathered = np.ascontiguousarray(gathered, dtype=np.float64)
+    gathered = np.ascontiguousarray(gathered, dtype=dtype)
     if gathered.shape != (p.J * p.K, m):
         raise ValueError("gathered must be (J*K, m)")
     want = candidate_count(p.s, p.widen, m)
-    mu = np.zeros(m)
+    mu = np.zeros(m, dtype=dtype)
     cand = np.zeros(want, dtype=np.int64)
     sup = np.zeros(want, dtype=np.int64)
-    vals = np.zeros(want)
+    vals = np.zeros(want, dtype=dtype)
     ns = C.c_int64()
-    _check(lib().orc_transform_gathered(_ptr(a), C.c_int64(m), C.c_int64(n), _ptr(x), C.c_double(p.epsilon),
-                                        C.c_double(p.delta), C.c_int64(p.s), C.c_int64(p.J), C.c_int64(p.K),
-                                        C.c_int64(p.widen), _ptr(indices), _ptr(gathered), _ptr(mu), _ptr(cand),
-                                        _ptr(sup), _ptr(vals), C.byref(ns)))
+    fn = lib().orc_transform_gathered if dtype == np.float64 else lib().orc_transform_gathered_f32
+    _check(fn(_ptr(a), C.c_int64(m), C.c_int64(n), _ptr(x), C.c_double(p.epsilon),
+              C.c_double(p.delta), C.c_int64(p.s), C.c_int64(p.J), C.c_int64(p.K),
+              C.c_int64(p.widen), _ptr(indices), _ptr(gathered), _ptr(mu), _ptr(cand),
+              _ptr(sup), _ptr(vals), C.byref(ns)))
     k = ns.value
     return TransformResult(sup[:k].copy(), vals[:k].copy(), cand, mu, p.J * p.K)
+
+
+def kerdock_block(a, s: int, dtype=np.float64) -> np.ndarray:
+    """Kerdock basis s of preprocess(a) (sketch.hpp:171-196): (d, m), row w = column s*d + w."""
+    a = np.ascontiguousarray(a, dtype=dtype)
+    m, n = a.shape
+    d = 1 << even_log2_ceil(n)
+    out = np.zeros((d, m), dtype=dtype)
+    _check(lib().orc_kerdock_block(_ptr(a), C.c_int(1 if a.dtype == np.float64 else 0), C.c_int64(m),
+                                   C.c_int64(n), C.c_int64(s), _ptr(out)))
+    return out
 
 
 def design_columns(k: int, n: int, ells) -> np.ndarray:

@@ -279,3 +279,26 @@ def test_acceptance_mom_deviation_rate(orc):  # acceptance.cpp:151-179 (reduced:
         r = orc.transform(sk, x, _params(orc, epsilon=0.05, s=8, J=J, K=K, seed=9000 + t))
         fails += int(np.max(np.abs(r.mu - truth)) >= 0.1)
     assert fails / 40 <= 0.1 + 3 * np.sqrt(0.1 / 40)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_gathered_transform_and_block_match_full_sketch(orc, dtype):
+    """The two checker entry points the full-size GPU tests use: kerdock_block (one basis of
+    sketch.hpp:171-196) equals that basis of preprocess(), and the draw_and_gather transform
+    (stream.hpp:184-191) equals transform() bit for bit, in fp64 and run in float."""
+    rng = np.random.default_rng(12)
+    a = rng.standard_normal((24, 50)).astype(dtype)
+    sk = orc.preprocess(a, dtype=dtype)
+    cols = sk.columns()
+    for s in (0, 7, sk.d // 2 - 1):
+        assert orc.kerdock_block(a, s, dtype).tobytes() == cols[s * sk.d:(s + 1) * sk.d].tobytes()
+    for t in range(4):
+        x = rng.standard_normal(50).astype(dtype)
+        p = _params(orc, epsilon=0.3, s=3, J=40, K=3, seed=100 + t)
+        idx = orc.draw_samples(sk.L, p)
+        r1 = orc.transform(sk, x, p)
+        r2 = orc.transform_gathered(a, x, p, idx, cols[idx], dtype=dtype)
+        assert r1.mu.tobytes() == r2.mu.tobytes()
+        assert r1.candidate_set.tolist() == r2.candidate_set.tolist()
+        assert r1.support.tolist() == r2.support.tolist()
+        assert r1.values.tobytes() == r2.values.tobytes()
