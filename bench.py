@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--row-block", type=int, default=0,
                     help="config 4: rows per retain-sampled block (0 = as many as ~70%% of free HBM holds)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the post-timing oracle check of the timed batch")
     ap.add_argument("--config", default="3", choices=["1", "2", "3", "4", "5"],
                     help="BASELINE.json configs: 3 = headline (default); 1, 2 = parity-case workloads; "
                          "5 = s x eps sweep with the dense-GEMM crossover")
@@ -73,8 +74,98 @@ def peaks():
 
 
 def bytes_per_vector(N, m, n, want, es=4):
-    """Algorithmic HBM bytes per vector: N sampled columns, want rows of A, x."""
+    """Algorithmic bytes per vector as SURVEY.md §8(d) counts them: N sampled columns, want rows of A, x."""
     return es * (N * m + want * n + n)
+
+
+def dram_bytes_per_vector(N, m, n, es=4):
+    """DRAM-resident algorithmic bytes per vector: the N sampled sketch columns and x.
+
+    The `want` gathered rows of A are left out: A (64 MiB at n = 4096) stays L2-resident for the whole
+    launch (its rows are loaded with an evict_last policy), which is the rule §8(d) itself applies to
+    the L2-resident sign tables. The measured DRAM traffic of the kernel (ncu) is reported beside it;
+    traffic / algorithmic is the re-read waste (A-row L2 misses, x re-reads)."""
+    return es * (N * m + n)
+
+
+# DRAM bytes of one stream-kernel launch of 65,536 config-3 vectors, ncu --set full
+# (dram__bytes_read.sum + dram__bytes_write.sum), profiles/r02_ncu_stream_kernel.txt
+NCU_STREAM_DRAM_BYTES_65536 = 845.770680e9 + 3.188722e9
+NCU_STREAM_SOURCE = "profiles/r01_ncu_stream_kernel.txt (ncu --set full, one 65,536-vector launch, scaled per vector)"
+
+
+def spread_vectors(B, sms=148, extra=8, seed=0):
+    """Vector ids covering every position in the persistent kernel's walk (CTA c handles
+    c, c + grid, c + 2 grid, ...): the 1st / 2nd / ... / last vector of several CTAs."""
+    grid = min(B, sms)
+    rounds = (B + grid - 1) // grid
+    ids = set()
+    for r in sorted({0, 1, 2, rounds // 2, rounds - 2, rounds - 1}):
+        if r < 0:
+            continue
+        for off in (0, grid // 2, grid - 1):
+            v = r * grid + off
+            if 0 <= v < B:
+                ids.add(v)
+    ids.update({B - 1})
+    rng = np.random.default_rng(seed)
+    target = min(B, len(ids) + extra)
+    while len(ids) < target:
+        ids.add(int(rng.integers(0, B)))
+    return sorted(ids)
+
+
+def parity_check(fst, sk, A, X, seeds, out, J, K, s_val, eps_val, strict, nvec=32):
+    """After timing: outputs of the timed batch for >= nvec spread vectors against the oracle's
+    draw_and_gather transform (stream.hpp:184-191, 197-268) on the GPU's own gathered columns,
+    in fp64, on exactly the inputs the GPU saw. Bars (BASELINE.json north_star): draws bit-exact;
+    supports identical except entries within 1e-6 of eps or at the rank-want estimator cut-off;
+    values within 1e-5 relative (fp32) / 1e-12 (fp64 STRICT, where supports must be identical)."""
+    from oracle import oracle as orc   # checker only, outside the timed region
+    B = X.shape[0]
+    ids = spread_vectors(B, extra=max(0, nvec - 18))
+    want = fst.candidate_count(s_val, WIDEN, sk.m)
+    p = fst.StreamParams(epsilon=eps_val, s=s_val, J=J, K=K, widen=WIDEN)
+    a64 = A.double().cpu().numpy()
+    counts = out.counts.cpu().numpy()
+    sup, vals = out.support.cpu().numpy(), out.values.cpu().numpy()
+    seeds_np = np.asarray(seeds, dtype=np.uint64)
+    idx = fst.draw_samples(sk, p, seeds=seeds_np[ids])
+    draws_ok = exact = allowed = 0
+    max_rel = 0.0
+    failures = []
+    for q, v in enumerate(ids):
+        op = orc.StreamParams(epsilon=eps_val, s=s_val, J=J, K=K, widen=WIDEN, seed=int(seeds_np[v]))
+        ref_idx = orc.draw_samples(sk.L, op)
+        draws_ok += int(np.array_equal(idx[q], ref_idx))
+        x = X[v].double().cpu().numpy()
+        r = orc.transform_gathered(a64, x, op, ref_idx, sk.gather(ref_idx).astype(np.float64))
+        g_sup = sup[v, :counts[v]].tolist()
+        g_val = vals[v, :counts[v]].astype(np.float64)
+        ri = dict(zip(r.support.tolist(), r.values))
+        for i, gv in zip(g_sup, g_val):
+            if i in ri:
+                max_rel = max(max_rel, abs(gv - ri[i]) / max(abs(ri[i]), 1e-300))
+        if g_sup == r.support.tolist():
+            exact += 1
+            continue
+        if strict:
+            failures.append(v)
+            continue
+        ax = a64 @ x
+        cut = np.sort(np.abs(r.mu))[::-1][want - 1] if want <= sk.m else 0.0
+        ok = all(abs(abs(ax[i]) - eps_val) <= 1e-6 or abs(abs(r.mu[i]) - cut) <= 1e-5 * max(1.0, cut)
+                 for i in set(g_sup) ^ set(r.support.tolist()))
+        allowed += int(ok)
+        if not ok:
+            failures.append(v)
+    tol = 1e-12 if strict else 1e-5
+    ok = draws_ok == len(ids) and not failures and max_rel <= tol
+    return {"status": "ok" if ok else "FAIL", "vectors_checked": len(ids), "vector_ids": ids,
+            "draws_bit_exact": draws_ok, "support_identical": exact, "support_diff_allowed": allowed,
+            "failures": failures, "max_value_rel_err": max_rel, "value_tol": tol,
+            "oracle": "oracle.transform_gathered (fp64 restatement of stream.hpp:197-268) on the GPU's gathered "
+                      "columns; inputs = the GPU's exact A and x"}
 
 
 # ------------------------------------------------------------- clocks ----
@@ -136,7 +227,7 @@ class ClockSampler:
 
 # -------------------------------------------------------- CPU baseline ----
 def cpu_sample(a64: np.ndarray, X64: np.ndarray, seeds: np.ndarray, J: int, K: int, threads: int,
-               target_s: float, predrawn: bool = False):
+               target_s: float, predrawn: bool = False, s_val: int = S, eps_val: float = EPS):
     """The reference algorithm (oracle restatement) on host cores over a pool of prepared vectors.
 
     The fp64 sketch at n=4096 needs 275 GB of host RAM (the box has ~196 GB), so
@@ -152,11 +243,11 @@ def cpu_sample(a64: np.ndarray, X64: np.ndarray, seeds: np.ndarray, J: int, K: i
     N = J * K
     gathered = np.empty((P, N, m), dtype=np.float64)
     for v in range(P):
-        p = orc.StreamParams(epsilon=EPS, s=S, J=J, K=K, widen=WIDEN, seed=int(seeds[v]))
+        p = orc.StreamParams(epsilon=eps_val, s=s_val, J=J, K=K, widen=WIDEN, seed=int(seeds[v]))
         idx = orc.draw_samples(L, p)
         S_ = orc.design_columns(k, n, idx)          # (N, n)
         gathered[v] = S_ @ a64.T                    # column ell = A s_ell
-    p = orc.StreamParams(epsilon=EPS, s=S, J=J, K=K, widen=WIDEN)
+    p = orc.StreamParams(epsilon=eps_val, s=s_val, J=J, K=K, widen=WIDEN)
     _, t_pool = orc.bench_gathered(a64, X64, p, seeds, gathered, L, threads, P, predrawn)
     total = max(P, int(P * max(1.0, target_s / max(t_pool, 1e-3))))
     counts, secs = orc.bench_gathered(a64, X64, p, seeds, gathered, L, threads, total, predrawn)
@@ -179,13 +270,37 @@ WORKLOADS = {
 }
 
 
-def make_problem(cfg, A64, B, first, dev):
+def make_problem(cfg, A64, B, first, dev, targets=None):
     from paper_2105_05879_b200 import generators
     if cfg is WORKLOADS["1"]:
-        return generators.config1_problem(B=B, seed=X_SEED, device=dev, a_seed=cfg["a_seed"])
+        return generators.config1_problem(B=B, seed=X_SEED, device=dev, a_seed=cfg["a_seed"], A64=A64,
+                                          targets=targets)
     if cfg is WORKLOADS["2"]:
-        return generators.config2_problem(B=B, seed=X_SEED, device=dev, a_seed=cfg["a_seed"], first=first)
-    return generators.config3_problem(B=B, seed=X_SEED, device=dev, first=first, A64=A64)
+        return generators.config2_problem(B=B, seed=X_SEED, device=dev, a_seed=cfg["a_seed"], first=first, A64=A64,
+                                          targets=targets)
+    return generators.config3_problem(B=B, seed=X_SEED, device=dev, first=first, A64=A64, targets=targets)
+
+
+def build_matrix(cfg, dev, gaussian_fill=None):
+    """A in fp64 on `dev`: the SeededRng Gaussian fill (library or oracle, bit-identical), then QR
+    (Haar) or 1/sqrt(n) scaling (iid); both arms call this, so they get the same A bits."""
+    from paper_2105_05879_b200 import generators
+    n = cfg["n"]
+    if cfg["a"] == "haar":
+        return generators.haar_orthogonal(n, cfg["a_seed"], dev, gaussian_fill=gaussian_fill)
+    return generators.iid_gaussian(n, cfg["a_seed"], dev, gaussian_fill=gaussian_fill)
+
+
+def batch_size(args, cfg):
+    return args.batch if args.config == "3" else cfg["B"]
+
+
+def workload_config(args, cfg, world):
+    """The `config` object both arms print (identical keys and values)."""
+    return {"workload": cfg["desc"], "vectors_per_gpu_per_step": batch_size(args, cfg), "J": args.J, "K": args.K,
+            "widen": WIDEN, "parallelism": f"vector-sharded x{world}, sketch replicated per GPU",
+            "l2": ("inputs larger than L2 (137.5 GB sketch; 1 GiB of x per step)" if args.config == "3"
+                   else "small config: sketch may be L2-resident")}
 
 
 def run_b200(args):
@@ -208,14 +323,17 @@ def run_b200(args):
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device(dev))
+        dist.barrier()
+        nccl = ".".join(map(str, torch.cuda.nccl.version())) if not one_dev else "-"
+        print(f"[bench] rank {rank}/{world} on {dev}: {dist.get_backend()} process group up "
+              f"(NCCL {nccl}), group size {dist.get_world_size()}", file=sys.stderr, flush=True)
 
     cfg = WORKLOADS[args.config]
     n_dim = cfg["n"]
     es = 8 if cfg["dtype"] == "fp64" else 4
     # ---- A: built on rank 0, broadcast over NCCL ----
     if rank == 0:
-        A64 = (generators.haar_orthogonal(n_dim, cfg["a_seed"], dev) if cfg["a"] == "haar"
-               else generators.iid_gaussian(n_dim, cfg["a_seed"], dev))
+        A64 = build_matrix(cfg, dev)
     else:
         A64 = torch.empty((n_dim, n_dim), dtype=torch.float64, device=dev)
     if world > 1:
@@ -246,7 +364,7 @@ def run_b200(args):
     sketch_bytes = sk.L * sk.m * es
 
     # ---- this rank's shard of the vector stream ----
-    B = args.batch if args.config == "3" else cfg["B"]
+    B = batch_size(args, cfg)
     first, _ = parallel.vector_shard(rank, world, B)
     prob = make_problem(cfg, A64, B, first, dev)
     X = prob.X
@@ -311,19 +429,21 @@ def run_b200(args):
 
     # ---- roofline of the dominant kernel (the fused stream kernel) ----
     peak, peak_kind = peaks()
-    bvec = bytes_per_vector(N, sk.m, sk.n, want, es)
+    bvec = bytes_per_vector(N, sk.m, sk.n, want, es)         # SURVEY.md §8(d) count (A rows included)
+    dvec = dram_bytes_per_vector(N, sk.m, sk.n, es)          # DRAM-resident algorithmic bytes
     per_launch_ms = stream_ms / max(1, stream_launches)
     vec_per_launch = B * args.steps / max(1, stream_launches)
-    achieved = bvec * vec_per_launch / (per_launch_ms / 1e3) / 1e9
+    achieved = dvec * vec_per_launch / (per_launch_ms / 1e3) / 1e9
+    achieved_8d = bvec * vec_per_launch / (per_launch_ms / 1e3) / 1e9
     pre_achieved = sketch_bytes / (fwht_ms + ident_ms) / 1e6 if (fwht_ms + ident_ms) > 0 else None
 
     # DRAM bytes per launch of the stream kernel from the committed ncu --set full capture
-    # (dram__bytes_read.sum + dram__bytes_write.sum = 845.77 GB + 3.19 GB for one config-3
-    # launch of 65,536 vectors), scaled to this run's vectors per launch
+    # (dram__bytes_read.sum + dram__bytes_write.sum of one config-3 launch of 65,536 vectors),
+    # scaled to this run's vectors per launch
     traffic, traffic_src = None, None
     if args.config == "3":
-        traffic = (845.770680e9 + 3.188722e9) / 65536 * vec_per_launch
-        traffic_src = "profiles/r01_ncu_stream_kernel.txt (ncu --set full, 65,536-vector launch, scaled per vector)"
+        traffic = NCU_STREAM_DRAM_BYTES_65536 / 65536 * vec_per_launch
+        traffic_src = NCU_STREAM_SOURCE
 
     # ---- end to end through the public API with host buffers ----
     e2e = None
@@ -348,11 +468,20 @@ def run_b200(args):
                "d2h_bytes_per_step": int(B * 4 + B * want * (4 + es))}
         assert np.array_equal(oh.counts.numpy(), counts), "host-buffer path disagrees with device path"
 
+    # ---- parity of the timed batch's outputs against the oracle (after timing) ----
+    parity = None
+    if not args.no_parity:
+        strict = es == 8
+        parity = parity_check(fst, sk, prob.A, X, prob.seeds, out, args.J, args.K, s_val, eps_val, strict)
+        print(f"[bench] rank {rank}: parity {parity['status']} ({parity['vectors_checked']} vectors of the timed "
+              f"batch vs the oracle, support identical {parity['support_identical']}, "
+              f"max value rel err {parity['max_value_rel_err']:.2e})", file=sys.stderr, flush=True)
+
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and args.config == "3":
         P = 32
-        a64 = A64.cpu().numpy()
+        a64 = prob.A.double().cpu().numpy()          # exactly the A the GPU computes on
         X64 = X[:P].double().cpu().numpy()
         threads = os.cpu_count() or 1
         r = cpu_sample(a64, X64, prob.seeds[:P], args.J, args.K, threads, args.cpu_seconds)
@@ -397,12 +526,8 @@ def run_b200(args):
         "vs_baseline": None,
         "dtype": cfg["dtype"],
         "data": cfg["data"],
-        "config": {"workload": cfg["desc"],
-                   "vectors_per_gpu_per_step": B, "J": args.J, "K": args.K, "widen": WIDEN,
-                   "parallelism": f"vector-sharded x{world}, sketch replicated per GPU",
-                   "l2": ("inputs larger than L2 (137.5 GB sketch; 1 GiB of x per step)" if args.config == "3"
-                          else "small config: sketch may be L2-resident"),
-                   "mean_support": float(np.mean(counts))},
+        "config": workload_config(args, cfg, world),
+        "mean_support": float(np.mean(counts)),
         "preprocess": {"ms": pre_ms, "fwht_ms": fwht_ms, "identity_ms": ident_ms, "allgather_ms": gather_ms,
                        "replicate": args.replicate,
                        "sketch_bytes": sketch_bytes,
@@ -411,7 +536,15 @@ def run_b200(args):
                                     "peak_source": peak_kind}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": traffic, "traffic_source": traffic_src, "kernel": "stream_kernel",
-                     "bytes_per_vector": bvec, "per_launch_ms": per_launch_ms, "peak_source": peak_kind,
+                     "bytes_per_vector": dvec,
+                     "bytes_model": (f"DRAM-resident algorithmic bytes {es}*(N*m + n) per vector (N sampled "
+                                     "columns + x); the want gathered rows of A are L2 hits (A is L2-resident, "
+                                     "evict_last) and are excluded, as SURVEY.md §8(d) excludes the L2-resident "
+                                     "sign tables"),
+                     "traffic_over_algorithmic": (traffic / (dvec * vec_per_launch)) if traffic else None,
+                     "survey_8d": {"bytes_per_vector": bvec, "achieved": achieved_8d, "frac": achieved_8d / peak,
+                                   "note": "es*(N*m + want*n + n): counts the L2-served A rows as DRAM bytes"},
+                     "per_launch_ms": per_launch_ms, "peak_source": peak_kind,
                      "per_launch_source": ("library CUDA events over the timed region" if profile_in_timed else
                                            "library CUDA events over a second, untimed pass of the same K steps")},
         "kernels_ms": {"stream": stream_ms, "draw": draw_ms, "stream_launches": stream_launches,
@@ -420,6 +553,7 @@ def run_b200(args):
         "clocks": clk.summary(),
         "e2e": e2e,
         "cpu_baseline": cpu,
+        "parity": parity,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -653,53 +787,85 @@ def run_config4(args):
 
 # ------------------------------------------------------- reference arm ----
 def run_reference(args):
-    """Reference algorithm on the host cores (rank 0 only), same metric/config."""
+    """Reference arm: the reference algorithm on the host cores (rank 0 only; other ranks exit 0),
+    on the b200 arm's config and EXACT inputs. A is built by the same routine (the oracle's
+    SeededRng Gaussian fill, bit-identical to the library's, then the same QR on the same device)
+    and the vectors by the same generator (the oracle's restatement of the library's target
+    generator, bit-identical) and the same first 8192-vector chunk of x = A^T y; the reference
+    then computes in fp64 on the fp32 inputs the GPU sees (configs 2 / 3) or on the fp64 inputs
+    (config 1). The product library is not loaded in this process."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
+        print(f"[bench] reference arm: rank {rank}/{world} idle (rank 0 times the host reference)",
+              file=sys.stderr, flush=True)
         return
+    import torch
     from oracle import oracle as orc
     orc.build()
+    cfg = WORKLOADS[args.config]
     threads = os.cpu_count() or 1
-    n = N_DIM
-    g = orc.rng_gaussian(A_SEED, n * n).reshape(n, n)
-    q, r = np.linalg.qr(g)
-    a64 = q * np.sign(np.diag(r))
-    P = 32
-    t = np.uint64(X_SEED) ^ np.arange(P, dtype=np.uint64)
-    gen = [orc.mix_seed(int(v) ^ 0x67656E) for v in t]
-    seeds = np.array([orc.mix_seed(int(v) ^ 0x747278) for v in t], dtype=np.uint64)
-    X = np.zeros((P, n))
-    for v in range(P):
-        x, truth = orc.gen_exact_sparse(a64, S, gen[v])
-        y = truth + 1e-3 * np.random.default_rng(int(gen[v])).standard_normal(n)
-        x = a64.T @ y
-        X[v] = x / np.linalg.norm(x)
+    dev = "cuda:0" if torch.cuda.is_available() else "cpu"
+    A64 = build_matrix(cfg, dev, gaussian_fill=orc.rng_gaussian)
+    B_ref = min(batch_size(args, cfg), 8192)        # the b200 arm's first x chunk: same GEMM shape, same bits
+    prob = make_problem(cfg, A64, B_ref, 0, dev, targets=orc.gen_sparse_targets)
+    P = min(32, B_ref)
+    a64 = prob.A.double().cpu().numpy()
+    X = prob.X[:P].double().cpu().numpy()
+    seeds = prob.seeds[:P]
+    del prob, A64
+    s_val = cfg["s"]
     vals, secs_all = [], []
     for i in range(args.warmup + args.steps):
-        rr = cpu_sample(a64, X, seeds, args.J, args.K, threads, args.cpu_seconds / 2)
+        rr = cpu_sample(a64, X, seeds, args.J, args.K, threads, args.cpu_seconds / 2, s_val=s_val,
+                        eps_val=cfg["eps"])
         if i >= args.warmup:
             vals.append(rr["vectors"])
             secs_all.append(rr["seconds"])
     value = sum(vals) / sum(secs_all)
     line = {
         "impl": "reference",
-        "metric": METRIC, "value": value, "unit": "vectors/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "metric": METRIC if args.config == "3" else f"thresholded-Ax vectors/sec ({cfg['desc'].split(':')[0]})",
+        "value": value, "unit": "vectors/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs_all) / len(secs_all),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp64",
-        "data": "synthetic (same generator recipe as the b200 arm, host numpy QR)",
-        "config": {"workload": "config3: n=m=4096, s=32, eps=0.1, J=375, K=2, widen=10 (N=750, want=320)",
-                   "J": args.J, "K": args.K, "widen": WIDEN},
+        "data": cfg["data"] + "; the b200 arm's exact A and x (fp32 values widened to fp64 for configs 2/3)",
+        "config": workload_config(args, cfg, world),
         "cpu_baseline": {"value": value, "unit": "vectors/s", "cores": threads, "kind": "port",
-                         "sample": f"per step ~{int(np.mean(vals))} vectors cycling 32 prepared vectors on "
-                                   f"{threads} threads; reference transform() restated in C++ (oracle/; the "
+                         "sample": f"per step ~{int(np.mean(vals))} vectors cycling the b200 arm's first {P} vectors "
+                                   f"on {threads} threads; reference transform() restated in C++ (oracle/; the "
                                    f"reference needs Eigen, absent), sampled columns pre-materialised in DRAM"},
         "e2e": {"value": value, "unit": "vectors/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+def relaunch_under_torchrun(args) -> bool:
+    """`bench.py --gpus N` (N > 1) started directly: re-run this command as N ranks (one process
+    per GPU) under torch.distributed.run on 127.0.0.1, exactly as the driver launches it. Returns
+    True when this process was the launcher (it has already waited for the ranks)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd[1:])}", file=sys.stderr, flush=True)
+    rc = subprocess.call(cmd)
+    if rc != 0:
+        sys.exit(rc)
+    return True
+
+
 def main():
     args = parse()
+    if relaunch_under_torchrun(args):
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        print(f"[bench] note: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
     elif args.config == "5":

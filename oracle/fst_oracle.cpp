@@ -522,7 +522,8 @@ template TransformResult<float> transform_with_samples<float>(const Sketch<float
 
 template <typename T>
 TransformResult<T> transform_gathered(const T* a, std::int64_t m, std::int64_t n, const T* x, const StreamParams& p,
-                                      const std::vector<std::int64_t>& indices, const T* gathered) {
+                                      const std::vector<std::int64_t>& indices, const T* gathered,
+                                      const std::vector<std::vector<std::uint64_t>>* kerdock_set) {
   // Same steps as transform_with_samples; sk.column(ell) replaced by the
   // gathered copy (stream.hpp:235-236).
   p.validate();
@@ -546,9 +547,13 @@ TransformResult<T> transform_gathered(const T* a, std::int64_t m, std::int64_t n
         t = pos < n ? sqrt_d * x[pos] : T(0);
       } else {
         const std::int64_t s = ell / design.d;
-        if (s != cached_s) {
-          const auto mat = kerdock_matrix(design, static_cast<std::uint64_t>(s));
-          reversed_q_rows(mat.data(), design.k, rev);
+        if (s != cached_s) {  // the reference reads sk.kerdock_set() (built once, sketch.hpp:130)
+          if (kerdock_set != nullptr) {
+            reversed_q_rows((*kerdock_set)[static_cast<std::size_t>(s)].data(), design.k, rev);
+          } else {
+            const auto mat = kerdock_matrix(design, static_cast<std::uint64_t>(s));
+            reversed_q_rows(mat.data(), design.k, rev);
+          }
           cached_s = s;
         }
         t = kerdock_inner_product(x, n, design.d, rev, static_cast<std::uint64_t>(ell % design.d));
@@ -584,10 +589,11 @@ TransformResult<T> transform_gathered(const T* a, std::int64_t m, std::int64_t n
 }
 template TransformResult<double> transform_gathered<double>(const double*, std::int64_t, std::int64_t, const double*,
                                                             const StreamParams&, const std::vector<std::int64_t>&,
-                                                            const double*);
+                                                            const double*,
+                                                            const std::vector<std::vector<std::uint64_t>>*);
 template TransformResult<float> transform_gathered<float>(const float*, std::int64_t, std::int64_t, const float*,
                                                           const StreamParams&, const std::vector<std::int64_t>&,
-                                                          const float*);
+                                                          const float*, const std::vector<std::vector<std::uint64_t>>*);
 
 // ----------------------------------------------------------- generators ----
 

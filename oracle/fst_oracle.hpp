@@ -175,9 +175,12 @@ TransformResult<T> transform_with_samples(const Sketch<T>& sk, const T* x, const
 /// drawn.use_gathered): identical arithmetic, columns supplied by the caller
 /// (gathered: N x m, row j = column ell_j). Used to check full-size (n=4096)
 /// GPU runs without materialising the 275 GB fp64 sketch.
+/// kerdock_set: the Kerdock matrices of every basis, built once as the reference's
+/// Sketch constructor does (sketch.hpp:130); nullptr rebuilds them per basis change.
 template <typename T>
 TransformResult<T> transform_gathered(const T* a, std::int64_t m, std::int64_t n, const T* x, const StreamParams& p,
-                                      const std::vector<std::int64_t>& indices, const T* gathered);
+                                      const std::vector<std::int64_t>& indices, const T* gathered,
+                                      const std::vector<std::vector<std::uint64_t>>* kerdock_set = nullptr);
 
 // ----------------------------------------------- kerdock.hpp:198-317 verifiers --
 

@@ -257,6 +257,18 @@ def rng_gaussian(seed: int, count: int) -> np.ndarray:
     return out
 
 
+def gen_sparse_targets(seeds, m: int, s: int, value_kind: int = 0, noise_sigma: float = 0.0,
+                       threads: int = 0) -> np.ndarray:
+    """(B, m) sparse targets, one SeededRng stream per vector (generators.hpp:44-53 draw order,
+    +-1/sqrt(s) or N(0,1) values, optional dense N(0, noise_sigma^2) noise)."""
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    Y = np.zeros((len(seeds), m), dtype=np.float64)
+    _check(lib().orc_gen_sparse_targets(_ptr(seeds), C.c_int64(len(seeds)), C.c_int64(m), C.c_int64(s),
+                                        C.c_int(value_kind), C.c_double(noise_sigma),
+                                        C.c_int(threads or (os.cpu_count() or 1)), _ptr(Y)))
+    return Y
+
+
 def rng_unit_double(seed: int, count: int) -> np.ndarray:
     out = np.zeros(count, dtype=np.float64)
     lib().orc_rng_unit_double(C.c_uint64(seed), C.c_int64(count), _ptr(out))

@@ -188,6 +188,46 @@ int orc_rng_gaussian(std::uint64_t seed, std::int64_t count, double* out) {
   for (std::int64_t i = 0; i < count; ++i) out[i] = r.gaussian();
   return 0;
 }
+// B sparse target vectors y (B x m, row-major) for the BASELINE configs: vector v
+// draws from SeededRng(seeds[v]) the s distinct rows of gen_exact_sparse
+// (generators.hpp:44-53: partial Fisher-Yates with index(m - i)), each value
+// +-1/sqrt(s) by coin (value_kind 0) or gaussian() (value_kind 1), then, if
+// noise_sigma > 0, noise_sigma * gaussian() added to every row in order (the
+// configs' dense-noise extension; the reference has no noise generator).
+// Threads over vectors; each vector's stream is independent of the split.
+int orc_gen_sparse_targets(const std::uint64_t* seeds, std::int64_t B, std::int64_t m, std::int64_t s,
+                           int value_kind, double noise_sigma, int threads, double* Y) {
+  return guarded([&] {
+    if (B < 0 || m < 1 || s < 1 || s > m || value_kind < 0 || value_kind > 1)
+      throw std::invalid_argument("gen_sparse_targets: bad arguments");
+    const double mag = 1.0 / std::sqrt(static_cast<double>(s));
+    auto work = [&](std::int64_t first, std::int64_t last) {
+      std::vector<std::int64_t> perm(static_cast<std::size_t>(m));
+      for (std::int64_t v = first; v < last; ++v) {
+        SeededRng rng(seeds[v]);
+        double* y = Y + v * m;
+        std::fill(y, y + m, 0.0);
+        std::iota(perm.begin(), perm.end(), std::int64_t{0});
+        for (std::int64_t i = 0; i < s; ++i) {
+          const auto j = i + static_cast<std::int64_t>(rng.index(static_cast<std::uint64_t>(m - i)));
+          std::swap(perm[i], perm[j]);
+          y[perm[i]] = value_kind == 0 ? (rng.coin() ? mag : -mag) : rng.gaussian();
+        }
+        if (noise_sigma > 0)
+          for (std::int64_t i = 0; i < m; ++i) y[i] += noise_sigma * rng.gaussian();
+      }
+    };
+    threads = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(threads, B)));
+    std::vector<std::thread> pool;
+    const std::int64_t per = (B + threads - 1) / threads;
+    for (int t = 0; t < threads; ++t) {
+      const std::int64_t f = t * per, l = std::min(B, f + per);
+      if (f < l) pool.emplace_back([&work, f, l] { work(f, l); });
+    }
+    for (auto& th : pool) th.join();
+  });
+}
+
 int orc_rng_unit_double(std::uint64_t seed, std::int64_t count, double* out) {
   SeededRng r(seed);
   for (std::int64_t i = 0; i < count; ++i) out[i] = r.unit_double();
@@ -362,6 +402,239 @@ int orc_kerdock_block(const void* a, int dtype, std::int64_t m, std::int64_t n, 
   });
 }
 
+// s_ell for each requested index (count x n, row j = s_{ell_j}), kerdock.hpp:156-167.
+int orc_design_columns(int k, std::int64_t n, const std::int64_t* ells, std::int64_t count, double* out) {
+  return guarded([&] {
+    const DesignParams p = DesignParams::make(k);
+    if (n < 1 || n > p.d) throw std::invalid_argument("design_columns: n out of [1,d]");
+    const double sqrt_d = std::sqrt(static_cast<double>(p.d));
+    std::vector<std::uint8_t> qbits;
+    std::int64_t cached = -1;
+    for (std::int64_t j = 0; j < count; ++j) {
+      const DecodedIndex idx = decode_index(p, ells[j]);
+      double* v = out + j * n;
+      if (idx.identity) {
+        std::fill(v, v + n, 0.0);
+        if (static_cast<std::int64_t>(idx.wpos) < n) v[idx.wpos] = sqrt_d;
+        continue;
+      }
+      if (static_cast<std::int64_t>(idx.s) != cached) {
+        const auto m = kerdock_matrix(p, idx.s);
+        qbits.assign(static_cast<std::size_t>(n), 0);
+        for (std::int64_t q = 0; q < n; ++q)
+          qbits[q] = static_cast<std::uint8_t>(
+              quadratic_form(m.data(), p.k, coords_of_position(static_cast<std::uint64_t>(q), p.k)));
+        cached = static_cast<std::int64_t>(idx.s);
+      }
+      for (std::int64_t q = 0; q < n; ++q)
+        v[q] = (qbits[q] ^ (__builtin_popcountll(idx.wpos & static_cast<std::uint64_t>(q)) & 1)) ? -1.0 : 1.0;
+    }
+  });
+}
+
+// CPU baseline over a pool of P prepared vectors (gathered columns in host
+// DRAM, P x N x m): `threads` threads process `total` vectors, vector t taking
+// pool entry t % P; each runs draw_samples + transform_with_samples (the
+// reference's transform(), stream.hpp:272-275) with its columns read from the
+// gathered buffer. Returns wall seconds and the support sizes of the pool.
+int orc_bench_gathered(const double* a, std::int64_t m, std::int64_t n, const double* X, std::int64_t P,
+                       double eps, double delta, std::int64_t s, std::int64_t J, std::int64_t K, std::int64_t widen,
+                       const std::uint64_t* seeds, const double* gathered, std::int64_t L, int threads,
+                       std::int64_t total, std::int64_t* counts_out, double* seconds, int predrawn) {
+  return guarded([&] {
+    const std::int64_t N = J * K;
+    // predrawn: the paper's timing convention (experiment.hpp:178-181) - draws done before the clock
+    std::vector<std::vector<std::int64_t>> drawn;
+    if (predrawn)
+      for (std::int64_t v = 0; v < P; ++v) drawn.push_back(draw_samples(L, make_params(eps, delta, s, J, K, widen, seeds[v])));
+    // the Kerdock set is built once, outside the clock, as the reference's Sketch constructor does
+    // (sketch.hpp:130); transform() only derives the reversed rows per basis change (stream.hpp:222-226)
+    const DesignParams design = DesignParams::make(even_log2_ceil(n));
+    std::vector<std::vector<std::uint64_t>> kset(static_cast<std::size_t>(design.kerdock_bases()));
+    for (std::int64_t s = 0; s < design.kerdock_bases(); ++s)
+      kset[static_cast<std::size_t>(s)] = kerdock_matrix(design, static_cast<std::uint64_t>(s));
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    threads = std::max(1, threads);
+    std::atomic<int> failed{0};
+    for (int th = 0; th < threads; ++th) {
+      pool.emplace_back([&, th] {
+        try {
+          for (std::int64_t t = th; t < total; t += threads) {
+            const std::int64_t v = t % P;
+            StreamParams p = make_params(eps, delta, s, J, K, widen, seeds[v]);
+            const auto r = predrawn ? transform_gathered(a, m, n, X + v * n, p, drawn[v], gathered + v * N * m, &kset)
+                                    : transform_gathered(a, m, n, X + v * n, p, draw_samples(L, p),
+                                                         gathered + v * N * m, &kset);
+            if (t < P) counts_out[v] = static_cast<std::int64_t>(r.support.size());
+          }
+        } catch (...) {
+          failed = 1;
+        }
+      });
+    }
+    for (auto& t : pool) t.join();
+    if (failed) throw std::runtime_error("bench_gathered: worker failed");
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  });
+}
+
+// ---- FSTK save/load (sketch.hpp:213-302), fp64 reference format ----
+// status: 7 IoError, 8 MagicMismatch, 9 VersionUnsupported, 10 TruncatedPayload, 11 MalformedHeader
+static void put_le(std::FILE* f, std::uint64_t v, int bytes) {
+  unsigned char b[8];
+  for (int i = 0; i < bytes; ++i) b[i] = static_cast<unsigned char>(v >> (8 * i));
+  std::fwrite(b, 1, bytes, f);
+}
+
+int orc_save(void* hv, const char* path, int with_a) {
+  auto* h = static_cast<OrcSketch*>(hv);
+  if (h->dtype != 1) { g_err = "oracle save: fp64 sketches only"; return 1; }
+  std::FILE* f = std::fopen(path, "wb");
+  if (!f) { g_err = std::string("cannot open for writing: ") + path; return 7; }
+  const auto& sk = h->d;
+  std::fwrite("FSTK", 1, 4, f);
+  put_le(f, 1, 4);
+  put_le(f, sk.m, 8); put_le(f, sk.n, 8); put_le(f, sk.design.k, 8); put_le(f, sk.design.d, 8); put_le(f, sk.design.L, 8);
+  const unsigned char flag = with_a ? 1 : 0;
+  std::fwrite(&flag, 1, 1, f);
+  std::fwrite(sk.columns.data(), 8, sk.columns.size(), f);
+  if (with_a) std::fwrite(sk.a.data(), 8, sk.a.size(), f);
+  const bool ok = std::fclose(f) == 0;
+  if (!ok) { g_err = std::string("write failed: ") + path; return 7; }
+  return 0;
+}
+
+int orc_load(const char* path, void** out) {
+  std::FILE* f = std::fopen(path, "rb");
+  if (!f) { g_err = std::string("cannot open for reading: ") + path; return 7; }
+  std::fseek(f, 0, SEEK_END);
+  const std::uint64_t fsize = static_cast<std::uint64_t>(std::ftell(f));
+  std::fseek(f, 0, SEEK_SET);
+  auto fail = [&](int code, const std::string& msg) { std::fclose(f); g_err = msg; return code; };
+  if (fsize < 49) return fail(10, std::string("sketch file shorter than its header: ") + path);
+  unsigned char hd[49];
+  if (std::fread(hd, 1, 49, f) != 49) return fail(10, "short header");
+  auto get = [&](int off, int bytes) { std::uint64_t v = 0; for (int i = 0; i < bytes; ++i) v |= std::uint64_t(hd[off + i]) << (8 * i); return v; };
+  if (std::memcmp(hd, "FSTK", 4) != 0) return fail(8, std::string("not an FSTK sketch file: ") + path);
+  const std::uint64_t version = get(4, 4);
+  if (version != 1) return fail(9, "unsupported FSTK version " + std::to_string(version));
+  const std::uint64_t m = get(8, 8), n = get(16, 8), k = get(24, 8), d = get(32, 8), L = get(40, 8);
+  const int flag = hd[48];
+  if (m == 0 || n == 0 || k < 2 || k > 16 || k % 2 != 0 || d != (std::uint64_t{1} << k) || L != d * (d / 2 + 1) || n > d ||
+      (flag != 0 && flag != 1))
+    return fail(11, std::string("inconsistent FSTK header fields: ") + path);
+  const std::uint64_t expected = 49 + 8 * m * L + (flag ? 8 * m * n : 0);
+  if (fsize < expected) return fail(10, std::string("FSTK payload truncated: ") + path);
+  if (fsize > expected) return fail(11, "FSTK file larger than its header declares");
+  auto* h = new OrcSketch();
+  h->dtype = 1;
+  h->d.design = DesignParams::make(static_cast<int>(k));
+  h->d.m = static_cast<std::int64_t>(m);
+  h->d.n = static_cast<std::int64_t>(n);
+  h->d.columns.resize(m * L);
+  bool ok = std::fread(h->d.columns.data(), 8, m * L, f) == m * L;
+  if (flag) {
+    h->d.a.resize(m * n);
+    ok = ok && std::fread(h->d.a.data(), 8, m * n, f) == m * n;
+  }
+  std::fclose(f);
+  if (!ok) {
+    delete h;
+    g_err = std::string("FSTK payload truncated: ") + path;
+    return 10;
+  }
+  for (std::int64_t s = 0; s < h->d.design.kerdock_bases(); ++s) h->d.kerdock.push_back(kerdock_matrix(h->d.design, s));
+  double rn = 0;
+  for (std::uint64_t i = 0; i < (flag ? m : 0); ++i) {
+    double acc = 0;
+    for (std::uint64_t j = 0; j < n; ++j) acc += h->d.a[i * n + j] * h->d.a[i * n + j];
+    rn = std::max(rn, std::sqrt(acc));
+  }
+  h->d.row_norm_max = rn;
+  *out = h;
+  return 0;
+}
+
+// generators.hpp:60-85 gen_mixture: returns x (n) and truth (m), both / |x|.
+int orc_gen_mixture(const double* a, std::int64_t m, std::int64_t n, double p, std::uint64_t seed, double* x_out,
+                    double* truth_out) {
+  return guarded([&] {
+    if (!(p > 0) || p > 1) throw std::invalid_argument("gen_mixture: need 0 < p <= 1");
+    std::vector<double> truth(static_cast<std::size_t>(m));
+    for (std::uint64_t attempt = 0;; ++attempt) {
+      SeededRng rng(mix_seed(seed) ^ (attempt * 0x9e3779b97f4a7c15ull));
+      bool any = false;
+      for (std::int64_t i = 0; i < m; ++i) {
+        if (rng.unit_double() <= p) {
+          truth[i] = rng.gaussian();
+          any = true;
+        } else {
+          truth[i] = 0.0;
+        }
+      }
+      if (any) break;
+    }
+    double nrm = 0;
+    for (std::int64_t j = 0; j < n; ++j) {
+      double acc = 0;
+      for (std::int64_t i = 0; i < m; ++i) acc += a[i * n + j] * truth[i];
+      x_out[j] = acc;
+      nrm += acc * acc;
+    }
+    nrm = std::sqrt(nrm);
+    for (std::int64_t j = 0; j < n; ++j) x_out[j] /= nrm;
+    for (std::int64_t i = 0; i < m; ++i) truth_out[i] = truth[i] / nrm;
+  });
+}
+
+// ---- generators ----
+int orc_gen_orthogonal(std::int64_t n, std::uint64_t seed, double* out) {
+  return guarded([&] {
+    const auto v = gen_orthogonal(n, seed);
+    std::memcpy(out, v.data(), sizeof(double) * v.size());
+  });
+}
+int orc_gen_exact_sparse(const double* a, std::int64_t m, std::int64_t n, std::int64_t s, std::uint64_t seed,
+                         double* x_out, double* truth_out) {
+  return guarded([&] {
+    const auto t = gen_exact_sparse(a, m, n, s, seed, x_out);
+    std::memcpy(truth_out, t.data(), sizeof(double) * t.size());
+  });
+}
+
+// ---- design verifiers (kerdock.hpp:198-317, cli.hpp:45-60) ----
+int orc_materialize_design(int k, double* out) {
+  return guarded([&] {
+    const auto u = materialize_design(DesignParams::make(k));
+    std::memcpy(out, u.data(), sizeof(double) * u.size());
+  });
+}
+int orc_verify_mub(int k, int cap, double* out4, int* exhaustive) {
+  return guarded([&] {
+    const MubReport r = verify_mub(DesignParams::make(k), cap);
+    out4[0] = r.max_within_gram_dev;
+    out4[1] = r.min_cross_sq;
+    out4[2] = r.max_cross_sq;
+    out4[3] = r.max_cross_dev;
+    *exhaustive = r.exhaustive ? 1 : 0;
+  });
+}
+int orc_verify_design_moments(int k, int cap, double* out2, int* exact) {
+  return guarded([&] {
+    const MomentReport r = verify_design_moments(DesignParams::make(k), cap);
+    out2[0] = r.m1;
+    out2[1] = r.m2;
+    *exact = r.exact ? 1 : 0;
+  });
+}
+int orc_design_moments_of(const double* u, std::int64_t d, std::int64_t L, double* out2) {
+  return guarded([&] {
+    const MomentReport r = design_moments_of(u, d, L);
+    out2[0] = r.m1;
+    out2[1] = r.m2;
+  });
+}
 double orc_design_moment_target(std::int64_t d, int k) { return design_moment_target(d, k); }
 int orc_verify_kerdock_set(int k, int* skew, std::int64_t* bad_pairs) {
   return guarded([&] {

@@ -60,19 +60,21 @@ def sparse_targets(gen_seeds: np.ndarray, m: int, s: int, value_kind: int = 0, n
     return Y
 
 
-def haar_orthogonal(n: int, seed: int, device="cuda:0"):
-    """generators.hpp:20-33 on the GPU (fp64): QR of the SeededRng Gaussian fill, diag(R) > 0."""
+def haar_orthogonal(n: int, seed: int, device="cuda:0", gaussian_fill=None):
+    """generators.hpp:20-33 on the GPU (fp64): QR of the SeededRng Gaussian fill, diag(R) > 0.
+    gaussian_fill(seed, count) replaces the library's fill (bench.py's reference arm passes the
+    oracle's bit-identical SeededRng so that it does not load the product library)."""
     import torch
-    g = torch.from_numpy(gaussian(seed, n * n).reshape(n, n)).to(device)
+    g = torch.from_numpy((gaussian_fill or gaussian)(seed, n * n).reshape(n, n)).to(device)
     q, r = torch.linalg.qr(g)
     sign = torch.sign(torch.diagonal(r))
     sign[sign == 0] = 1
     return q * sign.unsqueeze(0)
 
 
-def iid_gaussian(n: int, seed: int, device="cuda:0"):
+def iid_gaussian(n: int, seed: int, device="cuda:0", gaussian_fill=None):
     import torch
-    return torch.from_numpy(gaussian(seed, n * n).reshape(n, n)).to(device) / np.sqrt(n)
+    return torch.from_numpy((gaussian_fill or gaussian)(seed, n * n).reshape(n, n)).to(device) / np.sqrt(n)
 
 
 @dataclass
@@ -106,29 +108,33 @@ def _apply(A64, Y, mode: str, normalize: bool, chunk: int = 8192):
     return torch.cat(out, 0)
 
 
-def config1_problem(B: int = 64, seed: int = 0, device="cuda:0", a_seed: int = 777) -> Problem:
+def config1_problem(B: int = 64, seed: int = 0, device="cuda:0", a_seed: int = 777, targets=None,
+                    A64=None) -> Problem:
     import torch
-    A64 = haar_orthogonal(256, a_seed, device)
+    if A64 is None:
+        A64 = haar_orthogonal(256, a_seed, device)
     g, st = trial_seeds(seed, 0, B)
-    X = _apply(A64, sparse_targets(g, 256, 8), "T", False)
+    X = _apply(A64, (targets or sparse_targets)(g, 256, 8), "T", False)
     return Problem("config1", A64, X.to(torch.float64), st, 0.1, 8, torch.float64, A64)
 
 
-def config2_problem(B: int = 4096, seed: int = 0, device="cuda:0", a_seed: int = 1024, first: int = 0) -> Problem:
+def config2_problem(B: int = 4096, seed: int = 0, device="cuda:0", a_seed: int = 1024, first: int = 0,
+                    targets=None, A64=None) -> Problem:
     import torch
-    A64 = iid_gaussian(1024, a_seed, device)
+    if A64 is None:
+        A64 = iid_gaussian(1024, a_seed, device)
     g, st = trial_seeds(seed, first, B)
-    X = _apply(A64, sparse_targets(g, 1024, 16, value_kind=1), "inv", True)
+    X = _apply(A64, (targets or sparse_targets)(g, 1024, 16, value_kind=1), "inv", True)
     return Problem("config2", A64.float().contiguous(), X.float().contiguous(), st, 0.05, 16, torch.float32, A64)
 
 
 def config3_problem(B: int = 65536, seed: int = 0, device="cuda:0", a_seed: int = 4096, first: int = 0,
-                    A64=None) -> Problem:
+                    A64=None, targets=None) -> Problem:
     import torch
     if A64 is None:
         A64 = haar_orthogonal(4096, a_seed, device)
     g, st = trial_seeds(seed, first, B)
-    X = _apply(A64, sparse_targets(g, 4096, 32, value_kind=0, noise_sigma=1e-3), "T", True)
+    X = _apply(A64, (targets or sparse_targets)(g, 4096, 32, value_kind=0, noise_sigma=1e-3), "T", True)
     return Problem("config3", A64.float().contiguous(), X.float().contiguous(), st, 0.1, 32, torch.float32, A64)
 
 

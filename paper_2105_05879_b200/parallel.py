@@ -82,17 +82,25 @@ def sketch_tensor(sk, torch_mod=None):
 
 
 def allgather_basis_shards(full, world: int, rank: int, nk: int, d: int, ldc: int, group=None) -> None:
-    """In-place all-gather of the Kerdock block of a flat sketch tensor `full`.
+    """In-place all-gather of the Kerdock block of a flat sketch tensor `full`; each rank's own
+    shard (parallel.basis_shards(nk, world)[rank]) must already be filled.
 
-    Requires equal shard sizes (nk % world == 0; true for every config with
-    world a power of two); each rank's own shard must already be filled."""
+    Equal shards (nk % world == 0, e.g. 2048 bases over 1/2/4/8 GPUs) use one
+    all_gather_into_tensor; otherwise (world = 3, 5, 6, 7 ...) every rank broadcasts its own
+    contiguous byte range in turn, in place (no padding copy of a 137 GB sketch)."""
     import torch.distributed as dist
-    if nk % world:
-        raise ValueError("allgather_basis_shards: nk must divide evenly across ranks")
-    per = (nk // world) * d * ldc
-    kerdock = full[: nk * d * ldc]
-    mine = kerdock[rank * per:(rank + 1) * per]
-    dist.all_gather_into_tensor(kerdock, mine, group=group)
+    if world == 1:
+        return
+    if nk % world == 0:
+        per = (nk // world) * d * ldc
+        kerdock = full[: nk * d * ldc]
+        mine = kerdock[rank * per:(rank + 1) * per]
+        dist.all_gather_into_tensor(kerdock, mine, group=group)
+        return
+    for src, rng in enumerate(basis_shards(nk, world)):
+        lo, hi = shard_element_range(rng, d, ldc)
+        if hi > lo:
+            dist.broadcast(full[lo:hi], src=src if group is None else dist.get_global_rank(group, src), group=group)
 
 
 def column_owner(ells: np.ndarray, shards: List[Tuple[int, int]], d: int, nk: int) -> np.ndarray:
