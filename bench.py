@@ -123,7 +123,7 @@ def parity_check(fst, sk, A, X, seeds, out, J, K, s_val, eps_val, strict, nvec=3
     values within 1e-5 relative (fp32) / 1e-12 (fp64 STRICT, where supports must be identical)."""
     from oracle import oracle as orc   # checker only, outside the timed region
     B = X.shape[0]
-    ids = spread_vectors(B, extra=max(0, nvec - 18))
+    ids = list(range(B)) if B <= 2 * nvec else spread_vectors(B, extra=max(0, nvec - 18))
     want = fst.candidate_count(s_val, WIDEN, sk.m)
     p = fst.StreamParams(epsilon=eps_val, s=s_val, J=J, K=K, widen=WIDEN)
     a64 = A.double().cpu().numpy()
