@@ -10,9 +10,14 @@
  * maintainer would add.
  *
  * Residency: every `const void* X` / output pointer may be HOST or DEVICE
- * memory (detected with cudaPointerGetAttributes). Host buffers are staged
- * through pinned memory in chunks overlapped with compute (the end-to-end
- * path); device buffers are used in place.
+ * memory (detected with cudaPointerGetAttributes); device buffers are used in
+ * place. Host buffers are copied in chunks (the end-to-end path) on two
+ * copy streams, chunk i+1's input copy and kernel overlapping chunk i's
+ * compute and output copy. The copies run straight from / to the caller's
+ * buffers: page-locked (cudaHostAlloc / cudaHostRegister) host memory gets
+ * fully asynchronous DMA; pageable memory still overlaps compute (each
+ * chunk's output copy is issued only after the next chunk's kernel is
+ * queued) but costs the driver's staging copy.
  *
  * Errors: every function returns an fstg_status; the message of the last
  * failure on the calling thread is returned by fstg_last_error(). There is no

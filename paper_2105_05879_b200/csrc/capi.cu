@@ -574,17 +574,12 @@ uint64_t get_le(const unsigned char* p, int bytes) {
 
 // Streams a device matrix (rows x cols, pitch ld elements of size es_dev) to
 // the file as rows x cols values of size es_file (widening f32 -> f64 exactly).
+// Whole rows per chunk while a row fits the pinned chunk; longer rows (m above
+// kChunkBytes / 8 values, e.g. a reference file's huge m) go in element pieces.
 void write_device_matrix(FILE* f, const void* dev, int64_t rows, int64_t cols, int64_t ld, size_t es_dev,
                          size_t es_file, PinnedBuf& buf, const std::string& path) {
-  const size_t row_bytes_dev = size_t(cols) * es_dev;
-  const int64_t rows_per_chunk = std::max<int64_t>(1, int64_t(kChunkBytes / (size_t(cols) * 8)));
   std::vector<double> wide;
-  for (int64_t r0 = 0; r0 < rows; r0 += rows_per_chunk) {
-    const int64_t rc = std::min(rows_per_chunk, rows - r0);
-    cuda_check(cudaMemcpy2D(buf.p, row_bytes_dev, static_cast<const char*>(dev) + size_t(r0) * ld * es_dev, size_t(ld) * es_dev,
-                            row_bytes_dev, size_t(rc), cudaMemcpyDeviceToHost),
-               "D2H sketch chunk");
-    const size_t count = size_t(rc) * size_t(cols);
+  auto emit = [&](size_t count) {
     size_t wrote;
     if (es_dev == es_file) {
       wrote = std::fwrite(buf.p, es_file, count, f);
@@ -595,7 +590,28 @@ void write_device_matrix(FILE* f, const void* dev, int64_t rows, int64_t cols, i
       wrote = std::fwrite(wide.data(), 8, count, f);
     }
     if (wrote != count) throw CodedError(FSTG_ERR_IO, "write failed: " + path);
+  };
+  const size_t piece = kChunkBytes / 8;  // values per chunk (the widened copy is 8 bytes per value)
+  if (size_t(cols) <= piece) {
+    const size_t row_bytes_dev = size_t(cols) * es_dev;
+    const int64_t rows_per_chunk = int64_t(piece / size_t(cols));
+    for (int64_t r0 = 0; r0 < rows; r0 += rows_per_chunk) {
+      const int64_t rc = std::min(rows_per_chunk, rows - r0);
+      cuda_check(cudaMemcpy2D(buf.p, row_bytes_dev, static_cast<const char*>(dev) + size_t(r0) * ld * es_dev,
+                              size_t(ld) * es_dev, row_bytes_dev, size_t(rc), cudaMemcpyDeviceToHost),
+                 "D2H sketch chunk");
+      emit(size_t(rc) * size_t(cols));
+    }
+    return;
   }
+  for (int64_t r = 0; r < rows; ++r)
+    for (int64_t c0 = 0; c0 < cols; c0 += int64_t(piece)) {
+      const size_t cc = std::min<size_t>(piece, size_t(cols - c0));
+      cuda_check(cudaMemcpy(buf.p, static_cast<const char*>(dev) + (size_t(r) * ld + size_t(c0)) * es_dev,
+                            cc * es_dev, cudaMemcpyDeviceToHost),
+                 "D2H sketch piece");
+      emit(cc);
+    }
 }
 
 void save_impl(const fstg_sketch* sk, const char* path, int version) {
@@ -625,26 +641,36 @@ void save_impl(const fstg_sketch* sk, const char* path, int version) {
 
 // Reads rows x cols values of es_file bytes from the file into a device matrix
 // (pitch ld elements of the sketch dtype), rounding f64 -> f32 on the GPU.
+// Whole rows per chunk while a row fits the 64 MiB pinned / staging buffers;
+// a longer row (an FSTK header may declare any m) is read in element pieces,
+// so no file content can make a read exceed either buffer.
 void read_device_matrix(FILE* f, void* dev, int64_t rows, int64_t cols, int64_t ld, size_t es_file, size_t es_dev,
                         PinnedBuf& buf, void* staging, cudaStream_t st, const std::string& path) {
-  const int64_t rows_per_chunk = std::max<int64_t>(1, int64_t(kChunkBytes / (size_t(cols) * es_file)));
-  for (int64_t r0 = 0; r0 < rows; r0 += rows_per_chunk) {
-    const int64_t rc = std::min(rows_per_chunk, rows - r0);
-    const size_t count = size_t(rc) * size_t(cols);
+  // one piece: rc rows of cc values starting at (r0, c0)
+  auto piece = [&](int64_t r0, int64_t rc, int64_t c0, int64_t cc) {
+    const size_t count = size_t(rc) * size_t(cc);
     cuda_check(cudaStreamSynchronize(st), "sync");  // previous chunk's copy out of `buf` is done
     if (std::fread(buf.p, es_file, count, f) != count)
       throw CodedError(FSTG_ERR_TRUNCATED, "FSTK payload truncated: " + path);
+    char* dst = static_cast<char*>(dev) + (size_t(r0) * ld + size_t(c0)) * es_dev;
     if (es_file == es_dev) {
-      cuda_check(cudaMemcpy2DAsync(static_cast<char*>(dev) + size_t(r0) * ld * es_dev, size_t(ld) * es_dev, buf.p,
-                                   size_t(cols) * es_file, size_t(cols) * es_file, size_t(rc), cudaMemcpyHostToDevice,
-                                   st),
+      cuda_check(cudaMemcpy2DAsync(dst, size_t(ld) * es_dev, buf.p, size_t(cc) * es_file, size_t(cc) * es_file,
+                                   size_t(rc), cudaMemcpyHostToDevice, st),
                  "H2D sketch chunk");
     } else {
       cuda_check(cudaMemcpyAsync(staging, buf.p, count * es_file, cudaMemcpyHostToDevice, st), "H2D sketch chunk");
-      f64_to_f32_pitched<<<148 * 8, 256, 0, st>>>(static_cast<const double*>(staging), rc, cols,
-                                                 static_cast<float*>(dev) + size_t(r0) * ld, ld);
+      f64_to_f32_pitched<<<148 * 8, 256, 0, st>>>(static_cast<const double*>(staging), rc, cc,
+                                                 reinterpret_cast<float*>(dst), ld);
       cuda_check(cudaGetLastError(), "f64->f32");
     }
+  };
+  const size_t per = kChunkBytes / es_file;  // values per chunk
+  if (size_t(cols) <= per) {
+    const int64_t rows_per_chunk = int64_t(per / size_t(cols));
+    for (int64_t r0 = 0; r0 < rows; r0 += rows_per_chunk) piece(r0, std::min(rows_per_chunk, rows - r0), 0, cols);
+  } else {
+    for (int64_t r = 0; r < rows; ++r)
+      for (int64_t c0 = 0; c0 < cols; c0 += int64_t(per)) piece(r, 1, c0, std::min<int64_t>(int64_t(per), cols - c0));
   }
   cuda_check(cudaStreamSynchronize(st), "sync");
 }
@@ -941,6 +967,40 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
     cuda_check(cudaStreamWaitEvent(copy_st, ev_in[0], 0), "wait");
   }
 
+  struct Pending {
+    int64_t v0 = -1, cb = 0;
+    int b = 0;
+  } pending;
+  // D2H of a finished chunk's outputs on out_st (ordered after its kernel by ev_done)
+  auto drain = [&]() {
+    if (pending.v0 < 0) return;
+    const int64_t v0 = pending.v0, cb = pending.cb;
+    Bufs& bf = bufs[pending.b];
+    pending.v0 = -1;
+    cuda_check(cudaStreamWaitEvent(out_st, ev_done[pending.b], 0), "wait");
+    auto d2h = [&](void* dst, const void* src, size_t bytes) {
+      cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, out_st), "D2H");
+    };
+    d2h(out.counts + v0, bf.counts.p, size_t(cb) * sizeof(int32_t));
+    d2h(out.support + v0 * want, bf.support.p, size_t(cb) * want * sizeof(int32_t));
+    d2h(static_cast<T*>(out.values) + v0 * want, bf.values.p, size_t(cb) * want * sizeof(T));
+    if (out.cands) d2h(out.cands + v0 * want, bf.cands.p, size_t(cb) * want * sizeof(int32_t));
+    if (out.mu) d2h(static_cast<T*>(out.mu) + v0 * m, bf.mu.p, size_t(cb) * m * sizeof(T));
+    cuda_check(cudaEventRecord(ev_out[pending.b], out_st), "event");
+  };
+  // On an error mid-loop the copy streams may still be reading or writing this call's
+  // buffers: let them finish before the stream-ordered frees on st release the memory.
+  struct DrainOnThrow {
+    cudaStream_t a, b, c;
+    bool armed = true;
+    ~DrainOnThrow() {
+      if (!armed) return;
+      if (a) cudaStreamSynchronize(a);
+      if (b) cudaStreamSynchronize(b);
+      if (c) cudaStreamSynchronize(c);
+      cudaGetLastError();
+    }
+  } guard{copy_st, out_st, st};
   int it = 0;
   for (int64_t v0 = 0, cb = 0; v0 < B; v0 += cb, ++it) {
     cb = std::min(next_chunk, B - v0);
@@ -1030,24 +1090,17 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
                    pct(8, 13), pct(9, 13));
     }
     // ---- outputs ----
+    // The D2H of chunk i is issued after chunk i+1's copy-in and kernel are queued (next
+    // iteration): a copy into pageable host memory blocks this thread until it completes,
+    // and deferring it keeps the next kernel queued behind the running one either way.
     if (!all_dev) {
       cuda_check(cudaEventRecord(ev_done[b], st), "event");
-      if (!o_dev) {
-        cuda_check(cudaStreamWaitEvent(out_st, ev_done[b], 0), "wait");
-        auto d2h = [&](void* dst, const void* src, size_t bytes) {
-          cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, out_st), "D2H");
-        };
-        d2h(out.counts + v0, bf.counts.p, size_t(cb) * sizeof(int32_t));
-        d2h(out.support + v0 * want, bf.support.p, size_t(cb) * want * sizeof(int32_t));
-        d2h(static_cast<T*>(out.values) + v0 * want, bf.values.p, size_t(cb) * want * sizeof(T));
-        if (out.cands) d2h(out.cands + v0 * want, bf.cands.p, size_t(cb) * want * sizeof(int32_t));
-        if (out.mu) d2h(static_cast<T*>(out.mu) + v0 * m, bf.mu.p, size_t(cb) * m * sizeof(T));
-        cuda_check(cudaEventRecord(ev_out[b], out_st), "event");
-      } else {
-        cuda_check(cudaEventRecord(ev_out[b], st), "event");
-      }
+      if (o_dev) cuda_check(cudaEventRecord(ev_out[b], st), "event");
+      drain();
+      if (!o_dev) pending = Pending{v0, cb, b};
     }
   }
+  if (!all_dev) drain();
   if (indices != nullptr) {
     int h = 0;
     cuda_check(cudaMemcpyAsync(&h, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st), "copy flag");
@@ -1059,6 +1112,7 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
     cuda_check(cudaStreamSynchronize(out_st), "sync copies");
     cuda_check(cudaStreamSynchronize(st), "sync compute");
   }
+  guard.armed = false;
 }
 
 // ------------------------------------------- row-blocked design transform ----

@@ -371,6 +371,9 @@ def transform_gathered_batch(sk: Sketch, X, p: StreamParams, indices, gathered, 
     want = candidate_count(p.s, p.widen, sk.m)
     if out is None:
         out = _alloc_outputs(_is_torch(X) and X.is_cuda, B, want, sk.m, sk.dtype, candidates, mu, sk.device)
+    else:
+        _check_outputs(out, B, want, sk.m, sk.dtype, None)
+    _check_buf("indices", indices, (B, p.J * p.K), ("int64",))
     pc = p._c()
     _check(lib().fstg_transform_gathered_batch(sk.handle, _ptr(X), C.c_int64(B), C.byref(pc), _ptr(indices),
                                                _ptr(gathered), _ptr(out.counts), _ptr(out.support), _ptr(out.values),
@@ -405,8 +408,11 @@ def transform_design_batch(sk: Sketch, X, p: StreamParams, seeds=None, *, row_bl
     want = candidate_count(p.s, p.widen, sk.m)
     if out is None:
         out = _alloc_outputs(True, B, want, sk.m, sk.dtype, candidates, mu, sk.device)
+    else:
+        _check_outputs(out, B, want, sk.m, sk.dtype, _buf_info(X)[2])
     if seeds is not None and not (_is_torch(seeds) and seeds.is_cuda):
         seeds = torch.from_numpy(np.ascontiguousarray(seeds, dtype=np.uint64).view(np.int64)).to(X.device)
+    _check_seeds(seeds, B)
     pc = p._c()
     _check(lib().fstg_transform_design_batch(sk.handle, _ptr(X), C.c_int64(B), C.byref(pc), _ptr(seeds),
                                              C.c_int64(row_block), _ptr(out.counts), _ptr(out.support),
@@ -435,7 +441,11 @@ def design_partial_means(sk: Sketch, X, p: StreamParams, seeds=None, row_begin: 
     B, h = X.shape[0], row_end - row_begin
     if out is None:
         out = torch.empty((B, p.K, h), dtype=X.dtype, device=X.device)
+    elif (out.dim() != 3 or tuple(out.shape[:2]) != (B, p.K) or out.shape[2] < h or out.dtype != X.dtype
+          or out.device != X.device or out.stride(2) != 1):
+        raise ValueError("design_partial_means: out must be a (B, K, >= rows) tensor like X")
     seeds = _dev_seeds(seeds, X.device)
+    _check_seeds(seeds, B)
     _check(lib().fstg_design_partial_means(sk.handle, _ptr(X), C.c_int64(B), C.byref(p._c()), _ptr(seeds),
                                            C.c_int64(row_begin), C.c_int64(row_end), C.c_int64(row_block), _ptr(out),
                                            C.c_int64(out.stride(0)), C.c_int64(out.stride(1)), C.c_void_p(stream)))
@@ -454,6 +464,10 @@ def transform_from_means(sk: Sketch, X, p: StreamParams, means, *, candidates: b
     want = candidate_count(p.s, p.widen, sk.m)
     if out is None:
         out = _alloc_outputs(True, B, want, sk.m, sk.dtype, candidates, mu, sk.device)
+    else:
+        _check_outputs(out, B, want, sk.m, sk.dtype, _buf_info(X)[2])
+    if means.dim() != 3 or means.shape[0] != B or means.shape[1] < p.K + 1 or means.shape[2] < sk.m:
+        raise ValueError("transform_from_means: means must be (B, K + 1, ld >= m)")
     _check(lib().fstg_transform_from_means(sk.handle, _ptr(X), C.c_int64(B), C.byref(p._c()), _ptr(means),
                                            C.c_int64(means.stride(0)), C.c_int64(means.stride(1)), _ptr(out.counts),
                                            _ptr(out.support), _ptr(out.values), _ptr(out.candidates), _ptr(out.mu),
@@ -515,6 +529,46 @@ def _alloc_outputs(like_torch, B, want, m, dtype, want_cands, want_mu, device):
                        np.zeros((B, m), dtype=dtype) if want_mu else None)
 
 
+def _buf_info(a):
+    """(shape, dtype name, device tag) of a numpy array or torch tensor."""
+    if _is_torch(a):
+        return tuple(a.shape), str(a.dtype).split(".")[-1], ("cuda:%d" % a.device.index if a.is_cuda else "cpu")
+    a = np.asarray(a)
+    return a.shape, a.dtype.name, "cpu"
+
+
+def _check_buf(name, a, shape, dtypes, device=None):
+    """Rejects a caller buffer the C-ABI would read or write past (wrong length / dtype / device)."""
+    if a is None:
+        return
+    shp, dt, dev = _buf_info(a)
+    if tuple(shp) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(shp)} != {tuple(shape)}")
+    if dt not in dtypes:
+        raise ValueError(f"{name}: dtype {dt} not in {dtypes}")
+    if device is not None and dev != device:
+        raise ValueError(f"{name}: on {dev}, expected {device}")
+
+
+def _check_seeds(seeds, B):
+    if seeds is not None:
+        _check_buf("seeds", seeds, (B,), ("int64", "uint64"))
+
+
+def _check_outputs(out: "BatchResult", B, want, m, dtype, like):
+    """Every output buffer must hold B vectors of the right width and dtype, all on the same side
+    (host or the sketch's device) as `like` decides."""
+    vdt = np.dtype(dtype).name
+    dev = _buf_info(out.counts)[2]
+    if like is not None and like != dev:
+        raise ValueError(f"outputs on {dev} but inputs on {like}")
+    _check_buf("counts", out.counts, (B,), ("int32",), dev)
+    _check_buf("support", out.support, (B, want), ("int32",), dev)
+    _check_buf("values", out.values, (B, want), (vdt,), dev)
+    _check_buf("candidates", out.candidates, (B, want), ("int32",), dev)
+    _check_buf("mu", out.mu, (B, m), (vdt,), dev)
+
+
 def _prep_x(sk: Sketch, X):
     if _is_torch(X):
         X = X.contiguous()
@@ -538,8 +592,11 @@ def transform_batch(sk: Sketch, X, p: StreamParams, seeds=None, *, candidates: b
     p.validate()
     if out is None:
         out = _alloc_outputs(_is_torch(X) and X.is_cuda, B, want, sk.m, sk.dtype, candidates, mu, sk.device)
+    else:
+        _check_outputs(out, B, want, sk.m, sk.dtype, None)
     if seeds is not None and not _is_torch(seeds):
         seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    _check_seeds(seeds, B)
     pc = p._c()
     _check(lib().fstg_transform_batch(sk.handle, _ptr(X), C.c_int64(B), C.byref(pc), _ptr(seeds),
                                       _ptr(out.counts), _ptr(out.support), _ptr(out.values),
@@ -558,9 +615,12 @@ def transform_with_samples_batch(sk: Sketch, X, p: StreamParams, indices, *, can
         indices = np.ascontiguousarray(indices, dtype=np.int64).reshape(B, -1)
     if tuple(indices.shape) != (B, p.J * p.K):
         raise ValueError("transform: drawn sample count does not match J*K")
+    _check_buf("indices", indices, (B, p.J * p.K), ("int64",))
     want = candidate_count(p.s, p.widen, sk.m)
     if out is None:
         out = _alloc_outputs(_is_torch(X) and X.is_cuda, B, want, sk.m, sk.dtype, candidates, mu, sk.device)
+    else:
+        _check_outputs(out, B, want, sk.m, sk.dtype, None)
     pc = p._c()
     _check(lib().fstg_transform_with_samples_batch(sk.handle, _ptr(X), C.c_int64(B), C.byref(pc), _ptr(indices),
                                                    _ptr(out.counts), _ptr(out.support), _ptr(out.values),

@@ -106,3 +106,30 @@ def test_no_cpu_fallback_without_gpu(fst):
     assert fst.device_count() == 0
     with pytest.raises(fst.CudaError):
         fst.preprocess(np.eye(4))
+
+
+def test_python_buffer_validation():
+    """The Python mirror rejects buffers the C-ABI would read or write past:
+    short or mistyped seeds, mis-shaped outputs, outputs on the wrong side."""
+    from paper_2105_05879_b200 import fst
+    B, want, m = 4, 10, 32
+    fst._check_seeds(np.zeros(B, dtype=np.uint64), B)
+    fst._check_seeds(np.zeros(B, dtype=np.int64), B)
+    for bad in (np.zeros(B - 1, dtype=np.uint64), np.zeros(B, dtype=np.int32), np.zeros((B, 1), dtype=np.int64)):
+        with pytest.raises(ValueError):
+            fst._check_seeds(bad, B)
+    ok = fst.BatchResult(np.zeros(B, np.int32), np.zeros((B, want), np.int32), np.zeros((B, want), np.float32),
+                         np.zeros((B, want), np.int32), np.zeros((B, m), np.float32))
+    fst._check_outputs(ok, B, want, m, np.float32, None)
+    bad_cases = [
+        fst.BatchResult(np.zeros(B - 1, np.int32), ok.support, ok.values),
+        fst.BatchResult(ok.counts, np.zeros((B, want - 1), np.int32), ok.values),
+        fst.BatchResult(ok.counts, ok.support, np.zeros((B, want), np.float64)),
+        fst.BatchResult(ok.counts, ok.support, ok.values, np.zeros((B, want), np.int64)),
+        fst.BatchResult(ok.counts, ok.support, ok.values, None, np.zeros((B, m + 1), np.float32)),
+    ]
+    for out in bad_cases:
+        with pytest.raises(ValueError):
+            fst._check_outputs(out, B, want, m, np.float32, None)
+    with pytest.raises(ValueError):  # host outputs for device inputs
+        fst._check_outputs(ok, B, want, m, np.float32, "cuda:0")

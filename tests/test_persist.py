@@ -138,3 +138,46 @@ def test_gpu_load_errors_and_no_matrix(fst, orc, tmp_path):
         fst.transform(g, np.ones(4), fst.StreamParams(epsilon=0.1, s=1, J=2, K=2))
     with pytest.raises(fst.NoMatrixError):
         g.embedded_matrix()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_gpu_load_rows_longer_than_staging_chunk(tmp_path, dtype):
+    """A reference FSTK v1 file whose m (8,388,613) makes one column longer than the 64 MiB
+    pinned / staging chunk: the load reads element pieces, never past either
+    buffer, and save writes the same bytes back. Sparse file: zeros except a few marked values
+    at the piece boundaries."""
+    import struct
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2105_05879_b200 import fst
+    m, n, k = 8388613, 3, 2
+    d, L = 4, 12
+    path = str(tmp_path / "tall.fstk")
+    header = b"FSTK" + struct.pack("<IQQQQQB", 1, m, n, k, d, L, 1)
+    payload = 8 * m * L + 8 * m * n
+    with open(path, "wb") as f:
+        f.write(header)
+        f.truncate(49 + payload)
+    marks = {(0, 0): 1.5, (0, 8388607): -2.25, (0, 8388608): 3.0, (0, m - 1): 4.5, (1, 0): -6.0, (11, m - 1): 7.0}
+    for (col, row), val in marks.items():
+        _corrupt(path, 49 + 8 * (col * m + row), struct.pack("<d", val))
+    _corrupt(path, 49 + 8 * m * L + 8 * (m * n - 1), struct.pack("<d", 9.0))   # last entry of A
+    sk = fst.load(path, dtype=dtype)
+    assert (sk.m, sk.n, sk.L) == (m, n, L)
+    for (col, row), val in marks.items():
+        c = sk.column(col)
+        assert c[row] == val, (col, row)
+    assert np.count_nonzero(sk.column(0)) == 4
+    assert sk.embedded_matrix()[-1, -1] == 9.0
+    if dtype == np.float64:
+        out = str(tmp_path / "tall2.fstk")
+        fst.save(sk, out, version=1)
+        with open(path, "rb") as a, open(out, "rb") as b:
+            while True:
+                x, y = a.read(1 << 24), b.read(1 << 24)
+                assert x == y
+                if not x:
+                    break
+    sk.close()
