@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--row-block", type=int, default=0,
                     help="config 4: rows per retain-sampled block (0 = as many as ~70%% of free HBM holds)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--choose-params", action="store_true",
+                    help="J, K from choose_params(row_norm_max, gamma = eps/2, eta = 0.1, m), the reference CLI's "
+                         "default (cli.hpp:164-172, stream.hpp:58-69), instead of the paper's J=375, K=2")
     ap.add_argument("--no-parity", action="store_true", help="skip the post-timing oracle check of the timed batch")
     ap.add_argument("--config", default="3", choices=["1", "2", "3", "4", "5"],
                     help="BASELINE.json configs: 3 = headline (default); 1, 2 = parity-case workloads; "
@@ -226,6 +229,11 @@ class ClockSampler:
 
 
 # -------------------------------------------------------- CPU baseline ----
+def pool_size(N, m, budget=1.5e9):
+    """Prepared vectors for the CPU leg: their materialised fp64 columns (P x N x m) within ~1.5 GB."""
+    return int(max(1, min(32, budget // (N * m * 8))))
+
+
 def cpu_sample(a64: np.ndarray, X64: np.ndarray, seeds: np.ndarray, J: int, K: int, threads: int,
                target_s: float, predrawn: bool = False, s_val: int = S, eps_val: float = EPS):
     """The reference algorithm (oracle restatement) on host cores over a pool of prepared vectors.
@@ -258,14 +266,14 @@ def cpu_sample(a64: np.ndarray, X64: np.ndarray, seeds: np.ndarray, J: int, K: i
 # ------------------------------------------------------------ GPU arm ----
 WORKLOADS = {
     "3": dict(n=4096, dtype="fp32", s=32, eps=0.1, B=65536, a="haar", a_seed=4096,
-              desc="config3: n=m=4096, s=32, eps=0.1, J=375, K=2, widen=10 (N=750, want=320)",
+              desc="config3: n=m=4096, s=32, eps=0.1, J={J}, K={K}, widen=10 (N={N}, want=320)",
               data="synthetic (seeded config-3 generator: Haar-orthogonal A, y 32-sparse +-1/sqrt(32) + N(0,1e-6), "
                    "x = A^T y / |.|)"),
     "1": dict(n=256, dtype="fp64", s=8, eps=0.1, B=64, a="haar", a_seed=777,
-              desc="config1: n=m=256 fp64, s=8, eps=0.1, 64 vectors/step, J=375, K=2, widen=10",
+              desc="config1: n=m=256 fp64, s=8, eps=0.1, 64 vectors/step, J={J}, K={K}, widen=10",
               data="synthetic (Haar-orthogonal A, y 8-sparse +-1/sqrt(8), x = A^T y)"),
     "2": dict(n=1024, dtype="fp32", s=16, eps=0.05, B=4096, a="iid", a_seed=1024,
-              desc="config2: n=m=1024 fp32, A iid N(0,1/n), s=16, eps=0.05, 4096 vectors/step, J=375, K=2",
+              desc="config2: n=m=1024 fp32, A iid N(0,1/n), s=16, eps=0.05, 4096 vectors/step, J={J}, K={K}",
               data="synthetic (A iid N(0,1/n), y 16-sparse N(0,1), x = A^-1 y / |.|)"),
 }
 
@@ -297,7 +305,10 @@ def batch_size(args, cfg):
 
 def workload_config(args, cfg, world):
     """The `config` object both arms print (identical keys and values)."""
-    return {"workload": cfg["desc"], "vectors_per_gpu_per_step": batch_size(args, cfg), "J": args.J, "K": args.K,
+    desc = cfg["desc"].format(J=args.J, K=args.K, N=args.J * args.K)
+    if args.choose_params:
+        desc += " (J, K from choose_params(row_norm_max, eps/2, 0.1, m): the reference CLI default, cli.hpp:164-172)"
+    return {"workload": desc, "vectors_per_gpu_per_step": batch_size(args, cfg), "J": args.J, "K": args.K,
             "widen": WIDEN, "parallelism": f"vector-sharded x{world}, sketch replicated per GPU",
             "l2": ("inputs larger than L2 (137.5 GB sketch; 1 GiB of x per step)" if args.config == "3"
                    else "small config: sketch may be L2-resident")}
@@ -362,6 +373,9 @@ def run_b200(args):
     ident_ms, _ = fst.profile_read("preprocess_identity")
     pre_ms = parallel.max_over_ranks(sk.preprocess_ms + gather_ms, device=dev)
     sketch_bytes = sk.L * sk.m * es
+
+    if args.choose_params:  # the reference CLI's default regime (cli.hpp:164-172)
+        args.J, args.K = fst.choose_params(sk.row_norm_max(), cfg["eps"] / 2, 0.1, sk.m)
 
     # ---- this rank's shard of the vector stream ----
     B = batch_size(args, cfg)
@@ -480,7 +494,7 @@ def run_b200(args):
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and args.config == "3":
-        P = 32
+        P = pool_size(N, sk.m)
         a64 = prob.A.double().cpu().numpy()          # exactly the A the GPU computes on
         X64 = X[:P].double().cpu().numpy()
         threads = os.cpu_count() or 1
@@ -563,9 +577,16 @@ def run_b200(args):
 
 
 # ------------------------------------------------- config 5: sweep + GEMM ----
+L2_TMA_PEAK_GBS = 19600.0  # L2-resident 16 KiB bulk copies, 2-3 CTAs/SM (profiles/r01_tma_issue.txt)
+
+
 def run_sweep(args):
-    """Config 5: s in {4,16,64,256} x eps in {0.2,0.1,0.05} at n = 4096 on one GPU; the stream path
-    against dense h_eps(A x) by one cuBLAS GEMM per batch (fp32 SGEMM and TF32) on the same batch."""
+    """Config 5: s in {4,16,64,256} x eps in {0.2,0.1,0.05} at n = 4096 on one GPU, one GPU's shard of
+    the 1,048,576-vector job (131,072 vectors per launch = 1,048,576 / 8 GPUs, weak scaling), against
+    dense h_eps(A x) by one cuBLAS GEMM per batch (fp32 SGEMM and TF32) on the same batch. Per s, the
+    three stages of the fused kernel are timed in isolation with its role-removal switches
+    (FSTG_STREAM_DEBUG: 5 = column gather-accumulate only, 6 = coefficients only, 3 = candidate
+    select + refinement only) and each is set against its own roofline."""
     import torch
     from paper_2105_05879_b200 import fst, generators
     dev = "cuda:0"
@@ -573,9 +594,10 @@ def run_sweep(args):
     A64 = generators.haar_orthogonal(N_DIM, A_SEED, dev)
     A32 = A64.float().contiguous()
     sk = fst.preprocess(A32)
-    B = 131072 // 2 if args.batch == 65536 else args.batch  # 1,048,576 / 8 GPUs would be 131,072 per GPU
+    B = 131072 if args.batch == 65536 else args.batch
     stream = torch.cuda.current_stream()
     peak, _ = peaks()
+    reps = max(1, args.steps // 2)
 
     def timed(fn, reps):
         fn()
@@ -588,51 +610,87 @@ def run_sweep(args):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps
 
-    rows = []
-    for s_val in (4, 16, 64, 256):
-        prob = generators.config5_problem(s_val, 0.1, B, seed=X_SEED, device=dev, A64=A64)
-        X = prob.X
-        seeds_dev = torch.from_numpy(prob.seeds.view(np.int64)).to(dev)
-        for eps_val in (0.2, 0.1, 0.05):
-            p = fst.StreamParams(epsilon=eps_val, s=s_val, J=args.J, K=args.K, widen=WIDEN)
+    def kernel_ms(fn):
+        """stream-kernel device time per launch (library CUDA events) over `reps` calls."""
+        fn()
+        fst.profile_enable(True)
+        fst.profile_reset()
+        for _ in range(reps):
+            fn()
+        torch.cuda.synchronize()
+        k_ms, k_n = fst.profile_read("stream")
+        fst.profile_enable(False)
+        return k_ms / max(1, k_n)
+
+    rows, stages = [], []
+    N = args.J * args.K
+    with ClockSampler(0) as clk:
+        for s_val in (4, 16, 64, 256):
+            prob = generators.config5_problem(s_val, 0.1, B, seed=X_SEED, device=dev, A64=A64)
+            X = prob.X
+            seeds_dev = torch.from_numpy(prob.seeds.view(np.int64)).to(dev)
             want = fst.candidate_count(s_val, WIDEN, N_DIM)
+            p = fst.StreamParams(epsilon=0.1, s=s_val, J=args.J, K=args.K, widen=WIDEN)
             out = fst.transform_batch(sk, X, p, seeds_dev, stream=stream.cuda_stream)
-            fst.profile_enable(True)
-            fst.profile_reset()
-            ms_stream = timed(lambda: fst.transform_batch(sk, X, p, seeds_dev, out=out, stream=stream.cuda_stream),
-                              max(1, args.steps // 2))
-            k_ms, k_n = fst.profile_read("stream")
-            fst.profile_enable(False)
-            torch.backends.cuda.matmul.allow_tf32 = False
-            dense = lambda: torch.where((ax := X @ A32.T).abs() >= eps_val, ax, 0.0)  # noqa: E731
-            ms_sgemm = timed(dense, 3)
-            torch.backends.cuda.matmul.allow_tf32 = True
-            ms_tf32 = timed(dense, 3)
-            torch.backends.cuda.matmul.allow_tf32 = False
-            # support agreement of the stream with the exact dense threshold (fp64 reference)
-            sub = min(B, 4096)
-            ax = X[:sub].double() @ A64.T
-            dense_sup = ax.abs() >= eps_val
-            counts = out.counts[:sub].long()
-            stream_sup = torch.zeros_like(dense_sup)
-            valid = torch.arange(want, device=dev).unsqueeze(0) < counts.unsqueeze(1)
-            r_idx = torch.arange(sub, device=dev).unsqueeze(1).expand(-1, want)
-            stream_sup[r_idx[valid], out.support[:sub].long()[valid]] = True
-            match = float((stream_sup == dense_sup).all(dim=1).float().mean())
-            bvec = bytes_per_vector(args.J * args.K, N_DIM, N_DIM, want)
-            per_launch = k_ms / max(1, k_n)
-            rows.append({"s": s_val, "eps": eps_val, "want": want,
-                         "stream_vectors_per_s": B / (ms_stream / 1e3),
-                         "stream_roofline_frac": bvec * B / (per_launch / 1e3) / 1e9 / peak,
-                         "dense_sgemm_vectors_per_s": B / (ms_sgemm / 1e3),
-                         "dense_tf32_vectors_per_s": B / (ms_tf32 / 1e3),
-                         "support_match_vs_exact": match,
-                         "mean_true_support": float(dense_sup.sum(dim=1).float().mean()),
-                         "mean_stream_support": float(counts.float().mean())})
-    line = {"metric": "config5 sweep: thresholded-Ax vectors/sec vs dense GEMM (1 B200)", "n_gpus": 1,
-            "config": {"workload": f"config5: n=4096 fp32 Haar A, x = A^T y (s-sparse +-1/sqrt(s)), {B} vectors "
-                                   f"per batch, J={args.J}, K={args.K}, widen=10"},
-            "sweep": rows}
+            call = lambda: fst.transform_batch(sk, X, p, seeds_dev, out=out, stream=stream.cuda_stream)  # noqa: E731
+            st = {"s": s_val, "want": want}
+            try:
+                for name, bits in (("full", 0), ("gather_accumulate", 5), ("coefficients", 6), ("refinement", 3)):
+                    os.environ["FSTG_STREAM_DEBUG"] = str(bits)
+                    st[name + "_ms"] = kernel_ms(call)
+            finally:
+                os.environ.pop("FSTG_STREAM_DEBUG", None)
+            col_bytes = 4.0 * N * N_DIM * B
+            adds = float(N) * N_DIM * B
+            row_bytes = 4.0 * want * N_DIM * B
+            st["gather_accumulate_roofline"] = {"bound": "hbm", "unit": "GB/s", "peak": peak,
+                                                "achieved": col_bytes / st["gather_accumulate_ms"] / 1e6,
+                                                "frac": col_bytes / st["gather_accumulate_ms"] / 1e6 / peak}
+            st["coefficients_roofline"] = {"bound": "fp32 add", "unit": "Tadd/s", "peak": FP32_ADD_PEAK_TADD,
+                                           "achieved": adds / st["coefficients_ms"] / 1e9,
+                                           "frac": adds / st["coefficients_ms"] / 1e9 / FP32_ADD_PEAK_TADD}
+            st["refinement_roofline"] = {"bound": "l2", "unit": "GB/s", "peak": L2_TMA_PEAK_GBS,
+                                         "achieved": row_bytes / st["refinement_ms"] / 1e6,
+                                         "frac": row_bytes / st["refinement_ms"] / 1e6 / L2_TMA_PEAK_GBS}
+            st["full_hbm_frac_dram_bytes"] = (4.0 * (N * N_DIM + N_DIM) * B) / st["full_ms"] / 1e6 / peak
+            stages.append(st)
+            for eps_val in (0.2, 0.1, 0.05):
+                p = fst.StreamParams(epsilon=eps_val, s=s_val, J=args.J, K=args.K, widen=WIDEN)
+                out = fst.transform_batch(sk, X, p, seeds_dev, stream=stream.cuda_stream)
+                ms_stream = timed(lambda: fst.transform_batch(sk, X, p, seeds_dev, out=out, stream=stream.cuda_stream),
+                                  reps)
+                torch.backends.cuda.matmul.allow_tf32 = False
+                dense = lambda: torch.where((ax := X @ A32.T).abs() >= eps_val, ax, 0.0)  # noqa: E731
+                ms_sgemm = timed(dense, 3)
+                torch.backends.cuda.matmul.allow_tf32 = True
+                ms_tf32 = timed(dense, 3)
+                torch.backends.cuda.matmul.allow_tf32 = False
+                # support agreement of the stream with the exact dense threshold (fp64 reference)
+                sub = min(B, 4096)
+                ax = X[:sub].double() @ A64.T
+                dense_sup = ax.abs() >= eps_val
+                counts = out.counts[:sub].long()
+                stream_sup = torch.zeros_like(dense_sup)
+                valid = torch.arange(want, device=dev).unsqueeze(0) < counts.unsqueeze(1)
+                r_idx = torch.arange(sub, device=dev).unsqueeze(1).expand(-1, want)
+                stream_sup[r_idx[valid], out.support[:sub].long()[valid]] = True
+                match = float((stream_sup == dense_sup).all(dim=1).float().mean())
+                rows.append({"s": s_val, "eps": eps_val, "want": want,
+                             "stream_vectors_per_s": B / (ms_stream / 1e3),
+                             "stream_hbm_frac_dram_bytes": 4.0 * (N * N_DIM + N_DIM) * B / ms_stream / 1e6 / peak,
+                             "dense_sgemm_vectors_per_s": B / (ms_sgemm / 1e3),
+                             "dense_tf32_vectors_per_s": B / (ms_tf32 / 1e3),
+                             "support_match_vs_exact": match,
+                             "mean_true_support": float(dense_sup.sum(dim=1).float().mean()),
+                             "mean_stream_support": float(counts.float().mean())})
+            del prob, X, out
+    line = {"metric": "config5 sweep: thresholded-Ax vectors/sec vs dense GEMM (1 B200 = one GPU's shard)", "n_gpus": 1,
+            "config": {"workload": f"config5: n=4096 fp32 Haar A, x = A^T y (s-sparse +-1/sqrt(s)), {B} vectors per "
+                                   f"launch (1,048,576 / 8 GPUs), J={args.J}, K={args.K}, widen=10"},
+            "sweep": rows, "stages": stages,
+            "stage_note": ("stage times are the stream kernel run with the other roles removed (FSTG_STREAM_DEBUG); "
+                           "the fused kernel overlaps them, so full_ms < the sum"),
+            "clocks": clk.summary()}
     print(json.dumps(line), flush=True)
     sk.close()
 
@@ -809,8 +867,11 @@ def run_reference(args):
     A64 = build_matrix(cfg, dev, gaussian_fill=orc.rng_gaussian)
     B_ref = min(batch_size(args, cfg), 8192)        # the b200 arm's first x chunk: same GEMM shape, same bits
     prob = make_problem(cfg, A64, B_ref, 0, dev, targets=orc.gen_sparse_targets)
-    P = min(32, B_ref)
     a64 = prob.A.double().cpu().numpy()
+    if args.choose_params:  # the reference CLI's default regime (cli.hpp:164-172)
+        args.J, args.K = orc.choose_params(float(np.max(np.linalg.norm(a64, axis=1))), cfg["eps"] / 2, 0.1,
+                                           a64.shape[0])
+    P = min(pool_size(args.J * args.K, a64.shape[0]), B_ref)
     X = prob.X[:P].double().cpu().numpy()
     seeds = prob.seeds[:P]
     del prob, A64
