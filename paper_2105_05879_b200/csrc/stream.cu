@@ -400,6 +400,121 @@ __device__ __forceinline__ T coeff_strict(const StreamArgs<T>& A, const T* xs, u
   return acc;
 }
 
+// ----------------------------------------------------------- refinement ----
+__device__ __forceinline__ bool screen_decide(float d, float s, int64_t nv, double eps) {
+  const double k = 4.0 * static_cast<double>((nv + 63) / 64) + 6.0;
+  const double bound = 1.01 * (k + 2.0) * 0x1.0p-24 * static_cast<double>(s) + 1e-30;
+  return !(fabs(static_cast<double>(d)) + bound < eps);  // true: needs the exact dot (NaN included)
+}
+// Exact refinement dot v_i = a_i . x for fp32 rows (stream.hpp:261): every
+// product a_j x_j is exact in fp64 and accumulated in fp64 (lane chunks
+// q = lane + 32 i, two accumulators alternating with i, then a warp tree).
+// Reads the row from global memory (L2-resident A, evict-last policy).
+__device__ __forceinline__ double refine_dot_exact(const float* __restrict__ arow, const float* xs, int64_t n,
+                                                   int lane, uint64_t pol_keep) {
+  constexpr int kRB = 4;
+  double dot = 0.0, dot2 = 0.0;
+  const int64_t nv = (n + 3) / 4;
+  const float4* a4 = reinterpret_cast<const float4*>(arow);
+  const float4* x4 = reinterpret_cast<const float4*>(xs);
+  for (int64_t q0 = lane; q0 < nv; q0 += 32 * kRB) {
+    float4 av[kRB];
+#pragma unroll
+    for (int u = 0; u < kRB; ++u)
+      av[u] = (q0 + 32 * u < nv) ? ldg_f4_policy(a4 + q0 + 32 * u, pol_keep) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < kRB; ++u) {
+      if (q0 + 32 * u < nv) {
+        const float4 xv4 = x4[q0 + 32 * u];
+        double& acc = (u & 1) ? dot2 : dot;
+        acc = fma(static_cast<double>(av[u].x), static_cast<double>(xv4.x), acc);
+        acc = fma(static_cast<double>(av[u].y), static_cast<double>(xv4.y), acc);
+        acc = fma(static_cast<double>(av[u].z), static_cast<double>(xv4.z), acc);
+        acc = fma(static_cast<double>(av[u].w), static_cast<double>(xv4.w), acc);
+      }
+    }
+  }
+  dot += dot2;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  return dot;
+}
+
+// fp32 screening pass of the refinement: d = fl(a . x) by FFMA chains and
+// S = fl(sum |a_j x_j|), in the same chunk order (depth k = 4 ceil(nv / 64) + 6
+// roundings per result). Rounding-error analysis of FMA dot products gives
+// |d - a.x| <= gamma_k S_true with gamma_k = k u / (1 - k u), u = 2^-24, and
+// S_true <= S / (1 - gamma_k); so |a.x| < eps is PROVEN when
+// |d| + 1.01 (k + 2) u S < eps (plus an absolute 1e-30 for underflow). Only
+// the remaining candidates (the support and its neighbourhood; NaN / inf fall
+// through as well) need the exact fp64 dot, whose value is the one reported:
+// outputs are identical to refining every candidate exactly.
+__device__ __forceinline__ bool refine_screen_f32(const float4* a4, const float4* x4, int64_t n, int lane,
+                                                  double eps) {
+  const int64_t nv = (n + 3) / 4;
+  float d0 = 0.f, d1 = 0.f, s0 = 0.f, s1 = 0.f;
+#pragma unroll 4
+  for (int64_t q = lane; q < nv; q += 32) {
+    const float4 av = a4[q], xv = x4[q];
+    const bool odd = (q >> 5) & 1;
+    float& d = odd ? d1 : d0;
+    float& s = odd ? s1 : s0;
+    d = fmaf(av.x, xv.x, d);
+    d = fmaf(av.y, xv.y, d);
+    d = fmaf(av.z, xv.z, d);
+    d = fmaf(av.w, xv.w, d);
+    s = fmaf(fabsf(av.x), fabsf(xv.x), s);
+    s = fmaf(fabsf(av.y), fabsf(xv.y), s);
+    s = fmaf(fabsf(av.z), fabsf(xv.z), s);
+    s = fmaf(fabsf(av.w), fabsf(xv.w), s);
+  }
+  float d = d0 + d1, s = s0 + s1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d += __shfl_xor_sync(0xffffffffu, d, o);
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+  }
+  return screen_decide(d, s, nv, eps);
+}
+
+// The same screening pass with the row read from global memory (rows longer
+// than one ring stage, n > 4096 fp32): kRB 16-byte loads in flight per lane.
+__device__ __forceinline__ bool refine_screen_f32_global(const float4* a4, const float4* x4, int64_t n, int lane,
+                                                         double eps, uint64_t pol_keep) {
+  constexpr int kRB = 4;
+  const int64_t nv = (n + 3) / 4;
+  float d0 = 0.f, d1 = 0.f, s0 = 0.f, s1 = 0.f;
+  for (int64_t q0 = lane; q0 < nv; q0 += 32 * kRB) {
+    float4 av[kRB];
+#pragma unroll
+    for (int u = 0; u < kRB; ++u)
+      av[u] = (q0 + 32 * u < nv) ? ldg_f4_policy(a4 + q0 + 32 * u, pol_keep) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < kRB; ++u) {
+      if (q0 + 32 * u < nv) {
+        const float4 xv = x4[q0 + 32 * u];
+        float& d = (u & 1) ? d1 : d0;
+        float& s = (u & 1) ? s1 : s0;
+        d = fmaf(av[u].x, xv.x, d);
+        d = fmaf(av[u].y, xv.y, d);
+        d = fmaf(av[u].z, xv.z, d);
+        d = fmaf(av[u].w, xv.w, d);
+        s = fmaf(fabsf(av[u].x), fabsf(xv.x), s);
+        s = fmaf(fabsf(av[u].y), fabsf(xv.y), s);
+        s = fmaf(fabsf(av[u].z), fabsf(xv.z), s);
+        s = fmaf(fabsf(av[u].w), fabsf(xv.w), s);
+      }
+    }
+  }
+  float d = d0 + d1, s = s0 + s1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d += __shfl_xor_sync(0xffffffffu, d, o);
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+  }
+  return screen_decide(d, s, nv, eps);
+}
+
 // --------------------------------------------------------------- kernel ----
 // One persistent CTA per SM; warp roles (24 warps, 768 threads):
 //   [0, 8)   consumers   : wait t_j and the column ring, acc += t_j * C[:, ell_j],
@@ -649,6 +764,8 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     }
     const int ttid = tid - kWarpTail * 32, tw = warp - kWarpTail;
     const uint64_t pol_keep = policy_evict_last();
+    // fp32 refinement screening (refine_screen_f32); FSTG_STREAM_DEBUG bit 16 refines every candidate exactly
+    const bool screen = !(A.debug & 16);
     int parity = 0;
     uint32_t rg = 0;  // running index of refinement rows through the ring (all tail threads agree)
     uint32_t lv = 0;
@@ -825,6 +942,19 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
           for (int64_t ci = first; ci < A.want; ci += kRStages) {
             const uint32_t g = rg + static_cast<uint32_t>(ci);
             wp.wait(&r_full[st], (g / kRStages) & 1u, kWTailRFull);
+            if constexpr (sizeof(T) == 4) {
+              if (screen) {
+                // fp32 screening pass; candidates it cannot rule out get the exact dot below
+                const bool maybe = refine_screen_f32(reinterpret_cast<const float4*>(rring + size_t(st) * A.rstride),
+                                                     reinterpret_cast<const float4*>(xs), A.n, lane, A.epsilon);
+                __syncwarp();
+                if (lane == 0) {
+                  mbar_arrive(&r_empty[st]);
+                  cflag[ci] = maybe ? 2 : 0;
+                }
+                continue;
+              }
+            }
             double dot = 0.0, dot2 = 0.0;
             if constexpr (sizeof(T) == 4) {
               const int64_t nv = (A.n + 3) / 4;
@@ -863,6 +993,19 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
           }
         }
         rg += static_cast<uint32_t>(A.want);
+        if constexpr (sizeof(T) == 4) {
+          if (screen) {
+            named_bar_sync(kBarTail, kTL);  // every screening flag is written
+            for (int64_t ci = tw; ci < A.want; ci += kTLW) {
+              if (cflag[ci] != 2) continue;  // warp-uniform
+              const double dot = refine_dot_exact(A.a + int64_t(cand[ci]) * A.lda, xs, A.n, lane, pol_keep);
+              if (lane == 0) {
+                cval[ci] = static_cast<T>(dot);
+                cflag[ci] = fabs(dot) >= A.epsilon ? 1 : 0;
+              }
+            }
+          }
+        }
       } else {
         // rows longer than one stage: direct 16-byte loads from L2
         for (int64_t ci = tw; ci < A.want; ci += kTLW) {
@@ -870,27 +1013,13 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
           const T* arow = A.a + row * A.lda;
           double dot = 0.0, dot2 = 0.0;
           if constexpr (sizeof(T) == 4) {
-            constexpr int kRB = 4;
-            const int64_t nv = (A.n + 3) / 4;
-            const float4* a4 = reinterpret_cast<const float4*>(arow);
-            const float4* x4 = reinterpret_cast<const float4*>(xs);
-            for (int64_t q0 = lane; q0 < nv; q0 += 32 * kRB) {
-              float4 av[kRB];
-#pragma unroll
-              for (int u = 0; u < kRB; ++u)
-                av[u] = (q0 + 32 * u < nv) ? ldg_f4_policy(a4 + q0 + 32 * u, pol_keep) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-              for (int u = 0; u < kRB; ++u) {
-                if (q0 + 32 * u < nv) {
-                  const float4 xv4 = x4[q0 + 32 * u];
-                  double& acc = (u & 1) ? dot2 : dot;
-                  acc = fma(static_cast<double>(av[u].x), static_cast<double>(xv4.x), acc);
-                  acc = fma(static_cast<double>(av[u].y), static_cast<double>(xv4.y), acc);
-                  acc = fma(static_cast<double>(av[u].z), static_cast<double>(xv4.z), acc);
-                  acc = fma(static_cast<double>(av[u].w), static_cast<double>(xv4.w), acc);
-                }
-              }
+            if (screen && !refine_screen_f32_global(reinterpret_cast<const float4*>(arow),
+                                                    reinterpret_cast<const float4*>(xs), A.n, lane, A.epsilon,
+                                                    pol_keep)) {
+              if (lane == 0) cflag[ci] = 0;  // proven |a_i . x| < eps
+              continue;
             }
+            dot = refine_dot_exact(arow, xs, A.n, lane, pol_keep);
           } else {
             constexpr int kRB = 4;
             const int64_t nv = (A.n + 1) / 2;
@@ -911,10 +1040,10 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
                 }
               }
             }
-          }
-          dot += dot2;
+            dot += dot2;
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+            for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+          }
           if (lane == 0) {
             cval[ci] = static_cast<T>(dot);
             cflag[ci] = fabs(dot) >= A.epsilon ? 1 : 0;

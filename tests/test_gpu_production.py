@@ -261,3 +261,39 @@ def test_m16384_fast_nonsplit_vs_oracle(fst, orc):
         np.testing.assert_allclose(g.mu, r.mu, rtol=1e-4, atol=5e-6, err_msg=f"vector {v}")
         assert _support_diff_allowed(g, r, r.mu, a64 @ x, 0.2, want), v
     sk.close()
+
+
+def _with_debug(bits, fn):
+    old = os.environ.get("FSTG_STREAM_DEBUG")
+    os.environ["FSTG_STREAM_DEBUG"] = str(bits)
+    try:
+        return fn()
+    finally:
+        if old is None:
+            os.environ.pop("FSTG_STREAM_DEBUG", None)
+        else:
+            os.environ["FSTG_STREAM_DEBUG"] = old
+
+
+def test_refinement_screening_is_output_invariant(fst, c3):
+    """The fp32 screening pass of the refinement (stream.cu refine_screen_f32) only skips the exact
+    fp64 dot for candidates PROVEN below eps: outputs are bit-identical to refining every candidate
+    exactly (FSTG_STREAM_DEBUG bit 16), including at an eps placed exactly on a refined value."""
+    import torch
+    prob, sk, seeds = c3
+    for eps in (0.1, None):
+        if eps is None:
+            # eps = |a_i . x| (fp64) of a mid-ranked support entry of vector 0: the boundary case
+            out0 = fst.transform_batch(sk, prob.X[:1].contiguous(), fst.StreamParams(epsilon=0.1, s=32, J=375, K=2),
+                                       seeds=seeds[:1].contiguous())
+            i = int(out0.support[0, 5])
+            eps = abs(float(prob.A[i].double() @ prob.X[0].double()))
+        p = fst.StreamParams(epsilon=eps, s=32, J=375, K=2)
+        scr = fst.transform_batch(sk, prob.X, p, seeds=seeds, candidates=True)
+        ref = _with_debug(16, lambda: fst.transform_batch(sk, prob.X, p, seeds=seeds, candidates=True))
+        assert torch.equal(scr.counts, ref.counts)
+        assert torch.equal(scr.candidates, ref.candidates)
+        cnt = ref.counts.cpu().numpy()
+        valid = torch.as_tensor(np.arange(320)[None, :] < cnt[:, None]).cuda()
+        assert torch.equal(scr.support[valid], ref.support[valid])
+        assert torch.equal(scr.values[valid], ref.values[valid])
