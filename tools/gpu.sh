@@ -74,6 +74,7 @@ case "$task" in
     timeout 600 $CMD > gpurun_out/launch_plain.json 2> gpurun_out/launch_plain.err; rc=$?; echo "plain rc=$rc"
     if [ $rc -eq 0 ]; then
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+        -k regex:"fwht|stream_kernel|draw_kernel|identity_kernel|qtable|qtrans|row_norm|narrow" \
         --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
     fi ;;
   ncu)
