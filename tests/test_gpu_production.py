@@ -297,3 +297,28 @@ def test_refinement_screening_is_output_invariant(fst, c3):
         valid = torch.as_tensor(np.arange(320)[None, :] < cnt[:, None]).cuda()
         assert torch.equal(scr.support[valid], ref.support[valid])
         assert torch.equal(scr.values[valid], ref.values[valid])
+
+
+def test_config3_host_buffers_equal_device_path(fst, c3):
+    """The e2e path (host X / seeds / outputs, chunked copies on their own streams, each chunk's
+    D2H deferred behind the next kernel) at config-3 shape: B = 600 host vectors run as chunks of
+    256 + 344 (both >= 148: the persistent kernel), bit-identical to the device path."""
+    import torch
+    prob, sk, seeds = c3
+    p = fst.StreamParams(epsilon=0.1, s=32, J=375, K=2)
+    dev = fst.transform_batch(sk, prob.X, p, seeds=seeds, candidates=True, mu=True)
+    Xh = prob.X.cpu().numpy()
+    host = fst.transform_batch(sk, Xh, p, seeds=prob.seeds, candidates=True, mu=True)
+    counts = dev.counts.cpu().numpy()
+    assert np.array_equal(counts, host.counts)
+    valid = np.arange(320)[None, :] < counts[:, None]
+    assert np.array_equal(dev.support.cpu().numpy()[valid], host.support[valid])
+    assert np.array_equal(dev.values.cpu().numpy()[valid], host.values[valid])
+    assert np.array_equal(dev.candidates.cpu().numpy(), host.candidates)
+    assert np.array_equal(dev.mu.cpu().numpy(), host.mu)
+    # pinned host buffers (the bench's e2e configuration) as well
+    Xp = torch.from_numpy(Xh).pin_memory()
+    sp = torch.from_numpy(prob.seeds.view(np.int64).copy()).pin_memory()
+    pin = fst.transform_batch(sk, Xp, p, seeds=sp)
+    assert np.array_equal(_np(pin.counts), counts)
+    assert np.array_equal(_np(pin.support)[valid], host.support[valid])
