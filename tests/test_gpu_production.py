@@ -322,3 +322,26 @@ def test_config3_host_buffers_equal_device_path(fst, c3):
     pin = fst.transform_batch(sk, Xp, p, seeds=sp)
     assert np.array_equal(_np(pin.counts), counts)
     assert np.array_equal(_np(pin.support)[valid], host.support[valid])
+
+
+@pytest.mark.parametrize("J,K,s,widen", [(250, 1, 4, 10), (125, 3, 4, 10), (60, 5, 3, 100), (375, 2, 30, 10)])
+def test_fp64_strict_nonsplit_k_and_widen_cases(fst, orc, J, K, s, widen):
+    """Persistent-kernel edge cases at B = 320 (every CTA on its 2nd / 3rd vector), n = m = 256 fp64
+    STRICT, every vector bit-exact: K = 1 (no median), odd K = 3 and 5 (order statistic with
+    batch-index ties), widen * s >= m (the candidate set is every row, stream.hpp:245-246)."""
+    n, B = 256, 320
+    a = orc.gen_orthogonal(n, 31337)
+    sk = fst.preprocess(a)
+    ref = orc.preprocess(a)
+    X = np.stack([orc.gen_exact_sparse(a, 8, orc.gen_seed(4000 + v))[0] for v in range(B)])
+    seeds = np.array([orc.stream_seed(4000 + v) for v in range(B)], dtype=np.uint64)
+    p = fst.StreamParams(epsilon=0.1, s=s, J=J, K=K, widen=widen)
+    out = _run_nonsplit(fst, sk, X, p, seeds)
+    for v in range(B):
+        r = orc.transform(ref, X[v], orc.StreamParams(epsilon=0.1, s=s, J=J, K=K, widen=widen, seed=int(seeds[v])))
+        g = out.result(v)
+        assert g.mu.tobytes() == r.mu.tobytes(), v
+        assert g.candidate_set.tolist() == r.candidate_set.tolist(), v
+        assert g.support.tolist() == r.support.tolist(), v
+        np.testing.assert_allclose(g.values, r.values, rtol=1e-12, atol=1e-15)
+    sk.close()
