@@ -345,3 +345,26 @@ def test_fp64_strict_nonsplit_k_and_widen_cases(fst, orc, J, K, s, widen):
         assert g.support.tolist() == r.support.tolist(), v
         np.testing.assert_allclose(g.values, r.values, rtol=1e-12, atol=1e-15)
     sk.close()
+
+
+def test_config3_with_samples_equals_transform_nonsplit(fst, c3):
+    """transform_with_samples (stream.hpp:197-268, caller-supplied indices, device int64 B x N) on
+    the persistent kernel equals transform (stream.hpp:272-275) bit for bit, B = 300."""
+    import torch
+    prob, sk, seeds = c3
+    B = 300
+    p = fst.StreamParams(epsilon=0.1, s=32, J=375, K=2)
+    X = prob.X[:B].contiguous()
+    a = fst.transform_batch(sk, X, p, seeds=seeds[:B].contiguous(), candidates=True, mu=True)
+    idx = torch.from_numpy(fst.draw_samples(sk, p, seeds=prob.seeds[:B])).cuda()
+    fst.profile_enable(True)
+    fst.profile_reset()
+    b = fst.transform_with_samples_batch(sk, X, p, idx, candidates=True, mu=True)
+    assert fst.profile_read("stream")[1] == 1 and fst.profile_read("stream_tail")[1] == 0
+    fst.profile_enable(False)
+    for name in ("counts", "candidates", "mu"):
+        assert torch.equal(getattr(a, name), getattr(b, name)), name
+    cnt = a.counts.cpu().numpy()
+    valid = torch.as_tensor(np.arange(320)[None, :] < cnt[:, None]).cuda()
+    assert torch.equal(a.support[valid], b.support[valid])
+    assert torch.equal(a.values[valid], b.values[valid])
