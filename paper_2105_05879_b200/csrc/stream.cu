@@ -17,7 +17,9 @@
 //     smaller index by an MSB radix select plus an index-ordered ballot scan
 //     (stream.hpp:245-257), the exact fp64-accumulated refinement of those rows
 //     of A through a TMA row ring (A L2-resident, evict-last; stream.hpp:259-266)
-//     and the ordered compaction of the |v| >= eps support.
+//     — in fp32 preceded by a screening pass with a rigorous rounding bound, so
+//     only candidates not proven below eps pay for the exact dot — and the
+//     ordered compaction of the |v| >= eps support.
 // STRICT mode reproduces the reference's operation order exactly: Gray-code
 // sequential coefficient sums and separately-rounded multiply/add.
 #include <cuda_runtime.h>
@@ -909,7 +911,8 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
       }
       named_bar_sync(kBarTail, kTL);
 
-      // ---- refinement: v_i = a_i . x, fp64 accumulation (stream.hpp:259-266) ----
+      // ---- refinement: v_i = a_i . x, fp64 accumulation (stream.hpp:259-266); fp32 rows are
+      //      screened first (refine_screen_f32) and only the unresolved ones refined exactly ----
       wp.wait(&x_full[xb], xu & 1u, kWTailXFull);
       const T* xs = xbuf + xb * dx;
       if (A.debug & 4) {
