@@ -118,6 +118,11 @@ def spread_vectors(B, sms=148, extra=8, seed=0):
     return sorted(ids)
 
 
+def torch_float32():
+    import torch
+    return torch.float32
+
+
 def parity_check(fst, sk, A, X, seeds, out, J, K, s_val, eps_val, strict, nvec=32):
     """After timing: outputs of the timed batch for >= nvec spread vectors against the oracle's
     draw_and_gather transform (stream.hpp:184-191, 197-268) on the GPU's own gathered columns,
@@ -134,15 +139,23 @@ def parity_check(fst, sk, A, X, seeds, out, J, K, s_val, eps_val, strict, nvec=3
     sup, vals = out.support.cpu().numpy(), out.values.cpu().numpy()
     seeds_np = np.asarray(seeds, dtype=np.uint64)
     idx = fst.draw_samples(sk, p, seeds=seeds_np[ids])
-    draws_ok = exact = allowed = 0
+    draws_ok = exact = allowed = bit_exact = 0
     max_rel = 0.0
     failures = []
+    fast = not strict and X.dtype == torch_float32()
     for q, v in enumerate(ids):
         op = orc.StreamParams(epsilon=eps_val, s=s_val, J=J, K=K, widen=WIDEN, seed=int(seeds_np[v]))
         ref_idx = orc.draw_samples(sk.L, op)
         draws_ok += int(np.array_equal(idx[q], ref_idx))
         x = X[v].double().cpu().numpy()
-        r = orc.transform_gathered(a64, x, op, ref_idx, sk.gather(ref_idx).astype(np.float64))
+        cols = sk.gather(ref_idx)
+        if fast:
+            # bit for bit against the CPU restatement of the FAST kernels' own summation orders
+            rk = orc.transform_gathered_fast_order(A.cpu().numpy(), X[v].cpu().numpy(), op, ref_idx, cols)
+            c = int(counts[v])
+            bit_exact += int(sup[v, :c].tolist() == rk.support.tolist()
+                             and vals[v, :c].tobytes() == rk.values.tobytes())
+        r = orc.transform_gathered(a64, x, op, ref_idx, cols.astype(np.float64))
         g_sup = sup[v, :counts[v]].tolist()
         g_val = vals[v, :counts[v]].astype(np.float64)
         ri = dict(zip(r.support.tolist(), r.values))
@@ -163,12 +176,14 @@ def parity_check(fst, sk, A, X, seeds, out, J, K, s_val, eps_val, strict, nvec=3
         if not ok:
             failures.append(v)
     tol = 1e-12 if strict else 1e-5
-    ok = draws_ok == len(ids) and not failures and max_rel <= tol
+    ok = draws_ok == len(ids) and not failures and max_rel <= tol and (not fast or bit_exact == len(ids))
     return {"status": "ok" if ok else "FAIL", "vectors_checked": len(ids), "vector_ids": ids,
             "draws_bit_exact": draws_ok, "support_identical": exact, "support_diff_allowed": allowed,
             "failures": failures, "max_value_rel_err": max_rel, "value_tol": tol,
+            "kernel_order_bit_exact": bit_exact if fast else None,
             "oracle": "oracle.transform_gathered (fp64 restatement of stream.hpp:197-268) on the GPU's gathered "
-                      "columns; inputs = the GPU's exact A and x"}
+                      "columns; inputs = the GPU's exact A and x. fp32 FAST: supports and values also bit-exact "
+                      "against oracle.transform_gathered_fast_order (the kernels' summation orders restated)"}
 
 
 # ------------------------------------------------------------- clocks ----
@@ -489,7 +504,8 @@ def run_b200(args):
         parity = parity_check(fst, sk, prob.A, X, prob.seeds, out, args.J, args.K, s_val, eps_val, strict)
         print(f"[bench] rank {rank}: parity {parity['status']} ({parity['vectors_checked']} vectors of the timed "
               f"batch vs the oracle, support identical {parity['support_identical']}, "
-              f"max value rel err {parity['max_value_rel_err']:.2e})", file=sys.stderr, flush=True)
+              f"max value rel err {parity['max_value_rel_err']:.2e}, bit-exact vs the kernel-order "
+              f"restatement {parity['kernel_order_bit_exact']})", file=sys.stderr, flush=True)
 
     # ---- CPU baseline (rank 0, N = 1) ----
     cpu = None

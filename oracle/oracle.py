@@ -425,6 +425,32 @@ def transform_gathered(a, x, p: StreamParams, indices, gathered, dtype=np.float6
     return TransformResult(sup[:k].copy(), vals[:k].copy(), cand, mu, p.J * p.K)
 
 
+def transform_gathered_fast_order(a, x, p: StreamParams, indices, gathered) -> TransformResult:
+    """The B200 FAST-mode arithmetic restated (lane-partitioned coefficient sums + xor tree, FMA
+    accumulation, the refinement's chunked fp64 dot), float32: bit-exact reference for the GPU's
+    fp32 FAST path. Same transform as transform_gathered(..., float32) up to summation order."""
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    m, n = a.shape
+    indices = np.ascontiguousarray(indices, dtype=np.int64)
+    gathered = np.ascontiguousarray(gathered, dtype=np.float32)
+    if gathered.shape != (p.J * p.K, m):
+        raise ValueError("gathered must be (J*K, m)")
+    want = candidate_count(p.s, p.widen, m)
+    mu = np.zeros(m, dtype=np.float32)
+    cand = np.zeros(want, dtype=np.int64)
+    sup = np.zeros(want, dtype=np.int64)
+    vals = np.zeros(want, dtype=np.float32)
+    ns = C.c_int64()
+    _check(lib().orc_transform_gathered_fast_order(_ptr(a), C.c_int64(m), C.c_int64(n), _ptr(x),
+                                                   C.c_double(p.epsilon), C.c_double(p.delta), C.c_int64(p.s),
+                                                   C.c_int64(p.J), C.c_int64(p.K), C.c_int64(p.widen),
+                                                   _ptr(indices), _ptr(gathered), _ptr(mu), _ptr(cand), _ptr(sup),
+                                                   _ptr(vals), C.byref(ns)))
+    k = ns.value
+    return TransformResult(sup[:k].copy(), vals[:k].copy(), cand, mu, p.J * p.K)
+
+
 def kerdock_block(a, s: int, dtype=np.float64) -> np.ndarray:
     """Kerdock basis s of preprocess(a) (sketch.hpp:171-196): (d, m), row w = column s*d + w."""
     a = np.ascontiguousarray(a, dtype=dtype)

@@ -3,6 +3,7 @@
 // Status codes mirror the reference's exception classes:
 //   0 ok, 1 std::invalid_argument, 2 std::out_of_range, 3 std::overflow_error,
 //   4 std::runtime_error, 5 std::logic_error / other.
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
@@ -359,6 +360,127 @@ static void transform_gathered_out(const T* a, std::int64_t m, std::int64_t n, c
   *nsupport = static_cast<std::int64_t>(r.support.size());
 }
 
+// ---------------------------------------------------------------------------
+// The B200 FAST-mode arithmetic, restated (test infrastructure): the same
+// transform as transform_gathered<float> (stream.hpp:197-268) with the
+// summation orders of the sm_100a kernels instead of the reference's, so the
+// fp32 FAST path can be checked bit for bit rather than to a tolerance:
+//  * coefficient t = s_ell^T x (stream.cu coeff_fast_multi, d >= 128): lane l
+//    of a warp sums +-x[128 i + 4 l + e] for i ascending, e = 0..3 (positions
+//    >= n read as 0), then the 32 lane sums are combined by the xor butterfly
+//    (offsets 16, 8, 4, 2, 1); d < 128 (coeff_generic): lane l sums positions
+//    l + 32 r. Identity indices: float(sqrt(d)) * x[pos].
+//  * accumulation: acc = fmaf(t, C[i, ell], acc) per element in j order (FAST
+//    uses FMA), batch mean acc / J, median as the reference (stream.hpp:126-143).
+//  * candidate rule and threshold as the reference (stream.hpp:245-266);
+//    refined value (stream.cu refine_dot_exact): exact products in fp64, lane l
+//    accumulating 4-element chunks q = l + 32 i into two chains by i parity,
+//    chains added, xor butterfly; stored as float, |v| >= eps tested in double.
+static float lane_tree_f(float (&a)[32]) {
+  for (int o = 16; o > 0; o >>= 1) {
+    float b[32];
+    for (int l = 0; l < 32; ++l) b[l] = a[l] + a[l ^ o];
+    std::memcpy(a, b, sizeof(b));
+  }
+  return a[0];
+}
+static double lane_tree_d(double (&a)[32]) {
+  for (int o = 16; o > 0; o >>= 1) {
+    double b[32];
+    for (int l = 0; l < 32; ++l) b[l] = a[l] + a[l ^ o];
+    std::memcpy(a, b, sizeof(b));
+  }
+  return a[0];
+}
+
+static void transform_gathered_fast_order(const float* a, std::int64_t m, std::int64_t n, const float* x,
+                                          const StreamParams& p, const std::int64_t* indices, const float* gathered,
+                                          float* mu_out, std::int64_t* cand_out, std::int64_t* support_out,
+                                          float* values_out, std::int64_t* nsupport) {
+  p.validate();
+  const DesignParams design = DesignParams::make(even_log2_ceil(n));
+  const std::int64_t d = design.d, kb = design.kerdock_bases() * d, N = p.J * p.K;
+  std::vector<float> xs(static_cast<std::size_t>(d), 0.f);
+  for (std::int64_t i = 0; i < n; ++i) xs[i] = x[i];
+  std::vector<std::uint8_t> q(static_cast<std::size_t>(d));
+  std::int64_t cached = -1;
+  std::vector<float> means(static_cast<std::size_t>(m * p.K), 0.f);
+  for (std::int64_t jj = 0; jj < N; ++jj) {
+    const std::int64_t ell = indices[jj];
+    if (ell < 0 || ell >= design.L) throw std::out_of_range("Sketch::column: index out of range");
+    float t;
+    if (ell >= kb) {
+      const std::int64_t pos = ell - kb;
+      t = pos < n ? static_cast<float>(std::sqrt(static_cast<double>(d))) * xs[pos] : 0.f;
+    } else {
+      const std::int64_t s = ell / d;
+      const std::uint64_t w = static_cast<std::uint64_t>(ell % d);
+      if (s != cached) {
+        const auto mat = kerdock_matrix(design, static_cast<std::uint64_t>(s));
+        for (std::int64_t pos = 0; pos < d; ++pos)
+          q[pos] = static_cast<std::uint8_t>(
+              quadratic_form(mat.data(), design.k, coords_of_position(static_cast<std::uint64_t>(pos), design.k)));
+        cached = s;
+      }
+      auto term = [&](std::int64_t pos) {
+        const bool neg = (q[pos] ^ (__builtin_popcountll(w & static_cast<std::uint64_t>(pos)) & 1)) != 0;
+        return neg ? -xs[pos] : xs[pos];
+      };
+      float lanes[32];
+      for (int l = 0; l < 32; ++l) {
+        float acc = 0.f;
+        if (d >= 128) {
+          for (std::int64_t i = 0; i < d / 128; ++i)
+            for (int e = 0; e < 4; ++e) acc += term(128 * i + 4 * l + e);
+        } else {
+          for (std::int64_t pos = l; pos < d; pos += 32) acc += term(pos);
+        }
+        lanes[l] = acc;
+      }
+      t = lane_tree_f(lanes);
+    }
+    float* col_sum = means.data() + (jj / p.J) * m;
+    const float* col = gathered + jj * m;
+    for (std::int64_t i = 0; i < m; ++i) col_sum[i] = std::fmaf(t, col[i], col_sum[i]);
+  }
+  for (auto& v : means) v /= static_cast<float>(p.J);
+  const std::vector<float> mu = median_of_batch_means(means.data(), m, p.K);
+  std::memcpy(mu_out, mu.data(), sizeof(float) * static_cast<std::size_t>(m));
+  const std::int64_t want = candidate_count(p.s, p.widen, m);
+  std::vector<std::int64_t> order(static_cast<std::size_t>(m));
+  for (std::int64_t i = 0; i < m; ++i) order[i] = i;
+  std::nth_element(order.begin(), order.begin() + want, order.end(), [&mu](std::int64_t u, std::int64_t v) {
+    const float a = std::fabs(mu[u]), b = std::fabs(mu[v]);
+    return a != b ? a > b : u < v;
+  });
+  std::sort(order.begin(), order.begin() + want);
+  std::int64_t ns = 0;
+  for (std::int64_t c = 0; c < want; ++c) {
+    const std::int64_t i = order[c];
+    cand_out[c] = i;
+    const std::int64_t nv = (n + 3) / 4;
+    double lanes[32];
+    for (int l = 0; l < 32; ++l) {
+      double chain[2] = {0.0, 0.0};
+      for (std::int64_t qq = l, it = 0; qq < nv; qq += 32, ++it)
+        for (int e = 0; e < 4; ++e) {
+          const std::int64_t pos = 4 * qq + e;
+          const double av = pos < n ? static_cast<double>(a[i * n + pos]) : 0.0;
+          const double xv = static_cast<double>(xs[pos < d ? pos : 0]) * (pos < n ? 1.0 : 0.0);
+          chain[it & 1] = std::fma(av, xv, chain[it & 1]);
+        }
+      lanes[l] = chain[0] + chain[1];
+    }
+    const double v = lane_tree_d(lanes);
+    if (std::fabs(v) >= p.epsilon) {
+      support_out[ns] = i;
+      values_out[ns] = static_cast<float>(v);
+      ++ns;
+    }
+  }
+  *nsupport = ns;
+}
+
 extern "C" {
 
 int orc_transform_gathered(const double* a, std::int64_t m, std::int64_t n, const double* x, double eps,
@@ -382,6 +504,18 @@ int orc_transform_gathered_f32(const float* a, std::int64_t m, std::int64_t n, c
   return guarded([&] {
     transform_gathered_out<float>(a, m, n, x, make_params(eps, delta, s, J, K, widen, 0), indices, gathered,
                                   mu_out, cand_out, support_out, values_out, nsupport);
+  });
+}
+
+// transform_gathered run in the B200 FAST-mode summation orders (float).
+int orc_transform_gathered_fast_order(const float* a, std::int64_t m, std::int64_t n, const float* x, double eps,
+                                      double delta, std::int64_t s, std::int64_t J, std::int64_t K, std::int64_t widen,
+                                      const std::int64_t* indices, const float* gathered, float* mu_out,
+                                      std::int64_t* cand_out, std::int64_t* support_out, float* values_out,
+                                      std::int64_t* nsupport) {
+  return guarded([&] {
+    transform_gathered_fast_order(a, m, n, x, make_params(eps, delta, s, J, K, widen, 0), indices, gathered, mu_out,
+                                  cand_out, support_out, values_out, nsupport);
   });
 }
 

@@ -368,3 +368,49 @@ def test_config3_with_samples_equals_transform_nonsplit(fst, c3):
     valid = torch.as_tensor(np.arange(320)[None, :] < cnt[:, None]).cuda()
     assert torch.equal(a.support[valid], b.support[valid])
     assert torch.equal(a.values[valid], b.values[valid])
+
+
+def _check_kernel_order(orc, sk, a32, X, idx, p_or, ids, out):
+    """Every checked vector bit-exact against oracle.transform_gathered_fast_order (the FAST
+    kernels' summation orders restated on the CPU) on the GPU's own gathered columns."""
+    mu, cand = _np(out.mu), _np(out.candidates)
+    counts, sup, vals = _np(out.counts), _np(out.support), _np(out.values)
+    for v in ids:
+        gathered = sk.gather(idx[v])[:, :sk.m]
+        r = orc.transform_gathered_fast_order(a32, X[v], p_or, idx[v], gathered)
+        assert mu[v].tobytes() == r.mu.tobytes(), v
+        assert cand[v].tolist() == r.candidate_set.tolist(), v
+        assert sup[v, :counts[v]].tolist() == r.support.tolist(), v
+        assert vals[v, :counts[v]].tobytes() == r.values.tobytes(), v
+
+
+def test_config3_fast_bit_exact_vs_kernel_order_restatement(fst, orc, c3):
+    """The headline instantiation (fp32 FAST, n = m = 4096, persistent kernel, B = 600) bit for bit
+    — mu, candidates, support, values — against a CPU restatement of its own arithmetic order
+    (the tolerance-based comparison with the reference's order is test_config3_fast_nonsplit_vs_oracle)."""
+    prob, sk, seeds = c3
+    p = fst.StreamParams(epsilon=0.1, s=32, J=375, K=2)
+    out = _run_nonsplit(fst, sk, prob.X, p, seeds)
+    idx = fst.draw_samples(sk, p, seeds=prob.seeds)
+    _check_kernel_order(orc, sk, prob.A.cpu().numpy(), prob.X.cpu().numpy(), idx,
+                        orc.StreamParams(epsilon=0.1, s=32, J=375, K=2), _spread(600, extra=14), out)
+
+
+@pytest.mark.parametrize("m,n,s,K", [(1024, 1024, 16, 2), (200, 64, 4, 3), (16384, 256, 16, 2), (6000, 500, 8, 1)])
+def test_fast_bit_exact_vs_kernel_order_shapes(fst, orc, m, n, s, K):
+    """FAST mode bit-exact on the persistent kernel (B = 300) for the small-column variant
+    (m <= 1024), the generic coefficient path (d < 128), 4-segment columns (m = 16384) and a
+    non-power-of-two n with K = 1."""
+    B = 300
+    rng = np.random.default_rng(m + n)
+    a32 = (rng.standard_normal((m, n)) / np.sqrt(n)).astype(np.float32)
+    sk = fst.preprocess(a32)
+    X = rng.standard_normal((B, n))
+    X = (X / np.linalg.norm(X, axis=1, keepdims=True)).astype(np.float32)
+    seeds = np.array([orc.stream_seed(11000 + v) for v in range(B)], dtype=np.uint64)
+    J = 750 // K
+    p = fst.StreamParams(epsilon=0.15, s=s, J=J, K=K)
+    out = _run_nonsplit(fst, sk, X, p, seeds)
+    idx = fst.draw_samples(sk, p, seeds=seeds)
+    _check_kernel_order(orc, sk, a32, X, idx, orc.StreamParams(epsilon=0.15, s=s, J=J, K=K), _spread(B, extra=6), out)
+    sk.close()

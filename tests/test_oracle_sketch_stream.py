@@ -302,3 +302,27 @@ def test_gathered_transform_and_block_match_full_sketch(orc, dtype):
         assert r1.candidate_set.tolist() == r2.candidate_set.tolist()
         assert r1.support.tolist() == r2.support.tolist()
         assert r1.values.tobytes() == r2.values.tobytes()
+
+
+def test_fast_order_restatement_matches_reference_order(orc):
+    """oracle.transform_gathered_fast_order (the B200 FAST kernels' summation orders) computes the
+    same transform as the reference order run in float, up to rounding: mu within 1e-5 of the
+    estimate's scale, identical candidate sets and supports on well-separated inputs; and it is
+    deterministic (bit-identical on repeat)."""
+    rng = np.random.default_rng(21)
+    for n, m in ((256, 40), (64, 30), (1000, 50)):
+        a = (rng.standard_normal((m, n)) / np.sqrt(n)).astype(np.float32)
+        sk = orc.preprocess(a, dtype=np.float32)
+        cols = sk.columns()
+        x = np.zeros(n, dtype=np.float32)
+        x[:3] = [0.8, -0.5, 0.3]
+        x = (a.T @ (np.eye(m, dtype=np.float32)[:, 0] * 3.0) + 0.01 * x).astype(np.float32)
+        p = _params(orc, epsilon=0.5, s=2, J=200, K=3, seed=5)
+        idx = orc.draw_samples(sk.L, p)
+        r1 = orc.transform_gathered(a, x, p, idx, cols[idx], dtype=np.float32)
+        r2 = orc.transform_gathered_fast_order(a, x, p, idx, cols[idx])
+        r3 = orc.transform_gathered_fast_order(a, x, p, idx, cols[idx])
+        assert r2.mu.tobytes() == r3.mu.tobytes()
+        np.testing.assert_allclose(r2.mu, r1.mu, rtol=1e-4, atol=1e-5 * np.max(np.abs(r1.mu)))
+        assert r2.support.tolist() == r1.support.tolist()
+        np.testing.assert_allclose(r2.values, r1.values, rtol=1e-5)
