@@ -326,3 +326,53 @@ def test_retain_cluster_partial_means_row_offsets(fst):
     off = _with_cluster(0, run)
     for cl in (4, 8):
         assert torch.equal(_with_cluster(cl, run), off), cl
+
+
+def test_config4_retained_columns_bit_exact(fst, orc):
+    """n = 16384 (k = 14, the 8.8 TB design): every retained value of the warp-specialised,
+    cluster-merged retain kernel is bit-identical to the float restatement of the reference's
+    per-basis block (oracle.kerdock_block, sketch.hpp:171-196) — not just within 2e-5 of A s_ell."""
+    n, m, d = 16384, 40, 16384
+    rng = np.random.default_rng(14)
+    a32 = (rng.standard_normal((m, n)) / np.sqrt(n)).astype(np.float32)
+    des = fst.preprocess_design(a32)
+    bases = [0, 1, 77, 4095, 4096, 8191]
+    ells = [int(s) * d + int(w) for s in bases for w in rng.integers(0, d, size=4)]
+    ells += [des.L - 1, des.L - d + 5]                          # identity block
+    got = fst.sample_columns(des, np.array(ells, dtype=np.int64))[:, :m]
+    blocks = {s: orc.kerdock_block(a32, s, np.float32) for s in bases}
+    for j, ell in enumerate(ells):
+        if ell < des.kerdock_bases() * d:
+            ref = blocks[ell // d][ell % d]
+        else:
+            w = ell - des.kerdock_bases() * d
+            ref = (np.float32(128.0) * a32[:, w]) if w < n else np.zeros(m, np.float32)
+        assert got[j].tobytes() == ref.tobytes(), ell
+
+
+def test_config4_design_transform_bit_exact_vs_kernel_order(fst, orc):
+    """The config-4 transform (row-blocked design path: retain-sampled FWHT rows + PARTIAL batch
+    means, then TAIL) at n = 16384 bit-exact, vector by vector, against the FAST kernels'
+    restated arithmetic on the retained columns."""
+    import torch
+    n, m, B = 16384, 48, 160
+    rng = np.random.default_rng(41)
+    a32 = (rng.standard_normal((m, n)) / np.sqrt(n)).astype(np.float32)
+    des = fst.preprocess_design(a32)
+    X = rng.standard_normal((B, n))
+    X = (X / np.linalg.norm(X, axis=1, keepdims=True)).astype(np.float32)
+    seeds = np.array([orc.stream_seed(13000 + v) for v in range(B)], dtype=np.uint64)
+    p = fst.StreamParams(epsilon=0.02, s=2, J=60, K=2)
+    Xd = torch.from_numpy(X).cuda()
+    out = fst.transform_design_batch(des, Xd, p, seeds=seeds, row_block=16, candidates=True, mu=True)
+    idx = fst.draw_samples(des, p, seeds=seeds)
+    mu, cand = out.mu.cpu().numpy(), out.candidates.cpu().numpy()
+    counts, sup, vals = out.counts.cpu().numpy(), out.support.cpu().numpy(), out.values.cpu().numpy()
+    for v in (0, 1, 79, 147, 148, 159):
+        cols = fst.sample_columns(des, idx[v])[:, :m]
+        r = orc.transform_gathered_fast_order(a32, X[v], orc.StreamParams(epsilon=0.02, s=2, J=60, K=2), idx[v],
+                                              cols)
+        assert mu[v].tobytes() == r.mu.tobytes(), v
+        assert cand[v].tolist() == r.candidate_set.tolist(), v
+        assert sup[v, :counts[v]].tolist() == r.support.tolist(), v
+        assert vals[v, :counts[v]].tobytes() == r.values.tobytes(), v
