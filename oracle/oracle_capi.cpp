@@ -366,10 +366,12 @@ static void transform_gathered_out(const T* a, std::int64_t m, std::int64_t n, c
 // summation orders of the sm_100a kernels instead of the reference's, so the
 // fp32 FAST path can be checked bit for bit rather than to a tolerance:
 //  * coefficient t = s_ell^T x (stream.cu coeff_fast_multi, d >= 128): lane l
-//    of a warp sums +-x[128 i + 4 l + e] for i ascending, e = 0..3 (positions
-//    >= n read as 0), then the 32 lane sums are combined by the xor butterfly
-//    (offsets 16, 8, 4, 2, 1); d < 128 (coeff_generic): lane l sums positions
-//    l + 32 r. Identity indices: float(sqrt(d)) * x[pos].
+//    of a warp visits x[128 i + 4 l + e] for i ascending, e = 0..3 (positions
+//    >= n read as 0), summing all of them into tot and the negatively signed
+//    ones into neg; its partial is fmaf(-2, neg, tot); the 32 lane partials are
+//    combined by the xor butterfly (offsets 16, 8, 4, 2, 1). d < 128
+//    (coeff_generic): lane l sums +-x[l + 32 r]. Identity indices:
+//    float(sqrt(d)) * x[pos].
 //  * accumulation: acc = fmaf(t, C[i, ell], acc) per element in j order (FAST
 //    uses FMA), batch mean acc / J, median as the reference (stream.hpp:126-143).
 //  * candidate rule and threshold as the reference (stream.hpp:245-266);
@@ -422,16 +424,22 @@ static void transform_gathered_fast_order(const float* a, std::int64_t m, std::i
               quadratic_form(mat.data(), design.k, coords_of_position(static_cast<std::uint64_t>(pos), design.k)));
         cached = s;
       }
-      auto term = [&](std::int64_t pos) {
-        const bool neg = (q[pos] ^ (__builtin_popcountll(w & static_cast<std::uint64_t>(pos)) & 1)) != 0;
-        return neg ? -xs[pos] : xs[pos];
+      auto negbit = [&](std::int64_t pos) {
+        return (q[pos] ^ (__builtin_popcountll(w & static_cast<std::uint64_t>(pos)) & 1)) != 0;
       };
+      auto term = [&](std::int64_t pos) { return negbit(pos) ? -xs[pos] : xs[pos]; };
       float lanes[32];
       for (int l = 0; l < 32; ++l) {
         float acc = 0.f;
         if (d >= 128) {
+          float tot = 0.f, neg = 0.f;
           for (std::int64_t i = 0; i < d / 128; ++i)
-            for (int e = 0; e < 4; ++e) acc += term(128 * i + 4 * l + e);
+            for (int e = 0; e < 4; ++e) {
+              const std::int64_t pos = 128 * i + 4 * l + e;
+              tot += xs[pos];
+              if (negbit(pos)) neg += xs[pos];
+            }
+          acc = std::fmaf(-2.f, neg, tot);
         } else {
           for (std::int64_t pos = l; pos < d; pos += 32) acc += term(pos);
         }

@@ -216,53 +216,8 @@ __device__ __forceinline__ uint32_t group_scan(uint32_t v, uint32_t* scan_smem, 
 }
 
 // ------------------------------------------------ sample coefficients ----
-// Fast path (d >= 128): lane owns positions 128 i + 4 lane + e; the sign of
-// x[pos] in s_ell is Q_s(pos) ^ parity(w & pos) (kerdock.hpp:132-152).
-template <typename T>
-__device__ __forceinline__ T coeff_fast(const StreamArgs<T>& A, const T* xs, const uint32_t* wbase, uint32_t ell,
-                                        int lane) {
-  if (static_cast<int64_t>(ell) >= A.kb) {
-    const int64_t pos = static_cast<int64_t>(ell) - A.kb;
-    return pos < A.n ? static_cast<T>(sqrt(static_cast<double>(A.d))) * xs[pos] : T(0);
-  }
-  const uint32_t s = ell >> A.k, w = ell & static_cast<uint32_t>(A.d - 1);
-  const uint32_t wlo = w & 3u, wmid = (w >> 2) & 31u, whi = w >> 7;
-  const uint32_t lanebit = __popc(wmid & static_cast<uint32_t>(lane)) & 1u;
-  const uint32_t base = wbase[((whi & 7u) << 2) | wlo];
-  const int64_t rows128 = A.d / 128;  // i in [0, d/128)
-  const int tw = static_cast<int>(A.d >= 1024 ? A.d / 1024 : 1);
-  const uint32_t* q = A.qtrans + (static_cast<int64_t>(s) * tw) * 32 + lane;
-  T acc = T(0);
-  for (int t = 0; t < tw; ++t) {
-    const uint32_t hiflip = __popc(whi & (8u * t)) & 1u;
-    const uint32_t M = __ldg(q + t * 32) ^ base ^ ((hiflip ^ lanebit) ? 0xffffffffu : 0u);
-#pragma unroll
-    for (int ip = 0; ip < 8; ++ip) {
-      const int64_t i = 8 * t + ip;
-      if (i < rows128) {
-        const T* xp = xs + 128 * i + 4 * lane;
-        if constexpr (sizeof(T) == 4) {
-          const float4 xv = *reinterpret_cast<const float4*>(xp);
-          acc += __uint_as_float(__float_as_uint(xv.x) ^ ((M << (31 - (4 * ip + 0))) & 0x80000000u));
-          acc += __uint_as_float(__float_as_uint(xv.y) ^ ((M << (31 - (4 * ip + 1))) & 0x80000000u));
-          acc += __uint_as_float(__float_as_uint(xv.z) ^ ((M << (31 - (4 * ip + 2))) & 0x80000000u));
-          acc += __uint_as_float(__float_as_uint(xv.w) ^ ((M << (31 - (4 * ip + 3))) & 0x80000000u));
-        } else {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const T xvv = xp[e];
-            acc += ((M >> (4 * ip + e)) & 1u) ? -xvv : xvv;
-          }
-        }
-      }
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  return acc;
-}
-
-// Fast path for NS samples at once (d >= 128): the x loads are shared by the
+// Fast path (d >= 128), NS samples at once: lane owns positions 128 i + 4 lane + e; the sign of
+// x[pos] in s_ell is Q_s(pos) ^ parity(w & pos) (kerdock.hpp:132-152). The x loads are shared by the
 // NS samples and the NS accumulation chains are independent, so one warp keeps
 // NS sign-table loads and NS FADD chains in flight. ells[k] >= kb (identity
 // block) are handled by the caller.
@@ -290,6 +245,10 @@ __device__ __forceinline__ void coeff_fast_multi(const StreamArgs<T>& A, const T
   T acc[NS];
 #pragma unroll
   for (int k = 0; k < NS; ++k) acc[k] = T(0);
+  // fp32: acc[k] collects the entries whose sign bit is set (one predicated FADD per entry and
+  // sample: LOP3.P + @P FADD, instead of shift + sign-XOR + FADD) and tot all entries, shared by
+  // the NS samples; the lane's partial is tot - 2 acc[k] (2 acc exact: one rounding)
+  T tot = T(0);
   for (int t0 = 0; t0 < tw; t0 += TWC) {
     uint32_t raw[TWC][NS];
 #pragma unroll
@@ -313,13 +272,18 @@ __device__ __forceinline__ void coeff_fast_multi(const StreamArgs<T>& A, const T
             const T* xp = xs + 128 * i + 4 * lane;
             if constexpr (sizeof(T) == 4) {
               const float4 xv = *reinterpret_cast<const float4*>(xp);
-              const uint32_t xb[4] = {__float_as_uint(xv.x), __float_as_uint(xv.y), __float_as_uint(xv.z),
-                                      __float_as_uint(xv.w)};
+              const float xe[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
+              for (int e = 0; e < 4; ++e) {
+                tot += xe[e];
 #pragma unroll
-                for (int k = 0; k < NS; ++k)
-                  acc[k] += __uint_as_float(xb[e] ^ ((M[k] << (31 - (4 * ip + e))) & 0x80000000u));
+                for (int k = 0; k < NS; ++k) {
+                  asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\tand.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t"
+                      "@p add.f32 %0, %0, %1;\n\t}"
+                      : "+f"(acc[k])
+                      : "f"(xe[e]), "r"(M[k]), "r"(1u << (4 * ip + e)));
+                }
+              }
             } else {
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
@@ -332,6 +296,10 @@ __device__ __forceinline__ void coeff_fast_multi(const StreamArgs<T>& A, const T
         }
       }
     }
+  }
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int k = 0; k < NS; ++k) acc[k] = fmaf(-2.f, acc[k], tot);
   }
 #pragma unroll
   for (int k = 0; k < NS; ++k) {
