@@ -56,6 +56,9 @@ constexpr int kTRing = FSTG_TRING;          // slots of the coefficient ring
 #define FSTG_NS 8
 #endif
 constexpr int kNS = FSTG_NS;
+#ifndef FSTG_CONS_PIPE
+#define FSTG_CONS_PIPE 0
+#endif
 constexpr int kSegBytes = 16384;            // one ring stage at most
 // samples per consumer iteration for small columns: FAST mode (config 2, fp32 m = 1024:
 // 3 / 4 / 5 / 6 -> 1.12M / 1.21M / 1.25M / 1.28M vectors/s) and STRICT mode (config 1, fp64
@@ -1087,6 +1090,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
       }
     };
     int64_t jb = 0, b = split ? w % A.K : 0;  // position inside the batch, batch index
+    const bool cons_fast = (A.debug & 3) == 0 && seg_last_rows == SEG;
     uint32_t tslot = static_cast<uint32_t>(g0 % kTRing), tphase = static_cast<uint32_t>((g0 / kTRing) & 1);
     for (int64_t j = 0; j < NI;) {
       bool grouped = false;
@@ -1141,6 +1145,39 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
           }
           j += CG;
           jb += CG - 1;  // + 1 below
+          grouped = true;
+        }
+      }
+      if constexpr (NSEG == 1 && !SMALL) {
+        if (!grouped && cons_fast) {
+          // one full-height segment per sample, every chunk in range (config 3): the loads first,
+          // the stage and the coefficient slot released before the FMAs use the loaded values
+          wp.wait(&t_full[tslot], tphase, kWConsT);
+          const T t = tring[tslot];
+          wp.wait(&full[stage], phase, kWConsCol);
+          const typename Vec<T>::V* src =
+              reinterpret_cast<const typename Vec<T>::V*>(ring + size_t(stage) * A.stage_stride);
+          T vv[CPT][VEC];
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) Vec<T>::get(src[tid + c * kNC], vv[c]);
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&empty[stage]);
+            mbar_arrive(&t_empty[tslot]);
+          }
+#pragma unroll
+          for (int c = 0; c < CPT; ++c)
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) accumulate(acc[0][c][e], t, vv[c][e]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
+          }
+          if (++tslot == kTRing) {
+            tslot = 0;
+            tphase ^= 1u;
+          }
+          ++j;
           grouped = true;
         }
       }
