@@ -56,9 +56,6 @@ constexpr int kTRing = FSTG_TRING;          // slots of the coefficient ring
 #define FSTG_NS 8
 #endif
 constexpr int kNS = FSTG_NS;
-#ifndef FSTG_CONS_PIPE
-#define FSTG_CONS_PIPE 0
-#endif
 constexpr int kSegBytes = 16384;            // one ring stage at most
 // samples per consumer iteration for small columns: FAST mode (config 2, fp32 m = 1024:
 // 3 / 4 / 5 / 6 -> 1.12M / 1.21M / 1.25M / 1.28M vectors/s) and STRICT mode (config 1, fp64
