@@ -99,6 +99,7 @@ struct StreamArgs {
   int stages;
   int stage_stride;  // bytes between ring stages (>= one segment, 128-byte multiple)
   int rstride;       // bytes per refinement-ring stage (one row of A); 0 = direct loads
+  int rstages;       // refinement-ring stages in use (<= kRStages), set by stream_grid_size
   int xbufs;         // x buffers in shared memory
   int nseg;
   int chunk;
@@ -130,7 +131,7 @@ template <typename T>
 int64_t stream_scratch_elems(const StreamArgs<T>& args, int grid);
 // Persistent grid size the stream kernel wants for this configuration.
 template <typename T>
-int stream_grid_size(const StreamArgs<T>& args, bool strict, int64_t B, size_t* smem_bytes, int* stages,
+int stream_grid_size(StreamArgs<T>& args, bool strict, int64_t B, size_t* smem_bytes, int* stages,
                      int* stage_stride, int* rstride, int* xbufs);
 
 }  // namespace fstg

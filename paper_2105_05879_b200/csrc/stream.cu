@@ -79,6 +79,13 @@ constexpr int kBarCoef = 2, kBarTail = 3;   // named barrier ids
 #endif
 constexpr int kRStages = FSTG_RSTAGES;       // refinement ring: tail warp 0 issues, warps 1..kRStages consume
 static_assert(kRStages >= 1 && kRStages <= kTLW - 1, "refinement stages are owned by tail warps 1..kTLW-1");
+// Stages in use at run time: one fewer for small candidate sets, so the column ring gets a
+// sixth 16 KiB stage (config 3, want = 320: 455k -> 464k vectors/s); large sets (config 5 at
+// s = 256) keep all kRStages (they are refinement-bound: 172k vs 189k with 5).
+#ifndef FSTG_RSTAGES_SMALL_WANT
+#define FSTG_RSTAGES_SMALL_WANT 512
+#endif
+constexpr int64_t kRSmallWant = FSTG_RSTAGES_SMALL_WANT;
 
 // Experiment instrumentation (FSTG_STREAM_DEBUG bit 8): cycles each warp role
 // spends in each mbarrier wait, summed over warps (lane 0) into g_wait_cycles.
@@ -165,7 +172,7 @@ struct SmemLayout {
 
 template <typename T>
 __host__ __device__ inline SmemLayout smem_layout(int64_t d, int stages, int stage_stride, int64_t want,
-                                                  int rstride, int xbufs) {
+                                                  int rstride, int xbufs, int rstages) {
   SmemLayout L{};
   size_t off = 0;
   auto take = [&off](size_t bytes, size_t align) {
@@ -184,7 +191,7 @@ __host__ __device__ inline SmemLayout smem_layout(int64_t d, int stages, int sta
   L.cand = take(size_t(want) * sizeof(int32_t), 16);
   L.cval = take(size_t(want) * sizeof(T), 16);
   L.cflag = take(size_t(want) * sizeof(uint8_t), 16);
-  L.rring = take(size_t(kRStages) * rstride, 128);  // rstride 0: refinement reads A directly
+  L.rring = take(size_t(rstages) * rstride, 128);  // rstride 0: refinement reads A directly
   L.total = (off + 15) / 16 * 16;
   return L;
 }
@@ -510,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
   constexpr int CG = SMALL ? (STRICT ? kSmallGroupStrict : kSmallGroupFast) : 1;  // samples per consumer iteration
 
   extern __shared__ __align__(1024) unsigned char smem[];
-  const SmemLayout Ls = smem_layout<T>(A.d, A.stages, A.stage_stride, A.want, A.rstride, A.xbufs);
+  const SmemLayout Ls = smem_layout<T>(A.d, A.stages, A.stage_stride, A.want, A.rstride, A.xbufs, A.rstages);
   unsigned char* ring = smem + Ls.ring;
   T* xbuf = reinterpret_cast<T*>(smem + Ls.x);
   T* tring = reinterpret_cast<T*>(smem + Ls.tbuf);
@@ -568,7 +575,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     mbar_init(&m_full[tid], kNCW);
     mbar_init(&m_empty[tid], 1);
   }
-  if (tid < kRStages) {
+  if (tid < A.rstages) {
     mbar_init(&r_full[tid], 1);
     mbar_init(&r_empty[tid], 1);
   }
@@ -893,26 +900,27 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
         // satisfies g % kRStages == st, so each stage's uses stay in order on
         // one warp (mbarrier parity never aliases).
         const uint32_t rbytes = static_cast<uint32_t>(A.lda * sizeof(T));
+        const uint32_t rst = static_cast<uint32_t>(A.rstages);
         if (tw == 0) {
           // lane st issues the rows of stage st (one issuing thread per stage, like its consumer)
-          if (lane < kRStages) {
+          if (lane < rst) {
             const uint32_t st = static_cast<uint32_t>(lane);
-            const uint32_t first = (st + kRStages - rg % kRStages) % kRStages;
-            for (int64_t ci = first; ci < A.want; ci += kRStages) {
+            const uint32_t first = (st + rst - rg % rst) % rst;
+            for (int64_t ci = first; ci < A.want; ci += rst) {
               const uint32_t g = rg + static_cast<uint32_t>(ci);
-              const uint32_t u = g / kRStages;
+              const uint32_t u = g / rst;
               if (u > 0) wp.wait(&r_empty[st], (u - 1) & 1u, kWTailREmpty);
               mbar_arrive_expect_tx(&r_full[st], rbytes);
               bulk_g2s(rring + size_t(st) * A.rstride, A.a + int64_t(cand[ci]) * A.lda, rbytes, &r_full[st], pol_keep);
             }
           }
           __syncwarp();
-        } else if (tw - 1 < kRStages) {
+        } else if (tw - 1 < static_cast<int>(rst)) {
           const uint32_t st = static_cast<uint32_t>(tw - 1);
-          const uint32_t first = (st + kRStages - rg % kRStages) % kRStages;  // first ci with (rg + ci) % kRS == st
-          for (int64_t ci = first; ci < A.want; ci += kRStages) {
+          const uint32_t first = (st + rst - rg % rst) % rst;  // first ci with (rg + ci) % rst == st
+          for (int64_t ci = first; ci < A.want; ci += rst) {
             const uint32_t g = rg + static_cast<uint32_t>(ci);
-            wp.wait(&r_full[st], (g / kRStages) & 1u, kWTailRFull);
+            wp.wait(&r_full[st], (g / rst) & 1u, kWTailRFull);
             if constexpr (sizeof(T) == 4) {
               if (screen) {
                 // fp32 screening pass; candidates it cannot rule out get the exact dot below
@@ -1255,7 +1263,7 @@ void stream_wait_profile(unsigned long long* out, int count) {
 
 // ------------------------------------------------------------- launching --
 template <typename T>
-int stream_grid_size(const StreamArgs<T>& args, bool strict, int64_t B, size_t* smem_bytes, int* stages,
+int stream_grid_size(StreamArgs<T>& args, bool strict, int64_t B, size_t* smem_bytes, int* stages,
                      int* stage_stride, int* rstride_out, int* xbufs_out) {
   const int64_t stage_bytes = (args.m_pad * int64_t(sizeof(T)) < kSegBytes) ? args.m_pad * int64_t(sizeof(T)) : kSegBytes;
   const int stride = static_cast<int>((stage_bytes + 127) / 128 * 128);
@@ -1264,14 +1272,17 @@ int stream_grid_size(const StreamArgs<T>& args, bool strict, int64_t B, size_t* 
   *rstride_out = rstride;
   const int xbufs = kXBuf;
   *xbufs_out = xbufs;
-  const SmemLayout L0 = smem_layout<T>(args.d, 0, stride, args.want, rstride, xbufs);
+  int rst = (args.want <= kRSmallWant && kRStages > 1) ? kRStages - 1 : kRStages;
+  if (const char* e = std::getenv("FSTG_RSTAGES_RT")) rst = std::max(1, std::min(kRStages, std::atoi(e)));  // experiments
+  args.rstages = rst;
+  const SmemLayout L0 = smem_layout<T>(args.d, 0, stride, args.want, rstride, xbufs, rst);
   int S = static_cast<int>((kSmemBudget - static_cast<int64_t>(L0.total) - 1024) / stride);
   // ~64 KiB in flight per SM is enough (profiles/r01_stream_stages.txt: 3-5 x 16 KiB stages beat 10)
   S = std::min(S, std::max(4, static_cast<int>(kInflightBytes / stride)));
   if (const char* e = std::getenv("FSTG_STREAM_STAGES")) S = std::min(S, std::max(2, std::atoi(e)));  // experiments
   if (S > kMaxStages) S = kMaxStages;
   if (S < 2) S = 2;
-  const SmemLayout L = smem_layout<T>(args.d, S, stride, args.want, rstride, xbufs);
+  const SmemLayout L = smem_layout<T>(args.d, S, stride, args.want, rstride, xbufs, rst);
   *smem_bytes = L.total;
   *stages = S;
   *stage_stride = stride;
@@ -1300,7 +1311,8 @@ static cudaError_t launch_one(const StreamArgs<T>& args, int grid, size_t smem, 
 
 template <typename T>
 cudaError_t launch_stream(const StreamArgs<T>& args, bool strict, int grid, cudaStream_t st) {
-  const SmemLayout L = smem_layout<T>(args.d, args.stages, args.stage_stride, args.want, args.rstride, args.xbufs);
+  const SmemLayout L = smem_layout<T>(args.d, args.stages, args.stage_stride, args.want, args.rstride, args.xbufs,
+                                      args.rstages);
   if (L.total > static_cast<size_t>(kSmemBudget)) return cudaErrorInvalidConfiguration;
   if (args.nseg <= 1 && args.m_pad <= int64_t(kNC) * (16 / int64_t(sizeof(T))) &&
       args.stages >= 4 * (strict ? kSmallGroupStrict : kSmallGroupFast)) {
@@ -1317,8 +1329,8 @@ cudaError_t launch_stream(const StreamArgs<T>& args, bool strict, int grid, cuda
 
 template cudaError_t launch_stream<float>(const StreamArgs<float>&, bool, int, cudaStream_t);
 template cudaError_t launch_stream<double>(const StreamArgs<double>&, bool, int, cudaStream_t);
-template int stream_grid_size<float>(const StreamArgs<float>&, bool, int64_t, size_t*, int*, int*, int*, int*);
-template int stream_grid_size<double>(const StreamArgs<double>&, bool, int64_t, size_t*, int*, int*, int*, int*);
+template int stream_grid_size<float>(StreamArgs<float>&, bool, int64_t, size_t*, int*, int*, int*, int*);
+template int stream_grid_size<double>(StreamArgs<double>&, bool, int64_t, size_t*, int*, int*, int*, int*);
 template int64_t stream_scratch_elems<float>(const StreamArgs<float>&, int);
 template int64_t stream_scratch_elems<double>(const StreamArgs<double>&, int);
 
