@@ -1,6 +1,7 @@
 // C-ABI implementation (include/fst_b200.h): sketch lifetime, batching,
 // host<->device staging and profiling around the sm_100a kernels.
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 
 #include <algorithm>
 #include <atomic>
@@ -31,6 +32,9 @@ struct fstg_sketch {
   int64_t m = 0, n = 0, ldc = 0, lda = 0;
   void* cols = nullptr;
   void* a = nullptr;
+  uint16_t* ab = nullptr;  // fp32 sketches: bf16 (RN) copy of A for the refinement screening, row stride ldab
+  int64_t ldab = 0;
+  float* abn = nullptr;    // |ab row|_2 rounded up (the screening bound)
   uint32_t* qplain = nullptr;
   uint32_t* qtrans = nullptr;
   uint32_t* revtab = nullptr;
@@ -201,6 +205,32 @@ __global__ void finite_check_kernel(const void* a, int dtype, int64_t count, int
   }
 }
 
+// bf16 screening table (stream.cu refine_screen_bf16): ab[i, j] = RN_bf16(a[i, j]), padding zeroed
+__global__ void bf16_table_kernel(const float* __restrict__ a, int64_t lda, int64_t m, int64_t n,
+                                  uint16_t* __restrict__ ab, int64_t ldab) {
+  const int64_t total = m * ldab;
+  for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t i = t / ldab, j = t % ldab;
+    const __nv_bfloat16 h = __float2bfloat16_rn(j < n ? a[i * lda + j] : 0.f);
+    ab[t] = __bfloat16_as_ushort(h);
+  }
+}
+
+// |ab row i|_2 in fp64, rounded up to fp32 (one warp per row)
+__global__ void bf16_row_norms_kernel(const uint16_t* __restrict__ ab, int64_t ldab, int64_t m, float* __restrict__ out) {
+  const int lane = threadIdx.x % 32;
+  for (int64_t i = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) / 32; i < m;
+       i += int64_t(gridDim.x) * blockDim.x / 32) {
+    double s = 0.0;
+    for (int64_t j = lane; j < ldab; j += 32) {
+      const double v = static_cast<double>(__uint_as_float(static_cast<uint32_t>(ab[i * ldab + j]) << 16));
+      s = fma(v, v, s);
+    }
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[i] = __double2float_ru(sqrt(s) * (1.0 + 0x1.0p-40));
+  }
+}
+
 template <typename T>
 __global__ void gather_kernel(const T* __restrict__ cols, int64_t ldc, int64_t m, const int64_t* __restrict__ idx,
                               int64_t count, int64_t L, T* __restrict__ out, int* __restrict__ bad) {
@@ -274,6 +304,31 @@ struct DevBuf {
     return static_cast<U*>(p);
   }
 };
+
+// bf16 screening copy of an fp32 embedded A (32 MiB at n = 4096); built with the sketch
+void build_screen_table(fstg_sketch* sk, cudaStream_t st) {
+  if (sk->dtype != FSTG_F32 || !sk->has_a || sk->a == nullptr || sk->m == 0) return;
+  sk->ldab = round_up(sk->n, 8);
+  const size_t bytes = size_t(sk->m) * size_t(sk->ldab) * 2;
+  cuda_check(cudaMalloc(&sk->ab, bytes), "allocate bf16 screening table");
+  sk->device_bytes += bytes;
+  bf16_table_kernel<<<148 * 4, 256, 0, st>>>(static_cast<const float*>(sk->a), sk->lda, sk->m, sk->n, sk->ab, sk->ldab);
+  cuda_check(cudaGetLastError(), "bf16 screening table");
+  cuda_check(cudaMalloc(&sk->abn, size_t(sk->m) * sizeof(float)), "allocate screening row norms");
+  sk->device_bytes += size_t(sk->m) * sizeof(float);
+  bf16_row_norms_kernel<<<148 * 4, 256, 0, st>>>(sk->ab, sk->ldab, sk->m, sk->abn);
+  cuda_check(cudaGetLastError(), "screening row norms");
+}
+
+// the screening table a transform uses: none when screening is off (FSTG_STREAM_DEBUG bit 16)
+// or for the A/B experiment switch FSTG_NO_BF16_SCREEN
+const uint16_t* screen_table(const fstg_sketch* sk) {
+  const char* dbg = std::getenv("FSTG_STREAM_DEBUG");
+  if (dbg && (std::atoi(dbg) & 16)) return nullptr;
+  const char* off = std::getenv("FSTG_NO_BF16_SCREEN");
+  if (off && std::atoi(off) != 0) return nullptr;
+  return sk->ab;
+}
 
 // ---------------------------------------------------------- preprocess ----
 template <typename T>
@@ -376,6 +431,7 @@ void build_sketch(fstg_sketch* sk, const void* a_in, cudaStream_t st, int64_t b0
   double rn = 0;
   for (double v : h) rn = std::max(rn, v);
   sk->row_norm_max = rn;
+  if constexpr (sizeof(T) == 4) build_screen_table(sk, st);
 }
 
 void destroy_sketch(fstg_sketch* sk) {
@@ -385,6 +441,8 @@ void destroy_sketch(fstg_sketch* sk) {
   cudaSetDevice(sk->device);
   cudaFree(sk->cols);
   cudaFree(sk->a);
+  cudaFree(sk->ab);
+  cudaFree(sk->abn);
   cudaFree(sk->qplain);
   cudaFree(sk->qtrans);
   cudaFree(sk->revtab);
@@ -767,6 +825,7 @@ void load_impl(const char* path, int dtype, int device, void* stream, fstg_sketc
       cuda_check(cudaStreamSynchronize(st), "sync");
       for (double v : hn) rn = std::max(rn, v);
     }
+    if (flag) build_screen_table(sk, st);
     cuda_check(cudaStreamSynchronize(st), "sync");
     sk->row_norm_max = rn;
   } catch (...) {
@@ -874,6 +933,9 @@ void run_batch(const fstg_sketch* sk, const void* X, int64_t B, const fstg_strea
   args.ldc = sk->ldc;
   args.a = static_cast<const T*>(sk->a);
   args.lda = sk->lda;
+  args.ab = screen_table(sk);
+  args.ldab = sk->ldab;
+  args.abn = sk->abn;
   args.qplain = sk->qplain;
   args.qtrans = sk->qtrans;
   args.revtab = sk->revtab;
@@ -1151,6 +1213,9 @@ struct DesignRun {
     keep_pool_warm(sk->device);
     args.a = static_cast<const T*>(sk->a);
     args.lda = sk->lda;
+    args.ab = screen_table(sk);
+    args.ldab = sk->ldab;
+    args.abn = sk->abn;
     args.qplain = sk->qplain;
     args.qtrans = sk->qtrans;
     args.revtab = sk->revtab;

@@ -94,6 +94,12 @@ __device__ __forceinline__ float4 ldg_f4_policy(const float4* p, uint64_t policy
   return v;
 }
 
+__device__ __forceinline__ uint2 ldg_u2_policy(const uint2* p, uint64_t policy) {
+  uint2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(policy));
+  return v;
+}
+
 __device__ __forceinline__ double2 ldg_d2_policy(const double2* p, uint64_t policy) {
   double2 v;
   asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"

@@ -71,6 +71,11 @@ struct StreamArgs {
   int64_t ldc;  // column stride (elements), multiple of 16 bytes
   const T* a;
   int64_t lda;  // row stride of the embedded A (elements), multiple of 16 bytes
+  // fp32 only: bf16 (RN) copy of A for the refinement's screening pass, row stride ldab
+  // (elements, multiple of 8); null = screen on the fp32 rows (or no screening, debug bit 16)
+  const uint16_t* ab;
+  int64_t ldab;
+  const float* abn;  // |ab row i|_2, rounded up (with ab)
   const uint32_t* qplain;
   const uint32_t* qtrans;
   const uint32_t* revtab;
@@ -100,6 +105,7 @@ struct StreamArgs {
   int stage_stride;  // bytes between ring stages (>= one segment, 128-byte multiple)
   int rstride;       // bytes per refinement-ring stage (one row of A); 0 = direct loads
   int rstages;       // refinement-ring stages in use (<= kRStages), set by stream_grid_size
+  int rrows;         // rows per refinement-ring stage (2 for bf16 screening rows), set by stream_grid_size
   int xbufs;         // x buffers in shared memory
   int nseg;
   int chunk;
@@ -119,7 +125,8 @@ struct StreamArgs {
   // experiment switches (env FSTG_STREAM_DEBUG; 0 in production):
   // bit 0: column pipeline only (coefficient warps idle, t = 1)
   // bit 1: coefficient pipeline only (no column loads, consumers skip the ring)
-  // bit 2: no refinement; bit 3: per-role mbarrier wait profile
+  // bit 2: no refinement; bit 3: per-role mbarrier wait profile; bit 4: no screening;
+  // bit 5: no exact dots after screening; bit 6: screening rows loaded but not screened
   int debug;
 };
 enum MeansMode { kMeansFull = 0, kMeansPartial = 1, kMeansTail = 2 };

@@ -70,7 +70,8 @@ constexpr int kSmallGroupFast = FSTG_SMALL_GROUP_FAST, kSmallGroupStrict = FSTG_
 constexpr int kMaxStages = 64;
 // x buffers: coefficients on v+1 while the tail refines v. A third buffer (coefficients two
 // vectors ahead) measured 5% slower at config 3 (profiles/r01_stream_pipeline.txt).
-constexpr int kXBuf = 2;
+constexpr int kXBuf = 3;   // barriers for up to 3; buffers in use: kXBufUse (FSTG_XBUFS for experiments)
+constexpr int kXBufUse = 2;
 constexpr int kSmemBudget = 227 * 1024;
 constexpr int kInflightBytes = 8 * 16384;    // cap on column bytes in flight per SM (shared memory decides)
 constexpr int kBarCoef = 2, kBarTail = 3;   // named barrier ids
@@ -86,6 +87,8 @@ static_assert(kRStages >= 1 && kRStages <= kTLW - 1, "refinement stages are owne
 #define FSTG_RSTAGES_SMALL_WANT 512
 #endif
 constexpr int64_t kRSmallWant = FSTG_RSTAGES_SMALL_WANT;
+// bf16 screening rows per refinement-ring stage (one x pass screens them together)
+constexpr int kRRowsBf16 = 2;
 
 // Experiment instrumentation (FSTG_STREAM_DEBUG bit 8): cycles each warp role
 // spends in each mbarrier wait, summed over warps (lane 0) into g_wait_cycles.
@@ -490,6 +493,103 @@ __device__ __forceinline__ bool refine_screen_f32_global(const float4* a4, const
     s += __shfl_xor_sync(0xffffffffu, s, o);
   }
   return screen_decide(d, s, nv, eps);
+}
+
+// Screening from the bf16 copy of A (fstg_sketch::ab, RN-rounded, 2 bytes per
+// entry: half the refinement's row traffic, an L2-resident table half the size).
+// With a^ = bf16(a): |a_j - a^_j| <= 2^-8 |a^_j| (unit roundoff of an 8-bit
+// significand) + 2^-134 below the normal range. d = fl(a^.x) is evaluated with
+// packed FFMA2 chains of depth k = ceil(nv/32) + 7 (nv = ceil(n/4) four-entry
+// chunks, lane chunks q = lane + 32 i, two packed accumulators), so
+// |d - a^.x| <= gamma_k sum|a^_j x_j|, and by Cauchy-Schwarz
+//   |a.x| <= |d| + (gamma_k + 2^-8) |a^|_2 |x|_2 + 2^-134 |x|_1.
+// |a^_i|_2 is precomputed per row (rounded up, fstg_sketch::abn); |x|_2 and
+// |x|_1 per vector in fp64. |a.x| < eps is PROVEN when
+//   |d| + 1.001 (1.01 (k + 2) 2^-24 + 2^-8) N_i X2 + 2^-125 X1 + 1e-30 < eps
+// (2^-125 also covers subnormal a^_j flushed to zero). No second (|a| |x|)
+// accumulation: one FFMA2 per two entries. Candidates it cannot rule out
+// (support, eps-neighbourhood, NaN / inf) get the exact fp64 dot over the fp32
+// row, so outputs are unchanged.
+struct XNorms {
+  double x2, x1;  // |x|_2, |x|_1 (fp64, all lanes)
+};
+template <typename T>
+__device__ __forceinline__ XNorms warp_x_norms(const T* xs, int64_t n, int lane) {
+  double s2 = 0.0, s1 = 0.0;
+  for (int64_t j = lane; j < n; j += 32) {
+    const double v = static_cast<double>(xs[j]);
+    s2 = fma(v, v, s2);
+    s1 += fabs(v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  return {sqrt(s2), s1};
+}
+__device__ __forceinline__ bool screen_decide_bf16(float d, float rown, const XNorms& xn, int64_t nv, double eps) {
+  const double k = static_cast<double>((nv + 31) / 32) + 7.0;
+  const double bound = 1.001 * (1.01 * (k + 2.0) * 0x1.0p-24 + 0x1.0p-8) * static_cast<double>(rown) * xn.x2 +
+                       0x1.0p-125 * xn.x1 + 1e-30;
+  return !(fabs(static_cast<double>(d)) + bound < eps);  // true: needs the exact dot (NaN included)
+}
+__device__ __forceinline__ float2 bf16x2_f32(uint32_t w) {
+  return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xffff0000u));
+}
+// d += a^[4q .. 4q+3] . x[4q .. 4q+3] on two packed accumulators
+__device__ __forceinline__ void bf16_chunk(uint2 aw, float4 xv, float2& p0, float2& p1) {
+  p0 = __ffma2_rn(bf16x2_f32(aw.x), make_float2(xv.x, xv.y), p0);
+  p1 = __ffma2_rn(bf16x2_f32(aw.y), make_float2(xv.z, xv.w), p1);
+}
+__device__ __forceinline__ float bf16_reduce(float2 p0, float2 p1) {
+  float d = (p0.x + p0.y) + (p1.x + p1.y);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+  return d;
+}
+
+// one bf16 row from the refinement ring
+__device__ __forceinline__ bool refine_screen_bf16(const uint2* a4, const float4* x4, int64_t n, int lane, float rown,
+                                                   const XNorms& xn, double eps) {
+  const int64_t nv = (n + 3) / 4;
+  float2 p0 = make_float2(0.f, 0.f), p1 = p0;
+#pragma unroll 4
+  for (int64_t q = lane; q < nv; q += 32) bf16_chunk(a4[q], x4[q], p0, p1);
+  return screen_decide_bf16(bf16_reduce(p0, p1), rown, xn, nv, eps);
+}
+
+// two bf16 rows of one ring stage screened in one pass over x (half the shared-memory x reads)
+__device__ __forceinline__ void refine_screen_bf16_pair(const uint2* a4, const uint2* b4, const float4* x4, int64_t n,
+                                                        int lane, float rowa, float rowb, const XNorms& xn, double eps,
+                                                        bool& ma, bool& mb) {
+  const int64_t nv = (n + 3) / 4;
+  float2 pa0 = make_float2(0.f, 0.f), pa1 = pa0, pb0 = pa0, pb1 = pa0;
+#pragma unroll 4
+  for (int64_t q = lane; q < nv; q += 32) {
+    const float4 xv = x4[q];
+    bf16_chunk(a4[q], xv, pa0, pa1);
+    bf16_chunk(b4[q], xv, pb0, pb1);
+  }
+  ma = screen_decide_bf16(bf16_reduce(pa0, pa1), rowa, xn, nv, eps);
+  mb = screen_decide_bf16(bf16_reduce(pb0, pb1), rowb, xn, nv, eps);
+}
+
+// the same with the bf16 row read from global memory (rows longer than one ring stage)
+__device__ __forceinline__ bool refine_screen_bf16_global(const uint2* a4, const float4* x4, int64_t n, int lane,
+                                                          float rown, const XNorms& xn, double eps, uint64_t pol_keep) {
+  constexpr int kRB = 8;
+  const int64_t nv = (n + 3) / 4;
+  float2 p0 = make_float2(0.f, 0.f), p1 = p0;
+  for (int64_t q0 = lane; q0 < nv; q0 += 32 * kRB) {
+    uint2 aw[kRB];
+#pragma unroll
+    for (int u = 0; u < kRB; ++u) aw[u] = (q0 + 32 * u < nv) ? ldg_u2_policy(a4 + q0 + 32 * u, pol_keep) : make_uint2(0u, 0u);
+#pragma unroll
+    for (int u = 0; u < kRB; ++u)
+      if (q0 + 32 * u < nv) bf16_chunk(aw[u], x4[q0 + 32 * u], p0, p1);
+  }
+  return screen_decide_bf16(bf16_reduce(p0, p1), rown, xn, nv, eps);
 }
 
 // --------------------------------------------------------------- kernel ----
@@ -899,29 +999,62 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
         // 1 + st owns stage st and takes the rows whose running index g
         // satisfies g % kRStages == st, so each stage's uses stay in order on
         // one warp (mbarrier parity never aliases).
-        const uint32_t rbytes = static_cast<uint32_t>(A.lda * sizeof(T));
+        // fp32 with the bf16 screening table: the ring holds bf16 rows, A.rrows (2) per stage so one
+        // pass over x in shared memory screens both (exact dots re-read the fp32 rows from L2)
+        const bool bf = sizeof(T) == 4 && A.ab != nullptr;
+        const uint32_t rbytes = bf ? static_cast<uint32_t>(A.ldab * 2) : static_cast<uint32_t>(A.lda * sizeof(T));
         const uint32_t rst = static_cast<uint32_t>(A.rstages);
+        const int64_t rps = bf ? A.rrows : 1;            // rows per ring stage (unit)
+        const int64_t nun = (A.want + rps - 1) / rps;    // units of this vector
         if (tw == 0) {
-          // lane st issues the rows of stage st (one issuing thread per stage, like its consumer)
+          // lane st issues the units of stage st (one issuing thread per stage, like its consumer)
           if (lane < rst) {
             const uint32_t st = static_cast<uint32_t>(lane);
             const uint32_t first = (st + rst - rg % rst) % rst;
-            for (int64_t ci = first; ci < A.want; ci += rst) {
-              const uint32_t g = rg + static_cast<uint32_t>(ci);
+            for (int64_t ui = first; ui < nun; ui += rst) {
+              const uint32_t g = rg + static_cast<uint32_t>(ui);
               const uint32_t u = g / rst;
               if (u > 0) wp.wait(&r_empty[st], (u - 1) & 1u, kWTailREmpty);
-              mbar_arrive_expect_tx(&r_full[st], rbytes);
-              bulk_g2s(rring + size_t(st) * A.rstride, A.a + int64_t(cand[ci]) * A.lda, rbytes, &r_full[st], pol_keep);
+              const int64_t r0 = ui * rps, r1 = min(A.want, r0 + rps);
+              mbar_arrive_expect_tx(&r_full[st], rbytes * static_cast<uint32_t>(r1 - r0));
+              for (int64_t ci = r0; ci < r1; ++ci) {
+                const void* src = bf ? static_cast<const void*>(A.ab + int64_t(cand[ci]) * A.ldab)
+                                     : static_cast<const void*>(A.a + int64_t(cand[ci]) * A.lda);
+                bulk_g2s(rring + size_t(st) * A.rstride + size_t(ci - r0) * rbytes, src, rbytes, &r_full[st], pol_keep);
+              }
             }
           }
           __syncwarp();
         } else if (tw - 1 < static_cast<int>(rst)) {
           const uint32_t st = static_cast<uint32_t>(tw - 1);
-          const uint32_t first = (st + rst - rg % rst) % rst;  // first ci with (rg + ci) % rst == st
-          for (int64_t ci = first; ci < A.want; ci += rst) {
-            const uint32_t g = rg + static_cast<uint32_t>(ci);
+          const uint32_t first = (st + rst - rg % rst) % rst;  // first unit with (rg + ui) % rst == st
+          const XNorms xn = bf ? warp_x_norms(xs, A.n, lane) : XNorms{0.0, 0.0};
+          for (int64_t ui = first; ui < nun; ui += rst) {
+            const uint32_t g = rg + static_cast<uint32_t>(ui);
+            const int64_t ci = ui * rps;
             wp.wait(&r_full[st], (g / rst) & 1u, kWTailRFull);
             if constexpr (sizeof(T) == 4) {
+              if (bf) {
+                // bf16 screening pass (refine_screen_bf16); unresolved candidates get the exact dot below
+                const uint2* a0 = reinterpret_cast<const uint2*>(rring + size_t(st) * A.rstride);
+                bool m0 = false, m1 = false;
+                if (A.debug & 64) {
+                  // experiment: row traffic without the screening arithmetic
+                } else if (ci + 1 < A.want && rps == 2)
+                  refine_screen_bf16_pair(a0, reinterpret_cast<const uint2*>(rring + size_t(st) * A.rstride + rbytes),
+                                          reinterpret_cast<const float4*>(xs), A.n, lane, A.abn[cand[ci]],
+                                          A.abn[cand[ci + 1]], xn, A.epsilon, m0, m1);
+                else
+                  m0 = refine_screen_bf16(a0, reinterpret_cast<const float4*>(xs), A.n, lane, A.abn[cand[ci]], xn,
+                                          A.epsilon);
+                __syncwarp();
+                if (lane == 0) {
+                  mbar_arrive(&r_empty[st]);
+                  cflag[ci] = m0 ? 2 : 0;
+                  if (ci + 1 < A.want && rps == 2) cflag[ci + 1] = m1 ? 2 : 0;
+                }
+                continue;
+              }
               if (screen) {
                 // fp32 screening pass; candidates it cannot rule out get the exact dot below
                 const bool maybe = refine_screen_f32(reinterpret_cast<const float4*>(rring + size_t(st) * A.rstride),
@@ -971,12 +1104,16 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
             }
           }
         }
-        rg += static_cast<uint32_t>(A.want);
+        rg += static_cast<uint32_t>(nun);
         if constexpr (sizeof(T) == 4) {
-          if (screen) {
+          if (screen || bf) {
             named_bar_sync(kBarTail, kTL);  // every screening flag is written
             for (int64_t ci = tw; ci < A.want; ci += kTLW) {
               if (cflag[ci] != 2) continue;  // warp-uniform
+              if (A.debug & 32) {  // experiment: no exact dots
+                if (lane == 0) cflag[ci] = 0;
+                continue;
+              }
               const double dot = refine_dot_exact(A.a + int64_t(cand[ci]) * A.lda, xs, A.n, lane, pol_keep);
               if (lane == 0) {
                 cval[ci] = static_cast<T>(dot);
@@ -987,14 +1124,21 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
         }
       } else {
         // rows longer than one stage: direct 16-byte loads from L2
+        const bool bf = sizeof(T) == 4 && A.ab != nullptr;
+        const XNorms xn = bf ? warp_x_norms(xs, A.n, lane) : XNorms{0.0, 0.0};
         for (int64_t ci = tw; ci < A.want; ci += kTLW) {
           const int64_t row = cand[ci];
           const T* arow = A.a + row * A.lda;
           double dot = 0.0, dot2 = 0.0;
           if constexpr (sizeof(T) == 4) {
-            if (screen && !refine_screen_f32_global(reinterpret_cast<const float4*>(arow),
-                                                    reinterpret_cast<const float4*>(xs), A.n, lane, A.epsilon,
-                                                    pol_keep)) {
+            const bool maybe =
+                bf ? refine_screen_bf16_global(reinterpret_cast<const uint2*>(A.ab + row * A.ldab),
+                                               reinterpret_cast<const float4*>(xs), A.n, lane, A.abn[row], xn,
+                                               A.epsilon, pol_keep)
+                   : (!screen || refine_screen_f32_global(reinterpret_cast<const float4*>(arow),
+                                                          reinterpret_cast<const float4*>(xs), A.n, lane, A.epsilon,
+                                                          pol_keep));
+            if (!maybe) {
               if (lane == 0) cflag[ci] = 0;  // proven |a_i . x| < eps
               continue;
             }
@@ -1267,10 +1411,17 @@ int stream_grid_size(StreamArgs<T>& args, bool strict, int64_t B, size_t* smem_b
                      int* stage_stride, int* rstride_out, int* xbufs_out) {
   const int64_t stage_bytes = (args.m_pad * int64_t(sizeof(T)) < kSegBytes) ? args.m_pad * int64_t(sizeof(T)) : kSegBytes;
   const int stride = static_cast<int>((stage_bytes + 127) / 128 * 128);
-  const int64_t row_bytes = args.lda * int64_t(sizeof(T));
-  const int rstride = row_bytes <= kSegBytes ? static_cast<int>((row_bytes + 127) / 128 * 128) : 0;
+  // the refinement ring holds bf16 screening rows when the sketch has them (fp32), two per stage
+  // when they fit (one pass over x screens both)
+  const bool bf = sizeof(T) == 4 && args.ab != nullptr;
+  const int64_t row_bytes = bf ? args.ldab * 2 : args.lda * int64_t(sizeof(T));
+  args.rrows = (bf && 2 * row_bytes <= kSegBytes) ? kRRowsBf16 : 1;
+  if (const char* e = std::getenv("FSTG_RROWS")) args.rrows = bf && 2 * row_bytes <= kSegBytes ? std::max(1, std::min(2, std::atoi(e))) : 1;  // experiments
+  const int64_t unit_bytes = row_bytes * args.rrows;
+  const int rstride = unit_bytes <= kSegBytes ? static_cast<int>((unit_bytes + 127) / 128 * 128) : 0;
   *rstride_out = rstride;
-  const int xbufs = kXBuf;
+  int xbufs = kXBufUse;
+  if (const char* e = std::getenv("FSTG_XBUFS")) xbufs = std::max(1, std::min(kXBuf, std::atoi(e)));  // experiments
   *xbufs_out = xbufs;
   int rst = (args.want <= kRSmallWant && kRStages > 1) ? kRStages - 1 : kRStages;
   if (const char* e = std::getenv("FSTG_RSTAGES_RT")) rst = std::max(1, std::min(kRStages, std::atoi(e)));  // experiments

@@ -263,23 +263,38 @@ def test_m16384_fast_nonsplit_vs_oracle(fst, orc):
     sk.close()
 
 
-def _with_debug(bits, fn):
-    old = os.environ.get("FSTG_STREAM_DEBUG")
-    os.environ["FSTG_STREAM_DEBUG"] = str(bits)
+def _with_env(name, value, fn):
+    old = os.environ.get(name)
+    os.environ[name] = str(value)
     try:
         return fn()
     finally:
         if old is None:
-            os.environ.pop("FSTG_STREAM_DEBUG", None)
+            os.environ.pop(name, None)
         else:
-            os.environ["FSTG_STREAM_DEBUG"] = old
+            os.environ[name] = old
+
+
+def _with_debug(bits, fn):
+    return _with_env("FSTG_STREAM_DEBUG", bits, fn)
+
+
+def _assert_same_outputs(a, b, want):
+    import torch
+    assert torch.equal(a.counts, b.counts)
+    assert torch.equal(a.candidates, b.candidates)
+    cnt = b.counts.cpu().numpy()
+    valid = torch.as_tensor(np.arange(want)[None, :] < cnt[:, None]).cuda()
+    assert torch.equal(a.support[valid], b.support[valid])
+    assert torch.equal(a.values[valid], b.values[valid])
 
 
 def test_refinement_screening_is_output_invariant(fst, c3):
-    """The fp32 screening pass of the refinement (stream.cu refine_screen_f32) only skips the exact
-    fp64 dot for candidates PROVEN below eps: outputs are bit-identical to refining every candidate
-    exactly (FSTG_STREAM_DEBUG bit 16), including at an eps placed exactly on a refined value."""
-    import torch
+    """The screening passes of the refinement only skip the exact fp64 dot for candidates PROVEN
+    below eps: the default bf16-table screening (stream.cu refine_screen_bf16) and the fp32-row
+    screening (refine_screen_f32, FSTG_NO_BF16_SCREEN=1) are bit-identical to refining every
+    candidate exactly (FSTG_STREAM_DEBUG bit 16), including at an eps placed exactly on a refined
+    value."""
     prob, sk, seeds = c3
     for eps in (0.1, None):
         if eps is None:
@@ -290,13 +305,42 @@ def test_refinement_screening_is_output_invariant(fst, c3):
             eps = abs(float(prob.A[i].double() @ prob.X[0].double()))
         p = fst.StreamParams(epsilon=eps, s=32, J=375, K=2)
         scr = fst.transform_batch(sk, prob.X, p, seeds=seeds, candidates=True)
+        f32 = _with_env("FSTG_NO_BF16_SCREEN", 1,
+                        lambda: fst.transform_batch(sk, prob.X, p, seeds=seeds, candidates=True))
         ref = _with_debug(16, lambda: fst.transform_batch(sk, prob.X, p, seeds=seeds, candidates=True))
-        assert torch.equal(scr.counts, ref.counts)
-        assert torch.equal(scr.candidates, ref.candidates)
-        cnt = ref.counts.cpu().numpy()
-        valid = torch.as_tensor(np.arange(320)[None, :] < cnt[:, None]).cuda()
-        assert torch.equal(scr.support[valid], ref.support[valid])
-        assert torch.equal(scr.values[valid], ref.values[valid])
+        _assert_same_outputs(scr, ref, 320)
+        _assert_same_outputs(f32, ref, 320)
+
+
+@pytest.mark.parametrize("n", [4096, 6000])
+def test_bf16_screening_wide_dynamic_range(fst, n):
+    """bf16 screening on a matrix whose rows span ~2^-140 .. 2^60 (subnormal bf16 entries, rows far
+    above and below eps) and eps values at, just above and just below refined magnitudes: outputs
+    equal the exact refinement of every candidate. n = 6000 has 24 KiB rows, so the refinement
+    reads rows from global memory (refine_screen_bf16_global) instead of the ring; its sketch
+    (d = 16384) cannot be materialised, so it runs the design-only transform."""
+    import torch
+    rng = np.random.default_rng(n)
+    m = 512
+    a = rng.standard_normal((m, n)).astype(np.float32) / np.float32(np.sqrt(n))
+    scale = np.ldexp(1.0, rng.integers(-20, 8, size=m)).astype(np.float32)
+    a *= scale[:, None]
+    a[::7, ::3] = np.float32(np.ldexp(1.0, -140))    # fp32 subnormals (bf16 subnormal / zero)
+    a[5, :16] = np.float32(2.0 ** 60)                 # a huge row: never provable, exact dot
+    design = n > 4096
+    sk = (fst.preprocess_design if design else fst.preprocess)(torch.from_numpy(a).cuda())
+    run = fst.transform_design_batch if design else fst.transform_batch
+    B = 300
+    x = rng.standard_normal((B, n)).astype(np.float32)
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    X = torch.from_numpy(x).cuda()
+    seeds = torch.arange(B, dtype=torch.int64, device="cuda") * 7919 + 3
+    v = np.abs(a.astype(np.float64) @ x[0].astype(np.float64))
+    for eps in (1e-3, float(np.sort(v)[-3]), float(np.nextafter(np.sort(v)[-3], 0)), 0.5):
+        p = fst.StreamParams(epsilon=eps, s=8, J=40, K=3, widen=8)
+        scr = run(sk, X, p, seeds=seeds, candidates=True)
+        ref = _with_debug(16, lambda: run(sk, X, p, seeds=seeds, candidates=True))
+        _assert_same_outputs(scr, ref, 64)
 
 
 def test_config3_host_buffers_equal_device_path(fst, c3):
