@@ -50,6 +50,7 @@ constexpr int kWarpCoef = kNCW, kWarpTail = kNCW + kCW, kWarpProd = kNCW + kCW +
 #define FSTG_TRING 64
 #endif
 constexpr int kTRing = FSTG_TRING;          // slots of the coefficient ring
+static_assert((kTRing & (kTRing - 1)) == 0, "coefficient ring: power of two");
 // Samples per coefficient-warp group: one x read from shared memory serves kNS
 // samples (8 vs 4: +8% at config 3, profiles/r01_stream_pipeline.txt; 16 spills).
 #ifndef FSTG_NS
@@ -1241,7 +1242,59 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
     int64_t jb = 0, b = split ? w % A.K : 0;  // position inside the batch, batch index
     const bool cons_fast = (A.debug & 3) == 0 && seg_last_rows == SEG;
     uint32_t tslot = static_cast<uint32_t>(g0 % kTRing), tphase = static_cast<uint32_t>((g0 / kTRing) & 1);
-    for (int64_t j = 0; j < NI;) {
+    bool item_done = false;
+    if constexpr (NSEG == 1 && !SMALL) {
+      if (cons_fast && A.J < (int64_t(1) << 30)) {
+        // Full-height single-segment columns (config 3): a tight per-batch sample loop with
+        // 32-bit counters, the batch end outside it. Per sample: the coefficient and column
+        // waits, the loads, the stage and the coefficient slot released BEFORE the FMAs use the
+        // loaded values (mbarrier.arrive orders the loads), then the updates in j order.
+        const int J = static_cast<int>(A.J), nb = static_cast<int>(NI / A.J);
+        const T Jt = static_cast<T>(A.J);
+        for (int bb = 0; bb < nb; ++bb) {
+          for (int jj = 0; jj < J; ++jj) {
+            wp.wait(&t_full[tslot], tphase, kWConsT);
+            const T t = tring[tslot];
+            wp.wait(&full[stage], phase, kWConsCol);
+            const typename Vec<T>::V* src =
+                reinterpret_cast<const typename Vec<T>::V*>(ring + size_t(stage) * A.stage_stride);
+            T vv[CPT][VEC];
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) Vec<T>::get(src[tid + c * kNC], vv[c]);
+            __syncwarp();
+            if (lane == 0) {
+              mbar_arrive(&empty[stage]);
+              mbar_arrive(&t_empty[tslot]);
+            }
+#pragma unroll
+            for (int c = 0; c < CPT; ++c)
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) accumulate(acc[0][c][e], t, vv[c][e]);
+            if (++stage == S) {
+              stage = 0;
+              phase ^= 1u;
+            }
+            tslot = (tslot + 1) & static_cast<uint32_t>(kTRing - 1);
+            tphase ^= tslot == 0 ? 1u : 0u;
+          }
+          // batch b complete: mean = sum / J (IEEE division, stream.hpp:237)
+          if (b == 0 && su > 0 && !partial) wp.wait(&m_empty[slot], (su - 1) & 1u, kWConsMEmpty);
+          T* mb = means + b * bstride;
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) {
+            const int64_t row0 = int64_t(tid + c * kNC) * VEC;
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+              if (row0 + e < rows_out) mb[row0 + e] = acc[0][c][e] / Jt;
+              acc[0][c][e] = T(0);
+            }
+          }
+          ++b;
+        }
+        item_done = true;
+      }
+    }
+    for (int64_t j = 0; j < NI && !item_done;) {
       bool grouped = false;
       if constexpr (CG > 1) {
         if (jb + CG <= A.J && !(A.debug & 3)) {
