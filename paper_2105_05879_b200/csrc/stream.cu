@@ -170,8 +170,17 @@ struct Vec<double> {
   }
 };
 
+// x widened to fp64 for the exact refinement dots (fp32, d <= 4096, large candidate sets only:
+// the 32 KiB cost two column stages, which is worth it only when the exact dots dominate --
+// config 5 at s = 256, want = 2560: 199k -> 230k vectors/s; at s = 64, want = 640, it loses 5-12%)
+constexpr int64_t kX64MaxD = 4096, kX64MinWant = 1025;
+template <typename T>
+__host__ __device__ inline int64_t x64_elems(int64_t d, int64_t want) {
+  return (sizeof(T) == 4 && d <= kX64MaxD && want >= kX64MinWant) ? (d < 4 ? 4 : d) : 0;
+}
+
 struct SmemLayout {
-  size_t ring, x, tbuf, bars, hist, scan, misc, cand, cval, cflag, rring, total;
+  size_t ring, x, tbuf, bars, hist, scan, misc, cand, cval, cflag, rring, x64, total;
 };
 
 template <typename T>
@@ -196,6 +205,8 @@ __host__ __device__ inline SmemLayout smem_layout(int64_t d, int stages, int sta
   L.cval = take(size_t(want) * sizeof(T), 16);
   L.cflag = take(size_t(want) * sizeof(uint8_t), 16);
   L.rring = take(size_t(rstages) * rstride, 128);  // rstride 0: refinement reads A directly
+  // x widened to fp64 once per vector for the exact refinement dots (x64_elems)
+  L.x64 = take(x64_elems<T>(d, want) * sizeof(double), 16);
   L.total = (off + 15) / 16 * 16;
   return L;
 }
@@ -412,6 +423,38 @@ __device__ __forceinline__ double refine_dot_exact(const float* __restrict__ aro
         acc = fma(static_cast<double>(av[u].y), static_cast<double>(xv4.y), acc);
         acc = fma(static_cast<double>(av[u].z), static_cast<double>(xv4.z), acc);
         acc = fma(static_cast<double>(av[u].w), static_cast<double>(xv4.w), acc);
+      }
+    }
+  }
+  dot += dot2;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  return dot;
+}
+
+// The same dot with x already widened to fp64 in shared memory (one conversion per
+// element instead of two; identical operations and order, so identical values).
+__device__ __forceinline__ double refine_dot_exact_x64(const float* __restrict__ arow, const double* x64, int64_t n,
+                                                       int lane, uint64_t pol_keep) {
+  constexpr int kRB = 4;
+  double dot = 0.0, dot2 = 0.0;
+  const int64_t nv = (n + 3) / 4;
+  const float4* a4 = reinterpret_cast<const float4*>(arow);
+  const double2* x2 = reinterpret_cast<const double2*>(x64);
+  for (int64_t q0 = lane; q0 < nv; q0 += 32 * kRB) {
+    float4 av[kRB];
+#pragma unroll
+    for (int u = 0; u < kRB; ++u)
+      av[u] = (q0 + 32 * u < nv) ? ldg_f4_policy(a4 + q0 + 32 * u, pol_keep) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < kRB; ++u) {
+      if (q0 + 32 * u < nv) {
+        const double2 xa = x2[2 * (q0 + 32 * u)], xb = x2[2 * (q0 + 32 * u) + 1];
+        double& acc = (u & 1) ? dot2 : dot;
+        acc = fma(static_cast<double>(av[u].x), xa.x, acc);
+        acc = fma(static_cast<double>(av[u].y), xa.y, acc);
+        acc = fma(static_cast<double>(av[u].z), xb.x, acc);
+        acc = fma(static_cast<double>(av[u].w), xb.y, acc);
       }
     }
   }
@@ -639,6 +682,7 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
   int32_t* cand = reinterpret_cast<int32_t*>(smem + Ls.cand);
   T* cval = reinterpret_cast<T*>(smem + Ls.cval);
   uint8_t* cflag = reinterpret_cast<uint8_t*>(smem + Ls.cflag);
+  double* x64 = reinterpret_cast<double*>(smem + Ls.x64);
   __shared__ uint32_t wbase[32];
   __shared__ unsigned long long wait_acc[kWSites + 1];
   const long long t_start = kWaitProfile ? clock64() : 0;
@@ -1109,13 +1153,21 @@ __global__ void __launch_bounds__(kThreads, 1) stream_kernel(const StreamArgs<T>
         if constexpr (sizeof(T) == 4) {
           if (screen || bf) {
             named_bar_sync(kBarTail, kTL);  // every screening flag is written
+            const bool wide = x64_elems<T>(A.d, A.want) > 0;
+            if (wide) {
+              // x widened to fp64 once for this vector's exact dots
+              for (int64_t j = ttid; j < x64_elems<T>(A.d, A.want); j += kTL) x64[j] = static_cast<double>(xs[j]);
+              named_bar_sync(kBarTail, kTL);
+            }
             for (int64_t ci = tw; ci < A.want; ci += kTLW) {
               if (cflag[ci] != 2) continue;  // warp-uniform
               if (A.debug & 32) {  // experiment: no exact dots
                 if (lane == 0) cflag[ci] = 0;
                 continue;
               }
-              const double dot = refine_dot_exact(A.a + int64_t(cand[ci]) * A.lda, xs, A.n, lane, pol_keep);
+              const float* arow = reinterpret_cast<const float*>(A.a + int64_t(cand[ci]) * A.lda);
+              const double dot = wide ? refine_dot_exact_x64(arow, x64, A.n, lane, pol_keep)
+                                      : refine_dot_exact(arow, reinterpret_cast<const float*>(xs), A.n, lane, pol_keep);
               if (lane == 0) {
                 cval[ci] = static_cast<T>(dot);
                 cflag[ci] = fabs(dot) >= A.epsilon ? 1 : 0;
