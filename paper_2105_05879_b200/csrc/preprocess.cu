@@ -201,6 +201,43 @@ __global__ void __launch_bounds__(NT) fwht_sketch_kernel(const T* __restrict__ a
   const int r2 = tid % R, q2 = tid / R;
   const int64_t row2 = i0 + r2;
   constexpr int WPB = D >= 32 ? D / 32 : 1;
+  // Small rows (E * sizeof(T) <= 128 B per thread: fp32 k <= 10, fp64 k <= 8): the thread's E
+  // values of A are loaded once and kept in registers for all of the CTA's bases, so the basis
+  // loop issues no global loads (config 2: the per-basis L2 reloads left it latency-bound).
+  constexpr bool CACHE_A = E * sizeof(T) <= 128;
+  T areg[CACHE_A ? E : 1];
+  auto load_row = [&](T (&dst)[E]) {
+    if (row1 < m) {
+      const T* arow = a + row1 * lda;
+      const int64_t pos0 = int64_t(p1) * E;
+      if (pos0 + E <= n && (reinterpret_cast<uintptr_t>(arow + pos0) % 16) == 0) {
+        if constexpr (sizeof(T) == 4) {
+#pragma unroll
+          for (int e = 0; e < E; e += 4) {
+            const float4 f = ldg_f4_policy(reinterpret_cast<const float4*>(arow + pos0 + e), pol_keep);
+            dst[e] = f.x;
+            dst[e + 1] = f.y;
+            dst[e + 2] = f.z;
+            dst[e + 3] = f.w;
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < E; e += 2) {
+            const double2 f = ldg_d2_policy(reinterpret_cast<const double2*>(arow + pos0 + e), pol_keep);
+            dst[e] = f.x;
+            dst[e + 1] = f.y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) dst[e] = (pos0 + e < n) ? arow[pos0 + e] : T(0);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) dst[e] = T(0);
+    }
+  };
+  if constexpr (CACHE_A) load_row(areg);
 
   for (int64_t s = s_first; s < s_last; ++s) {
     if constexpr (RETAIN) {
@@ -216,34 +253,11 @@ __global__ void __launch_bounds__(NT) fwht_sketch_kernel(const T* __restrict__ a
       const int64_t pos0 = int64_t(p1) * E;
       qw[0] = (__ldg(qplain + s * WPB + pos0 / 32) >> (pos0 % 32));
     }
-    if (row1 < m) {
-      const T* arow = a + row1 * lda;
-      const int64_t pos0 = int64_t(p1) * E;
-      if (pos0 + E <= n && (reinterpret_cast<uintptr_t>(arow + pos0) % 16) == 0) {
-        if constexpr (sizeof(T) == 4) {
+    if constexpr (CACHE_A) {
 #pragma unroll
-          for (int e = 0; e < E; e += 4) {
-            const float4 f = ldg_f4_policy(reinterpret_cast<const float4*>(arow + pos0 + e), pol_keep);
-            v[e] = f.x;
-            v[e + 1] = f.y;
-            v[e + 2] = f.z;
-            v[e + 3] = f.w;
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < E; e += 2) {
-            const double2 f = ldg_d2_policy(reinterpret_cast<const double2*>(arow + pos0 + e), pol_keep);
-            v[e] = f.x;
-            v[e + 1] = f.y;
-          }
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < E; ++e) v[e] = (pos0 + e < n) ? arow[pos0 + e] : T(0);
-      }
+      for (int e = 0; e < E; ++e) v[e] = areg[e];
     } else {
-#pragma unroll
-      for (int e = 0; e < E; ++e) v[e] = T(0);
+      load_row(v);
     }
 #pragma unroll
     for (int e = 0; e < E; ++e) {

@@ -87,6 +87,27 @@ def test_preprocess_fp32_bit_exact_vs_float_restatement(fst, orc, m, n):
         assert sk.column(ell).tobytes() == cols[ell].tobytes()
 
 
+@pytest.mark.parametrize("m,n", [(1024, 1024), (100, 1000), (1057, 777)])
+def test_preprocess_fp32_k10_full_height_bit_exact(fst, orc, m, n):
+    """k = 10 fp32 (config 2) runs 32 rows per CTA (full 128-byte column lines): many row tiles,
+    a ragged last tile, zero padding n < d. Whole Kerdock blocks (every row of every column)
+    of 12 spread bases and the identity block, bit-exact vs the float restatement."""
+    a = _rand(m, n, m + n, np.float32)
+    sk = fst.preprocess(a)
+    assert sk.k == 10
+    d = sk.d
+    cols_of = lambda ell: sk.column(ell)  # noqa: E731
+    for s in (0, 1, 2, 31, 64, 127, 200, 255, 256, 400, 510, 511):
+        blk = orc.kerdock_block(a, s, np.float32)          # (d, m): row w = column s*d + w
+        got = np.stack([cols_of(s * d + w) for w in range(d)])
+        assert got.tobytes() == blk.tobytes(), s
+    ref_id = np.sqrt(np.float32(d)) * a.T                    # identity block: sqrt(d) A[:, w]
+    for w in range(0, d, 37):
+        col = cols_of((d // 2) * d + w)
+        want = ref_id[w] if w < n else np.zeros(m, np.float32)
+        assert col.tobytes() == want.astype(np.float32).tobytes(), w
+
+
 def test_preprocess_errors(fst):
     with pytest.raises(ValueError):
         fst.preprocess(np.zeros((0, 4)))
