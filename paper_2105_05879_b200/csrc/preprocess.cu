@@ -19,8 +19,9 @@
 //                      requested column and keeps just those (fstg_sample_columns,
 //                      rows [row0, m) for the row-blocked design transform).
 //  * fwht14_retain_ws_kernel — the k = 14 RETAIN pass (config 4) with warp
-//                      specialisation: butterfly warpgroup + copy warpgroup
-//                      (setmaxnreg), and the retained values of a 4-CTA
+//                      specialisation: two butterfly warpgroups + a copy
+//                      warpgroup that also evaluates the last two stages for
+//                      the requested positions (setmaxnreg), and the retained values of a 4-CTA
 //                      cluster's rows merged into 16-byte column segments
 //                      through distributed shared memory (st.async).
 //  * identity_kernel — column (d/2)*d + w = sqrt(d) * A[:, w] (sketch.hpp:200-208).
@@ -715,18 +716,30 @@ __global__ void __launch_bounds__(TmemCfg<KB>::NT, TmemCfg<KB>::MIN_CTAS) fwht_t
 // ---------------------------------------------------------------------------
 // Warp-specialised k = 14 retain kernel (config 4): the cluster-merged
 // write-back of fwht_tmem_kernel<14, true, CL>, with the request handling moved
-// off the butterfly warps. 256 threads per CTA, one row, CL-CTA clusters:
-//   warpgroup 0 (warps 0-3, setmaxnreg 216): TMEM row -> sign mask -> FWHT
-//     (registers, swizzled shared transpose, registers) -> staged in place
-//     (each thread rewrites the tile words it read, so no barrier before it);
-//   warpgroup 1 (warps 4-7, setmaxnreg 40): record prefetch (cp.async),
-//     st.async pushes of the requested values to the cluster, deferred
-//     16-byte write-back of the receive ring.
-// Hand-over per basis with named barriers: STAGED (id 1: wg0 arrives, wg1
-// syncs) and FREED (id 2: wg1 arrives once it holds its requested values in
-// registers, wg0 syncs before the next transpose overwrites the tile); wg0's own transpose barrier
-// is id 3 (128 threads), wg1's internal barrier id 4. The copy of basis s
-// overlaps the butterflies of basis s + 1.
+// off the butterfly warps. 384 threads per CTA, one row, CL-CTA clusters, two
+// CTAs per SM:
+//   warpgroups 0-1 (256 threads x 64 values, setmaxnreg 96): TMEM row -> sign
+//     mask -> position bits 0-5 in registers -> swizzled shared transpose
+//     (each 64-thread quarter of the row transposes on its own: barriers 5-8)
+//     -> bits 6-11 in registers -> staged in place (each thread rewrites the
+//     tile words it read, so no barrier before it);
+//   warpgroup 2 (setmaxnreg 40): record prefetch (cp.async), the last two
+//     stages (bits 12, 13) for the requested positions only, st.async pushes
+//     of those values to the cluster, deferred 16-byte write-back of the
+//     receive ring:
+//       out(w) = (S0 +- S1) +- (S2 +- S3), S_h = staged[h * 4096 + (w & 4095)],
+//     inner sign = bit 12 of w, outer sign = bit 13 — the same additions in
+//     the same order as stages h = 4096, 8192 of fwht_unnormalized
+//     (fwht.hpp:20-29), so every retained value is bit-identical to the full
+//     transform's.
+// Hand-over per basis with named barriers: STAGED (id 1: butterfly warps
+// arrive, copy warps sync) and FREED (id 2: copy warps arrive once they hold
+// their requested values in registers, butterfly warps sync before the next
+// transpose overwrites the tile); the copy warpgroup's internal barrier is
+// id 4. The copy of basis s overlaps the butterflies of basis s + 1.
+// (Round 2 measured the previous shape — 128 butterfly threads x 128 values,
+// all 14 stages — within 1% of this one, and five ways of overlapping its
+// phases without gain: profiles/r02_k14_retain.txt.)
 __device__ __forceinline__ void named_sync(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -734,21 +747,44 @@ __device__ __forceinline__ void named_arrive(uint32_t id, uint32_t n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+#ifdef FSTG_WS_PROF  // experiments: per-phase cycle counts of one butterfly / copy thread per CTA (tools/prof_k14.py)
+__device__ unsigned long long g_wsprof[16];
+__device__ __forceinline__ long long ws_clock() {
+  long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+  return t;
+}
+#define WS_PROF_BEGIN() long long wsacc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, wst = ws_clock()
+#define WS_T(i)                         \
+  do {                                  \
+    const long long tn_ = ws_clock();   \
+    wsacc[i] += tn_ - wst;              \
+    wst = tn_;                          \
+  } while (0)
+#define WS_PROF_END(base)                                                                              \
+  do {                                                                                                 \
+    if (t0 == 0)                                                                                       \
+      for (int i = 0; i < 8; ++i) atomicAdd(&g_wsprof[(base) + i], static_cast<unsigned long long>(wsacc[i])); \
+  } while (0)
+#else
+#define WS_PROF_BEGIN() do { } while (0)
+#define WS_T(i) do { } while (0)
+#define WS_PROF_END(base) do { } while (0)
+#endif
 // receive-ring depth (4 and 6 slots measured the same, profiles/r01_k14_retain.txt)
 constexpr int kWsSlots = 4;
 constexpr size_t kWsRecvBytes = size_t(kWsSlots) * TmemCfg<14>::RCAP * sizeof(float);
 
 template <int CL>
-__global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
+__global__ void __launch_bounds__(384, 2) fwht14_retain_ws_kernel(
     const float* __restrict__ a, int64_t lda, int64_t m, int64_t n, const uint32_t* __restrict__ qplain,
     int64_t basis_end, int bases_per_cta, float* __restrict__ cols, int64_t ldc, const int64_t* __restrict__ req_start,
     const uint2* __restrict__ req_rec, int64_t row0) {
   using C = TmemCfg<14>;
-  constexpr int E = C::E, D = C::D, WPT = C::WPT, CH = C::CH, SWC = C::SWC;
-  constexpr int WPB = D / 32, RCAP = C::RCAP, SS = kWsSlots, NW1 = 4;
-  constexpr uint32_t DL = 2;  // write-back lag in slot uses (1 / 2 / 3 measured the same)
-  static_assert(DL < SS, "write-back lag below the ring depth");
-  static_assert(C::R == 1 && (CL == 4 || CL == 8), "one row per CTA, 4- or 8-CTA clusters");
+  constexpr int E = 64, HALF = 6, D = C::D, WPT = E / 32, CH = E / 4, SWC = CH - 1, TCOLS = 128;
+  constexpr int WPB = D / 32, RCAP = C::RCAP, SS = kWsSlots, NW1 = 4, NB = 256, NALL = 384;
+  constexpr uint32_t DL = 2;
+  static_assert(DL < SS && (CL == 4 || CL == 8), "write-back lag below the ring depth; 4- or 8-CTA clusters");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* tile = reinterpret_cast<float*>(smem_raw);
   __shared__ uint32_t tmem_base_slot;
@@ -760,8 +796,7 @@ __global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
   __shared__ int rmine[SS];
 
   const int tid = threadIdx.x, warp = tid / 32;
-  const bool wg0 = __shfl_sync(0xffffffffu, tid / 128, 0) == 0;  // warp-uniform by construction (setmaxnreg regions)
-  const int t0 = tid & 127;  // index within the warpgroup
+  const bool bfly = __shfl_sync(0xffffffffu, tid / 128, 0) < 2;  // warp-uniform by construction (setmaxnreg regions)
   const int64_t i0 = row0 + int64_t(blockIdx.x);
   const int64_t s_first = int64_t(blockIdx.y) * bases_per_cta;
   const int64_t s_last = min(basis_end, s_first + bases_per_cta);
@@ -770,11 +805,11 @@ __global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_slot)),
-                 "n"(C::TCOLS)
+                 "n"(TCOLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  for (int64_t j = tid; j <= s_last - s_first; j += 256) rstart[j] = req_start[s_first + j];
+  for (int64_t j = tid; j <= s_last - s_first; j += NALL) rstart[j] = req_start[s_first + j];
   if (tid == 0) {
     for (int i = 0; i < SS; ++i) {
       mbar_init(&full_bar[i], 1);
@@ -792,15 +827,12 @@ __global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
     while (sb < s_last && rs(sb) == rs(sb + 1)) ++sb;
     return sb;
   };
-  auto staged = [&](uint32_t w) -> float {  // inverse of the in-place staging layout
-    const uint32_t e = w / E, q = w % E;
-    return tile[e * E + (q & 3) + 4 * ((q >> 2) ^ (e & SWC))];
-  };
 
-  if (wg0) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 216;" ::: "memory");  // 216 + 40 = 2 x 128 (no spills)
-    const uint32_t taddr = tmem_base_slot + (static_cast<uint32_t>(32 * warp) << 16);
-    const int p1 = t0, q2 = t0;
+  if (bfly) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 96;" ::: "memory");  // 256 x 96 + 128 x 40 <= 384 x 80
+    const uint32_t taddr = tmem_base_slot + (static_cast<uint32_t>(32 * (warp % 4)) << 16) +
+                           static_cast<uint32_t>(E * (warp / 4));
+    const int p1 = tid;  // phase 1: positions p1 * 64 + e
     {
       float v[E];
       const int64_t pos0 = int64_t(p1) * E;
@@ -822,14 +854,21 @@ __global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
       for (int c = 0; c < E / 32; ++c) tmem_st_x32(taddr + 32 * c, v + 32 * c);
       tmem_wait_st();
     }
+    // phase 2: thread (hi2 = tid / 64, lo6 = tid % 64) owns positions hi2 * 4096 + e * 64 + lo6
+    float* const src = tile + (tid >> 6) * (E * E) + (tid & 3);
+    const int cq = (tid & 63) >> 2;
     int64_t s = next_basis(s_first);
     uint32_t qn[WPT];
 #pragma unroll
     for (int w = 0; w < WPT; ++w) qn[w] = (s < s_last) ? __ldg(qplain + s * WPB + WPT * p1 + w) : 0u;
     bool first = true;
+    WS_PROF_BEGIN();
+    const int t0 = tid;  // (phase counters)
+    (void)t0;
     while (s < s_last) {
       const int64_t s_next = next_basis(s + 1);
       float v[E];
+      WS_T(0);
 #pragma unroll
       for (int c = 0; c < E / 32; ++c) tmem_ld_x32(taddr + 32 * c, v + 32 * c);
       uint32_t q[WPT];
@@ -840,12 +879,16 @@ __global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
         for (int w = 0; w < WPT; ++w) qn[w] = __ldg(qplain + s_next * WPB + WPT * p1 + w);
       }
       tmem_wait_ld();
+      WS_T(1);
+      // Kerdock sign mask (sketch.hpp:185): flip the sign bit where Q_s(pos) = 1 (exact)
 #pragma unroll
       for (int e = 0; e < E; ++e)
         v[e] = __uint_as_float(__float_as_uint(v[e]) ^ ((q[e / 32] << (31 - (e % 32))) & 0x80000000u));
-      reg_fwht_f32_packed<C::HALF>(v);
-      if (!first) named_sync(2, 256);  // FREED: the copy warps' reads of the previous staging are done
+      reg_fwht_f32_packed<HALF>(v);  // position bits 0-5
+      WS_T(2);
+      if (!first) named_sync(2, NALL);  // FREED: the copy warps' reads of the previous staging are done
       first = false;
+      WS_T(3);
       {
         float* dst = tile + p1 * E;
 #pragma unroll
@@ -853,19 +896,22 @@ __global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
           *reinterpret_cast<float4*>(dst + 4 * (c ^ (p1 & SWC))) =
               make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
       }
-      named_sync(3, 128);
-      float* src = tile + (q2 & 3);
-      const int cq = q2 >> 2;
+      named_sync(5 + (tid >> 6), 64);  // the quarter's transpose only (two warps)
+      WS_T(4);
 #pragma unroll
       for (int e = 0; e < E; ++e) v[e] = src[e * E + 4 * (cq ^ (e & SWC))];
-      reg_fwht_f32_packed<C::HALF>(v);
+      reg_fwht_f32_packed<HALF>(v);  // position bits 6-11
+      WS_T(5);
 #pragma unroll
-      for (int e = 0; e < E; ++e) src[e * E + 4 * (cq ^ (e & SWC))] = v[e];  // in place
-      named_arrive(1, 256);  // STAGED
+      for (int e = 0; e < E; ++e) src[e * E + 4 * (cq ^ (e & SWC))] = v[e];  // in place (bits 12, 13 left to the copy warps)
+      named_arrive(1, NALL);  // STAGED
+      WS_T(6);
       s = s_next;
     }
+    WS_PROF_END(0);
   } else {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+    const int t0 = tid & 127;
     uint32_t use = 0;
     int buf = 0;
     float* const cout = cols + (cbase - row0);
@@ -876,6 +922,16 @@ __global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
           for (int j = t0; j < cnt; j += 128) cp_async_8(&reqbuf[b * RCAP + j], req_rec + lo + j);
       }
       cp_async_commit();
+    };
+    // transform value at position w: stages 4096 and 8192 over the four staged quarter values
+    auto finish = [&](uint32_t w) -> float {
+      const uint32_t pe = (w >> 6) & 63u, lo6 = w & 63u;
+      const float* b = tile + pe * E + (lo6 & 3u) + 4u * ((lo6 >> 2) ^ (pe & SWC));
+      const float s0 = b[0], s1 = b[4096], s2 = b[8192], s3 = b[12288];
+      const uint32_t n12 = (w << 19) & 0x80000000u, n13 = (w << 18) & 0x80000000u;  // bits 12, 13 as sign flips
+      const float x = s0 + __uint_as_float(__float_as_uint(s1) ^ n12);
+      const float y = s2 + __uint_as_float(__float_as_uint(s3) ^ n12);
+      return x + __uint_as_float(__float_as_uint(y) ^ n13);
     };
     auto drain_use = [&](uint32_t ud) {
       const int slot = static_cast<int>(ud % SS);
@@ -903,10 +959,12 @@ __global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
     };
     int64_t s = next_basis(s_first);
     prefetch(s, 0);
+    WS_PROF_BEGIN();
     while (s < s_last) {
       const int64_t s_next = next_basis(s + 1);
       cp_async_wait_all();
-      named_sync(1, 256);  // STAGED: basis s is in the tile; every copy thread finished basis s - 1
+      named_sync(1, NALL);  // STAGED: basis s is in the tile; every copy thread finished basis s - 1
+      WS_T(0);
       prefetch(s_next, buf ^ 1);
       const int64_t r_lo = rs(s), r_hi = rs(s + 1);
       const int cnt = static_cast<int>(r_hi - r_lo);
@@ -922,17 +980,19 @@ __global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
         }
         for (int jj = t0; jj < mine; jj += 128)
           rslot[slot * (RCAP / CL) + jj] = recs[c0 + jj * CL + static_cast<int>(crank)].y;
-        // all of this thread's staged values of the chunk first (RCAP / 128 = 8 at most) ...
+        // all of this thread's values of the chunk first (RCAP / 128 = 8 at most) ...
         constexpr int U = RCAP / 128;
         float val[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int j = t0 + u * 128;
-          val[u] = j < nc ? staged(recs[c0 + j].x) : 0.f;
+          val[u] = j < nc ? finish(recs[c0 + j].x) : 0.f;
         }
         // ... so the butterfly warps can overwrite the tile while the pushes go out
-        if (c0 + RCAP >= cnt && s_next < s_last) named_arrive(2, 256);  // FREED (last chunk of this basis)
+        if (c0 + RCAP >= cnt && s_next < s_last) named_arrive(2, NALL);  // FREED (last chunk of this basis)
+        WS_T(1);
         if (round >= 1) mbar_wait(&empty_bar[slot], (round - 1) & 1);
+        WS_T(2);
         const uint32_t rbase = smem_u32(recv + slot * RCAP) + 4u * crank, fbar = smem_u32(&full_bar[slot]);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -941,12 +1001,15 @@ __global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
             st_async_f32(rbase + 4u * static_cast<uint32_t>((j / CL) * CL), val[u], static_cast<uint32_t>(j % CL), fbar);
         }
         ++use;
+        WS_T(3);
         if (use > DL) drain_use(use - 1 - DL);
+        WS_T(4);
         if (c0 + RCAP < cnt) named_sync(4, 128);  // next chunk reuses rslot / rmine entries
       }
       buf ^= 1;
       s = s_next;
     }
+    WS_PROF_END(8);
     named_sync(4, 128);  // the last pushes' rslot / rmine entries are visible
     for (uint32_t u = use > DL ? use - DL : 0; u < use; ++u) drain_use(u);
     for (uint32_t u = use > SS ? use - SS : 0; u < use; ++u) mbar_wait(&empty_bar[u % SS], (u / SS) & 1);
@@ -955,7 +1018,7 @@ __global__ void __launch_bounds__(256, 2) fwht14_retain_ws_kernel(
   __syncthreads();
   cluster_sync_all();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_slot), "n"(C::TCOLS) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_slot), "n"(TCOLS) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -1113,7 +1176,7 @@ static cudaError_t launch_fwht_tmem(const float* a, int64_t lda, int64_t m, int6
       if (e != cudaSuccess) return e;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(static_cast<unsigned>((row_tiles + CL - 1) / CL * CL), static_cast<unsigned>(gy));
-      cfg.blockDim = dim3(256);
+      cfg.blockDim = dim3(384);
       cfg.dynamicSmemBytes = C::SMEM + kWsRecvBytes;
       cfg.stream = st;
       cudaLaunchAttribute attr[1];
@@ -1201,3 +1264,11 @@ template cudaError_t launch_row_norms<float>(const float*, int64_t, int64_t, int
 template cudaError_t launch_row_norms<double>(const double*, int64_t, int64_t, int64_t, double*, cudaStream_t);
 
 }  // namespace fstg
+
+#ifdef FSTG_WS_PROF
+extern "C" int fstg_debug_wsprof(unsigned long long* out) {  // experiments only: read and clear the phase counters
+  unsigned long long z[16] = {};
+  if (cudaMemcpyFromSymbol(out, fstg::g_wsprof, sizeof(z)) != cudaSuccess) return 1;
+  return cudaMemcpyToSymbol(fstg::g_wsprof, z, sizeof(z)) == cudaSuccess ? 0 : 1;
+}
+#endif

@@ -38,4 +38,17 @@ for rep in range(3):
     full_ms = ms * 16384 / rows
     print(f"rows={rows} requests={nreq} fwht_ms={ms:.2f} -> full-pass-equivalent {full_ms:.0f} ms, "
           f"{adds / ms / 1e9:.2f} Tadd/s")
+try:  # variant builds with -DFSTG_WS_PROF: per-phase cycles of one butterfly / copy thread per CTA
+    import ctypes
+    fn = fst.lib().fstg_debug_wsprof
+    buf = (ctypes.c_ulonglong * 16)()
+    fn(buf)  # discard the warm-up accumulations
+    fst.sample_columns(sk, idx, out=out)
+    torch.cuda.synchronize()
+    fn(buf)
+    nbr = (d // 2) * rows  # basis-rows of the launch
+    print("wsprof cycles per basis-row: butterfly " + " ".join(f"{buf[i] / nbr:.0f}" for i in range(8))
+          + " | copy " + " ".join(f"{buf[8 + i] / nbr:.0f}" for i in range(8)))
+except AttributeError:
+    pass
 sk.close()
