@@ -67,6 +67,11 @@ def parse():
     return ap.parse_args()
 
 
+# Read-only DRAM ceiling of the stream kernel's access pattern (random 16 KiB columns, several issuing lanes),
+# measured on a B200 with tools/micro/rand_read.cu (profiles/r01_tma_issue.txt: 7,104-7,309 GB/s)
+RANDOM_READ_CEILING_GBS = 7250.0
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -594,6 +599,13 @@ def run_b200(args):
                      "survey_8d": {"bytes_per_vector": bvec, "achieved": achieved_8d, "frac": achieved_8d / peak,
                                    "note": "es*(N*m + want*n + n): counts the L2-served A rows as DRAM bytes"},
                      "per_launch_ms": per_launch_ms, "peak_source": peak_kind,
+                     # `peak` is a copy figure (half reads, half writes, with the bus turnarounds a copy
+                     # pays); this kernel only reads, so on a box with little power capping `frac` can
+                     # pass 1.0. The read-only ceiling of its own access pattern is reported beside it.
+                     "read_ceiling": {"gbs": RANDOM_READ_CEILING_GBS, "frac": achieved / RANDOM_READ_CEILING_GBS,
+                                      "source": "random 16 KiB bulk-copy column reads of a 128 GiB buffer, "
+                                                "tools/micro/rand_read.cu (profiles/r01_tma_issue.txt: "
+                                                "7.1-7.3 TB/s)"},
                      "per_launch_source": ("library CUDA events over the timed region" if profile_in_timed else
                                            "library CUDA events over a second, untimed pass of the same K steps")},
         "kernels_ms": {"stream": stream_ms, "draw": draw_ms, "stream_launches": stream_launches,

@@ -351,6 +351,15 @@ __device__ __forceinline__ void tmem_ld_x32(uint32_t taddr, float* v) {
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, float* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]), "=f"(v[8]),
+        "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+
 // 8-byte cp.async (LDGSTS) for the request-record prefetch
 __device__ __forceinline__ void cp_async_8(void* dst_smem, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
@@ -1022,6 +1031,199 @@ __global__ void __launch_bounds__(384, 2) fwht14_retain_ws_kernel(
 }
 
 // ---------------------------------------------------------------------------
+// k = 12 full-sketch kernel with store warps (config 3 preprocessing): the
+// arithmetic of fwht_tmem_kernel<12, false> (same stages, same order, same
+// bits), but the 64 scattered column stores per thread per basis are issued by
+// a separate warpgroup. In the single-role kernel a warp sits in its 64 stores
+// (four 128-byte lines per warp store, so ~4 L1 tag cycles each; the LSU queue
+// is shallow: lg_throttle) before it can start the next basis, and the store
+// drain (~4.1k cycles per basis per SM) and the butterfly chain (~4.5k) add up.
+// Here the butterfly warps park their phase-2 registers in the free half of
+// tensor memory (tcgen05.st, ~1 KB/clk) and go on; store warp j (lane quadrant
+// j) reads them back 32 columns at a time and replays the stores of butterfly
+// warps j, j + 4, j + 8, j + 12 while the next basis is computed.
+//   warps 0-15 (setmaxnreg 104): TMEM A tile -> sign mask -> FWHT -> TMEM staging
+//   warps 16-19 (setmaxnreg 64): TMEM staging -> st.global (transposed, sketch.hpp:191-196)
+// Named barriers: STAGED (id 1: butterfly warps arrive, store warps sync) and
+// DRAINED (id 2: store warps arrive once the staging half is in their
+// registers, butterfly warps sync before the next tcgen05.st).
+// ---------------------------------------------------------------------------
+template <int CL>
+__global__ void __launch_bounds__(640, 1) fwht12_sketch_ws_kernel(
+    const float* __restrict__ a, int64_t lda, int64_t m, int64_t n, const uint32_t* __restrict__ qplain,
+    int64_t basis_begin, int64_t basis_end, int bases_per_cta, float* __restrict__ cols, int64_t ldc) {
+  using C = TmemCfg<12>;
+  constexpr int E = C::E, R = C::R, RS = C::RS, D = C::D, WPT = C::WPT, CH = C::CH, SWC = C::SWC;
+  constexpr int WPB = D / 32, NB = 512, NALL = 640, TCOLS = 2 * C::TCOLS;
+  static_assert(TCOLS == 512 && E == 64 && R == 8, "A tile and staging fill tensor memory");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float* tile = reinterpret_cast<float*>(smem_raw);
+  __shared__ uint32_t tmem_base_slot;
+  __shared__ __align__(8) uint64_t peer_bar;  // CL > 1: one arrival per CTA of the cluster and basis
+
+  const int tid = threadIdx.x, warp = tid / 32;
+  const bool bfly = __shfl_sync(0xffffffffu, tid / 128, 0) < 4;  // warp-uniform by construction (setmaxnreg regions)
+  const int64_t i0 = int64_t(blockIdx.x) * R;
+  const int64_t s_first = basis_begin + int64_t(blockIdx.y) * bases_per_cta;
+  const int64_t s_last = min(basis_end, s_first + bases_per_cta);
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_slot)),
+                 "n"(TCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (CL > 1 && tid == 0) {
+    mbar_init(&peer_bar, CL);
+    fence_mbar_init();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if constexpr (CL > 1) cluster_sync_all();  // peers' barriers initialised before any remote arrive
+
+  if (bfly) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 104;" ::: "memory");  // 512 x 104 + 128 x 64 = 640 x 96
+    const int r1 = tid / E, p1 = tid % E;
+    const int64_t row1 = i0 + r1;
+    const int r2 = tid % R, q2 = tid / R;
+    const uint32_t taddr = tmem_base_slot + (static_cast<uint32_t>(32 * (warp % 4)) << 16) +
+                           static_cast<uint32_t>(E * (warp / 4));
+    const uint32_t tstage = taddr + C::TCOLS;
+    {
+      float v[E];
+      const int64_t pos0 = int64_t(p1) * E;
+      if (row1 < m && pos0 + E <= n) {
+        const float* arow = a + row1 * lda;
+#pragma unroll
+        for (int e = 0; e < E; e += 4) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(arow + pos0 + e));
+          v[e] = f.x;
+          v[e + 1] = f.y;
+          v[e + 2] = f.z;
+          v[e + 3] = f.w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = (row1 < m && pos0 + e < n) ? a[row1 * lda + pos0 + e] : 0.f;
+      }
+#pragma unroll
+      for (int c = 0; c < E / 32; ++c) tmem_st_x32(taddr + 32 * c, v + 32 * c);
+      tmem_wait_st();
+    }
+    uint32_t qn[WPT];
+#pragma unroll
+    for (int w = 0; w < WPT; ++w) qn[w] = (s_first < s_last) ? __ldg(qplain + s_first * WPB + WPT * p1 + w) : 0u;
+    for (int64_t s = s_first; s < s_last; ++s) {
+      float v[E];
+#pragma unroll
+      for (int c = 0; c < E / 32; ++c) tmem_ld_x32(taddr + 32 * c, v + 32 * c);
+      uint32_t q[WPT];
+#pragma unroll
+      for (int w = 0; w < WPT; ++w) q[w] = qn[w];
+      if (s + 1 < s_last) {
+#pragma unroll
+        for (int w = 0; w < WPT; ++w) qn[w] = __ldg(qplain + (s + 1) * WPB + WPT * p1 + w);
+      }
+      tmem_wait_ld();
+      // Kerdock sign mask (sketch.hpp:185): flip the sign bit where Q_s(pos) = 1 (exact)
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        v[e] = __uint_as_float(__float_as_uint(v[e]) ^ ((q[e / 32] << (31 - (e % 32))) & 0x80000000u));
+#ifndef FSTG_PRE_WS_NOCOMPUTE
+      reg_fwht_f32_packed<C::HALF>(v);  // position bits 0 .. 5
+      named_sync(3, NB);                // previous basis' tile reads done
+      {
+        float* dst = tile + r1 * RS + p1 * E;
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+          *reinterpret_cast<float4*>(dst + 4 * (c ^ (p1 & SWC))) =
+              make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+      }
+      named_sync(3, NB);
+      {
+        const float* src = tile + r2 * RS + (q2 & 3);
+        const int cq = q2 >> 2;
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = src[e * E + 4 * (cq ^ (e & SWC))];
+      }
+      reg_fwht_f32_packed<C::HALF>(v);  // position bits 6 .. 11
+#endif
+      if (s > s_first) {                // DRAINED: the store warps hold the previous basis
+        named_sync(2, NALL);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
+#pragma unroll
+      for (int c = 0; c < E / 32; ++c) tmem_st_x32(tstage + 32 * c, v + 32 * c);
+      tmem_wait_st();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      named_arrive(1, NALL);  // STAGED
+    }
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 64;" ::: "memory");
+    const int j = warp - 16, lane = tid & 31;  // lane quadrant j: butterfly warps j, j + 4, j + 8, j + 12
+    const uint32_t tstage = tmem_base_slot + (static_cast<uint32_t>(32 * j) << 16) + C::TCOLS;
+    const int64_t step = int64_t(E) * ldc;
+    for (int64_t s = s_first; s < s_last; ++s) {
+      named_sync(1, NALL);  // STAGED
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if constexpr (CL > 1) {
+        // The CL CTAs of a cluster hold the 8-row pieces of the same 32 * CL-byte column segments:
+        // start this basis' stores together, so the 32-byte sectors of a segment reach L2 within a
+        // short window and leave it as one DRAM burst (no data is exchanged: relaxed arrivals only).
+        // Uncoupled CTAs drift and the build time becomes bimodal (31 ms or 39-58 ms); pairs give a
+        // steady 32.3 ms; 4-CTA clusters only place on 132 of the 148 SMs (36.5 ms);
+        // profiles/r02_preprocess_storewarps.txt.
+        if (tid == NB)
+          for (int r = 0; r < CL; ++r) mbar_arrive_remote_relaxed(smem_u32(&peer_bar), r);
+        mbar_wait(&peer_bar, static_cast<uint32_t>(s - s_first) & 1u);
+      }
+      // 16 pieces of 16 staged columns (piece p: butterfly warp 4 * (p / 4) + j, its registers
+      // 16 * (p % 4) .. + 15), double-buffered: piece p + 1 is in flight while piece p is stored
+      float vb[2][16];
+      float* ptr = nullptr;
+      const bool live = i0 + (lane % R) < m;  // the replayed thread's row: (32 * w + lane) % 8 = lane % 8
+      tmem_ld_x16(tstage, vb[0]);
+      tmem_wait_ld();
+#pragma unroll
+      for (int p = 0; p < 16; ++p) {
+        const int g = p / 4, c16 = p % 4;
+        if (p + 1 < 16) tmem_ld_x16(tstage + E * ((p + 1) / 4) + 16 * ((p + 1) % 4), vb[(p + 1) & 1]);
+        // the butterfly thread whose registers this lane replays: phase-2 row r2, column group q2
+        if (c16 == 0) {
+          const int tb = 32 * (4 * g + j) + lane;
+          ptr = cols + (s * D + tb / R) * ldc + (i0 + tb % R);
+        }
+#ifndef FSTG_PRE_WS_NOSTORE
+        if (live) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            ptr[0] = vb[p & 1][e];
+            ptr += step;
+            asm volatile("" : "+l"(ptr));
+          }
+        }
+#else
+        if (live && vb[p & 1][0] == 1.2345e-33f) ptr[0] = vb[p & 1][1];
+#endif
+        if (p + 1 < 16) {
+          tmem_wait_ld();
+          if (p + 1 == 15 && s + 1 < s_last) {  // the staging half is in registers: free again
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            named_arrive(2, NALL);  // DRAINED
+          }
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if constexpr (CL > 1) cluster_sync_all();  // no peer arrives on an exited CTA's barrier
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base_slot), "n"(TCOLS) : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // Identity block: column nk*d + w = sqrt(d) * A[:, w] for w < n, zero for
 // n <= w < d. 32x32 tiles transposed through shared memory.
 // ---------------------------------------------------------------------------
@@ -1152,10 +1354,44 @@ static cudaError_t launch_fwht_tmem(const float* a, int64_t lda, int64_t m, int6
   const int64_t row_tiles = (m - row0 + C::R - 1) / C::R;
   // the A tile is reused across bpc bases (TMEM); full sketch: 128 (32/64/128/256 measured
   // 37.5/37.0/36.3/36.8 ms at n = 4096, profiles/r01_preprocess_writepath.txt)
-  int bpc = RETAIN ? C::MAXBPC : 128;
+  bool sketch_ws = false;  // k = 12 full sketch: store-warp kernel (default), 2-CTA clusters
+  int sketch_cl = 2;
+  if constexpr (KB == 12 && !RETAIN) {
+    sketch_ws = row0 == 0;
+    if (const char* ev = std::getenv("FSTG_SKETCH_WS")) sketch_ws = sketch_ws && std::atoi(ev) != 0;  // experiments
+    if (const char* ev = std::getenv("FSTG_SKETCH_CL")) sketch_cl = std::atoi(ev);                    // experiments
+    if (sketch_cl != 2 && sketch_cl != 4) sketch_cl = 1;
+  }
+  // store-warp kernel: 64 bases per CTA (CTAs restart before they drift apart: 32 / 64 / 128 / 512 measured
+  // 33.3 / 32.3 / 31.3-35.3 / 35.1-37.9 ms with CTA pairs); single-role kernel: 128
+  int bpc = RETAIN ? C::MAXBPC : (sketch_ws ? 64 : 128);
+  if (const char* ev = std::getenv("FSTG_SKETCH_BPC")) {  // experiments
+    if (!RETAIN && std::atoi(ev) > 0) bpc = std::atoi(ev);
+  }
   while (bpc > 1 && row_tiles * ((nb + bpc - 1) / bpc) < 148 * 8) bpc /= 2;
   const int64_t gy = (nb + bpc - 1) / bpc;
   if (row_tiles > 0x7fffffff || gy > 65535) return cudaErrorInvalidConfiguration;
+  if constexpr (KB == 12 && !RETAIN) {
+    if (sketch_ws) {
+      const int cl = sketch_cl;
+      auto kw = cl == 4 ? fwht12_sketch_ws_kernel<4> : cl == 2 ? fwht12_sketch_ws_kernel<2> : fwht12_sketch_ws_kernel<1>;
+      e = cudaFuncSetAttribute(kw, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+      if (e != cudaSuccess) return e;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>((row_tiles + cl - 1) / cl * cl), static_cast<unsigned>(gy));
+      cfg.blockDim = dim3(640);
+      cfg.dynamicSmemBytes = C::SMEM;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = static_cast<unsigned>(cl);
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      return cudaLaunchKernelEx(&cfg, kw, a, lda, m, n, qplain, b0, b1, bpc, cols, ldc);
+    }
+  }
   if constexpr (RETAIN && C::R == 1) {
     // cluster-merged write-back (8 rows per cluster): needs the packed records and
     // 16-byte aligned 4-row column segments

@@ -81,7 +81,7 @@ case "$task" in
     what=${1:-stream}
     case "$what" in
       stream) CMD="python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-parity"; K="-k regex:stream_kernel --launch-skip 3 --launch-count 1" ;;
-      fwht)   CMD="python tools/prof_preprocess.py 1024"; K="-k regex:fwht_tmem_kernel --launch-count 1" ;;
+      fwht)   CMD="python tools/prof_preprocess.py 1024"; K="-k regex:fwht --launch-count 1" ;;
       k14)    CMD="python tools/prof_k14.py 256 6144000"; K="-k regex:fwht14 --launch-count 1" ;;
       *) echo "unknown ncu target $what"; exit 2 ;;
     esac
