@@ -18,6 +18,11 @@
 //                      prefetched; RETAIN mode walks only bases holding a
 //                      requested column and keeps just those (fstg_sample_columns,
 //                      rows [row0, m) for the row-blocked design transform).
+//  * fwht12_sketch_ws_kernel — the k = 12 full-sketch build (config 3) with
+//                      store warps: butterfly warps park their results in
+//                      the free half of tensor memory and a fifth warpgroup
+//                      issues the scattered column stores; 2-CTA clusters
+//                      start each basis' stores together.
 //  * fwht14_retain_ws_kernel — the k = 14 RETAIN pass (config 4) with warp
 //                      specialisation: two butterfly warpgroups + a copy
 //                      warpgroup that also evaluates the last two stages for
