@@ -187,6 +187,34 @@ def test_k12_tmem_sketch_full_height_bit_exact(fst, orc, c3):
     assert torch.equal(ident, expect)
 
 
+@pytest.mark.parametrize("m", [4, 100, 264])
+@pytest.mark.parametrize("cl", ["1", "2", "4"])
+def test_k12_store_warp_sketch_variants_bit_identical(fst, orc, m, cl, monkeypatch):
+    """The k = 12 store-warp sketch kernel (results parked in tensor memory, stores replayed by a
+    fifth warpgroup; uncoupled CTAs, CTA pairs (default) and 4-CTA clusters) writes the same bits
+    as the single-role kernel (FSTG_SKETCH_WS=0) and as the float restatement of
+    sketch.hpp:171-196 — with fewer rows than a row tile, a ragged last tile, an odd number of row
+    tiles (the cluster's padding CTA owns no row) and n < d (zero-padded positions)."""
+    import torch
+    from paper_2105_05879_b200 import parallel
+    n = 4000  # pads to d = 4096
+    a32 = np.random.default_rng(31 + m).standard_normal((m, n)).astype(np.float32)
+    monkeypatch.setenv("FSTG_SKETCH_WS", "0")
+    sk0 = fst.preprocess(a32)
+    ref = parallel.sketch_tensor(sk0).view(sk0.L, sk0.column_stride)[:, :m].clone()
+    sk0.close()
+    monkeypatch.setenv("FSTG_SKETCH_WS", "1")
+    monkeypatch.setenv("FSTG_SKETCH_CL", cl)
+    sk = fst.preprocess(a32)
+    got = parallel.sketch_tensor(sk)
+    assert torch.equal(got.view(sk.L, sk.column_stride)[:, :m], ref)
+    d, ldc = sk.d, sk.column_stride
+    for s in (0, 63, 64, 2047):  # first / last basis of a CTA's range
+        blk = got[s * d * ldc:(s + 1) * d * ldc].view(d, ldc)[:, :m].cpu().numpy()
+        assert blk.tobytes() == orc.kerdock_block(a32, s, np.float32).tobytes(), s
+    sk.close()
+
+
 # ------------------------------------------------------- fp64 STRICT n=1024 ----
 def test_fp64_strict_n1024_nonsplit_every_vector(fst, orc):
     from paper_2105_05879_b200 import generators
