@@ -3,6 +3,8 @@
 // W warps per CTA (W % 4 == 0), 1 CTA per SM, 128 TMEM columns per warp-quarter
 // group; each warp repeatedly issues tcgen05.ld.32x32b.x32 (4 KiB per warp-instruction)
 // or tcgen05.st of the same shape. Prints bytes/clk/SM from clock64 of warp 0.
+// (Round 1's version consumed the loaded values with a run-time register index, which
+// put the 128-value buffer in local memory and measured that traffic: ~32 B/clk/SM.)
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -60,7 +62,7 @@ __global__ void __launch_bounds__(W * 32, 1) tmem_kernel(float* out, int iters, 
       }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int k = 0; k < 4; ++k) acc += w[k][(it + k) & 31];
+      for (int k = 0; k < 4; ++k) acc += w[k][0] + w[k][13] + w[k][31];  // static indices: w stays in registers
     }
   }
   if constexpr (STORE) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
