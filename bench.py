@@ -97,9 +97,9 @@ def dram_bytes_per_vector(N, m, n, es=4):
 
 
 # DRAM bytes of one stream-kernel launch of 65,536 config-3 vectors, ncu --set full
-# (dram__bytes_read.sum + dram__bytes_write.sum), profiles/r02_ncu_stream_kernel_bf16.txt
-NCU_STREAM_DRAM_BYTES_65536 = 837.429339e9 + 3.204567e9
-NCU_STREAM_SOURCE = ("profiles/r02_ncu_stream_kernel_bf16.txt (ncu --set full, one 65,536-vector launch, "
+# (dram__bytes_read.sum + dram__bytes_write.sum), profiles/r02_ncu_stream_kernel_final.txt
+NCU_STREAM_DRAM_BYTES_65536 = 837.875902e9 + 3.203679e9
+NCU_STREAM_SOURCE = ("profiles/r02_ncu_stream_kernel_final.txt (ncu --set full, one 65,536-vector launch, "
                      "scaled per vector)")
 
 
