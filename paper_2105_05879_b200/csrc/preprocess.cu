@@ -1064,7 +1064,7 @@ __global__ void __launch_bounds__(640, 1) fwht12_sketch_ws_kernel(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float* tile = reinterpret_cast<float*>(smem_raw);
   __shared__ uint32_t tmem_base_slot;
-  __shared__ __align__(8) uint64_t peer_bar;  // CL > 1: one arrival per CTA of the cluster and basis
+  __shared__ __align__(8) uint64_t peer_bar[2];  // CL > 1: one arrival per CTA of the cluster and basis (even / odd)
 
   const int tid = threadIdx.x, warp = tid / 32;
   const bool bfly = __shfl_sync(0xffffffffu, tid / 128, 0) < 4;  // warp-uniform by construction (setmaxnreg regions)
@@ -1079,7 +1079,8 @@ __global__ void __launch_bounds__(640, 1) fwht12_sketch_ws_kernel(
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (CL > 1 && tid == 0) {
-    mbar_init(&peer_bar, CL);
+    mbar_init(&peer_bar[0], CL);
+    mbar_init(&peer_bar[1], CL);
     fence_mbar_init();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1146,6 +1147,12 @@ __global__ void __launch_bounds__(640, 1) fwht12_sketch_ws_kernel(
               make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
       }
       named_sync(3, NB);
+      if constexpr (CL > 1) {  // "this CTA is half-way through basis s" to every CTA of the cluster (incl. itself)
+        if (tid == 0) {
+          const uint32_t kb = static_cast<uint32_t>(s - s_first);
+          for (int r = 0; r < CL; ++r) mbar_arrive_remote_relaxed(smem_u32(&peer_bar[kb & 1]), r);
+        }
+      }
       {
         const float* src = tile + r2 * RS + (q2 & 3);
         const int cq = q2 >> 2;
@@ -1175,13 +1182,13 @@ __global__ void __launch_bounds__(640, 1) fwht12_sketch_ws_kernel(
       if constexpr (CL > 1) {
         // The CL CTAs of a cluster hold the 8-row pieces of the same 32 * CL-byte column segments:
         // start this basis' stores together, so the 32-byte sectors of a segment reach L2 within a
-        // short window and leave it as one DRAM burst (no data is exchanged: relaxed arrivals only).
-        // Uncoupled CTAs drift and the build time becomes bimodal (31 ms or 39-58 ms); pairs give a
-        // steady 32.3 ms; 4-CTA clusters only place on 132 of the 148 SMs (36.5 ms);
-        // profiles/r02_preprocess_storewarps.txt.
-        if (tid == NB)
-          for (int r = 0; r < CL; ++r) mbar_arrive_remote_relaxed(smem_u32(&peer_bar), r);
-        mbar_wait(&peer_bar, static_cast<uint32_t>(s - s_first) & 1u);
+        // short window and leave it as one DRAM burst (no data is exchanged: relaxed arrivals only,
+        // sent by the butterfly warps half a basis earlier so the hand-shake is off the store path).
+        // Uncoupled CTAs drift and the build time becomes bimodal (31 ms or 39-58 ms); 4-CTA
+        // clusters only place on 132 of the 148 SMs; profiles/r02_preprocess_storewarps.txt.
+        // (Two barriers, even / odd basis: a waiter can never see its barrier wrap a second time.)
+        const uint32_t kb = static_cast<uint32_t>(s - s_first);
+        mbar_wait(&peer_bar[kb & 1], (kb >> 1) & 1u);
       }
       // 16 pieces of 16 staged columns (piece p: butterfly warp 4 * (p / 4) + j, its registers
       // 16 * (p % 4) .. + 15), double-buffered: piece p + 1 is in flight while piece p is stored
@@ -1367,9 +1374,9 @@ static cudaError_t launch_fwht_tmem(const float* a, int64_t lda, int64_t m, int6
     if (const char* ev = std::getenv("FSTG_SKETCH_CL")) sketch_cl = std::atoi(ev);                    // experiments
     if (sketch_cl != 2 && sketch_cl != 4) sketch_cl = 1;
   }
-  // store-warp kernel: 64 bases per CTA (CTAs restart before they drift apart: 32 / 64 / 128 / 512 measured
-  // 33.3 / 32.3 / 31.3-35.3 / 35.1-37.9 ms with CTA pairs); single-role kernel: 128
-  int bpc = RETAIN ? C::MAXBPC : (sketch_ws ? 64 : 128);
+  // 128 bases per CTA for both k = 12 sketch kernels (store-warp kernel with CTA pairs: 32 / 64 / 128 / 256 / 512
+  // measured 32.6 / 31.8 / 31.4 / 31.5 / 31.5 ms, profiles/r02_preprocess_storewarps.txt)
+  int bpc = RETAIN ? C::MAXBPC : 128;
   if (const char* ev = std::getenv("FSTG_SKETCH_BPC")) {  // experiments
     if (!RETAIN && std::atoi(ev) > 0) bpc = std::atoi(ev);
   }
