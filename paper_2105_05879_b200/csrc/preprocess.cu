@@ -737,7 +737,7 @@ __global__ void __launch_bounds__(TmemCfg<KB>::NT, TmemCfg<KB>::MIN_CTAS) fwht_t
 //     (each 64-thread quarter of the row transposes on its own: barriers 5-8)
 //     -> bits 6-11 in registers -> staged in place (each thread rewrites the
 //     tile words it read, so no barrier before it);
-//   warpgroup 2 (setmaxnreg 40): record prefetch (cp.async), the last two
+//   warpgroup 2 (setmaxnreg 48): record prefetch (cp.async), the last two
 //     stages (bits 12, 13) for the requested positions only, st.async pushes
 //     of those values to the cluster, deferred 16-byte write-back of the
 //     receive ring:
@@ -843,7 +843,7 @@ __global__ void __launch_bounds__(384, 2) fwht14_retain_ws_kernel(
   };
 
   if (bfly) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 96;" ::: "memory");  // 256 x 96 + 128 x 40 <= 384 x 80
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 96;" ::: "memory");  // 256 x 96 + 128 x 48 = 384 x 80
     const uint32_t taddr = tmem_base_slot + (static_cast<uint32_t>(32 * (warp % 4)) << 16) +
                            static_cast<uint32_t>(E * (warp / 4));
     const int p1 = tid;  // phase 1: positions p1 * 64 + e
@@ -924,7 +924,7 @@ __global__ void __launch_bounds__(384, 2) fwht14_retain_ws_kernel(
     }
     WS_PROF_END(0);
   } else {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");  // 256 x 96 + 128 x 48 = 384 x 80
     const int t0 = tid & 127;
     uint32_t use = 0;
     int buf = 0;
@@ -937,16 +937,8 @@ __global__ void __launch_bounds__(384, 2) fwht14_retain_ws_kernel(
       }
       cp_async_commit();
     };
-    // transform value at position w: stages 4096 and 8192 over the four staged quarter values
-    auto finish = [&](uint32_t w) -> float {
-      const uint32_t pe = (w >> 6) & 63u, lo6 = w & 63u;
-      const float* b = tile + pe * E + (lo6 & 3u) + 4u * ((lo6 >> 2) ^ (pe & SWC));
-      const float s0 = b[0], s1 = b[4096], s2 = b[8192], s3 = b[12288];
-      const uint32_t n12 = (w << 19) & 0x80000000u, n13 = (w << 18) & 0x80000000u;  // bits 12, 13 as sign flips
-      const float x = s0 + __uint_as_float(__float_as_uint(s1) ^ n12);
-      const float y = s2 + __uint_as_float(__float_as_uint(s3) ^ n12);
-      return x + __uint_as_float(__float_as_uint(y) ^ n13);
-    };
+    // (transform value at position w: stages 4096 and 8192 over the four staged quarter values,
+    //  (S0 +- S1) +- (S2 +- S3), evaluated in the chunk loop below)
     auto drain_use = [&](uint32_t ud) {
       const int slot = static_cast<int>(ud % SS);
       mbar_wait(&full_bar[slot], (ud / SS) & 1);
@@ -977,34 +969,67 @@ __global__ void __launch_bounds__(384, 2) fwht14_retain_ws_kernel(
     while (s < s_last) {
       const int64_t s_next = next_basis(s + 1);
       cp_async_wait_all();
-      named_sync(1, NALL);  // STAGED: basis s is in the tile; every copy thread finished basis s - 1
-      WS_T(0);
-      prefetch(s_next, buf ^ 1);
+      named_sync(4, 128);  // every copy thread finished basis s - 1 and its records of basis s are visible
       const int64_t r_lo = rs(s), r_hi = rs(s + 1);
       const int cnt = static_cast<int>(r_hi - r_lo);
       const uint2* recs = cnt <= RCAP ? reqbuf + buf * RCAP : req_rec + r_lo;
+      // Everything that does not need the tile happens before STAGED: the requested positions of
+      // the first chunk (RCAP / 128 = 8 per thread) are in registers when the tile arrives, so the
+      // stretch between STAGED and FREED — which the butterfly warps wait out before their next
+      // transpose — is the staged reads and three adds per request only.
+      constexpr int U = RCAP / 128;
+      uint32_t wv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int j = t0 + u * 128;
+        wv[u] = j < min(RCAP, cnt) ? recs[j].x : 0u;
+      }
+      named_sync(1, NALL);  // STAGED: basis s is in the tile
+      WS_T(0);
+      prefetch(s_next, buf ^ 1);  // (after FREED instead: spills in the 48-register warps, 118.8 -> 132.9 ms)
       for (int c0 = 0; c0 < cnt; c0 += RCAP) {
         const int nc = min(RCAP, cnt - c0);
         const int slot = static_cast<int>(use % SS);
         const uint32_t round = use / SS;
         const int mine = (nc - static_cast<int>(crank) + CL - 1) / CL;
+        if (c0 > 0) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int j = t0 + u * 128;
+            wv[u] = j < nc ? recs[c0 + j].x : 0u;
+          }
+        }
+        float val[U];
+#pragma unroll
+        for (int h = 0; h < U; h += 4) {  // four requests' staged reads in flight at a time
+          float sv[4][4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t w = wv[h + u], pe = (w >> 6) & 63u, lo6 = w & 63u;
+            const float* b = tile + pe * E + (lo6 & 3u) + 4u * ((lo6 >> 2) ^ (pe & SWC));
+            sv[u][0] = b[0];
+            sv[u][1] = b[4096];
+            sv[u][2] = b[8192];
+            sv[u][3] = b[12288];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const uint32_t w = wv[h + u];
+            const uint32_t n12 = (w << 19) & 0x80000000u, n13 = (w << 18) & 0x80000000u;  // bits 12, 13 as sign flips
+            const float x = sv[u][0] + __uint_as_float(__float_as_uint(sv[u][1]) ^ n12);
+            const float y = sv[u][2] + __uint_as_float(__float_as_uint(sv[u][3]) ^ n12);
+            val[h + u] = x + __uint_as_float(__float_as_uint(y) ^ n13);
+          }
+        }
+        // ... so the butterfly warps can overwrite the tile while the pushes go out
+        if (c0 + RCAP >= cnt && s_next < s_last) named_arrive(2, NALL);  // FREED (last chunk of this basis)
+        WS_T(1);
         if (t0 == 0) {
           mbar_arrive_expect_tx_cta(&full_bar[slot], static_cast<uint32_t>(4 * CL * mine));
           rmine[slot] = mine;
         }
         for (int jj = t0; jj < mine; jj += 128)
           rslot[slot * (RCAP / CL) + jj] = recs[c0 + jj * CL + static_cast<int>(crank)].y;
-        // all of this thread's values of the chunk first (RCAP / 128 = 8 at most) ...
-        constexpr int U = RCAP / 128;
-        float val[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int j = t0 + u * 128;
-          val[u] = j < nc ? finish(recs[c0 + j].x) : 0.f;
-        }
-        // ... so the butterfly warps can overwrite the tile while the pushes go out
-        if (c0 + RCAP >= cnt && s_next < s_last) named_arrive(2, NALL);  // FREED (last chunk of this basis)
-        WS_T(1);
         if (round >= 1) mbar_wait(&empty_bar[slot], (round - 1) & 1);
         WS_T(2);
         const uint32_t rbase = smem_u32(recv + slot * RCAP) + 4u * crank, fbar = smem_u32(&full_bar[slot]);
