@@ -970,6 +970,7 @@ __global__ void __launch_bounds__(384, 2) fwht14_retain_ws_kernel(
       const int64_t s_next = next_basis(s + 1);
       cp_async_wait_all();
       named_sync(4, 128);  // every copy thread finished basis s - 1 and its records of basis s are visible
+      prefetch(s_next, buf ^ 1);  // next basis' records, issued while the tile is still being staged
       const int64_t r_lo = rs(s), r_hi = rs(s + 1);
       const int cnt = static_cast<int>(r_hi - r_lo);
       const uint2* recs = cnt <= RCAP ? reqbuf + buf * RCAP : req_rec + r_lo;
@@ -986,7 +987,6 @@ __global__ void __launch_bounds__(384, 2) fwht14_retain_ws_kernel(
       }
       named_sync(1, NALL);  // STAGED: basis s is in the tile
       WS_T(0);
-      prefetch(s_next, buf ^ 1);  // (after FREED instead: spills in the 48-register warps, 118.8 -> 132.9 ms)
       for (int c0 = 0; c0 < cnt; c0 += RCAP) {
         const int nc = min(RCAP, cnt - c0);
         const int slot = static_cast<int>(use % SS);
